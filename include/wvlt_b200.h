@@ -1,0 +1,129 @@
+/*
+ * wvlt_b200.h -- C ABI of the B200 wavelet tree / wavelet matrix construction path.
+ *
+ * The reference (`wvlt`, Python + numba) has no C ABI: its operator layer is
+ * the set of numba kernels in pkg/src/wvlt/_kernels.py, each of which takes
+ * preallocated arrays, mutates them in place and returns nothing
+ * (_kernels.py:1-13).  The entry points below replace those kernels and the
+ * per-level orchestration in construct.py with sm_100a CUDA, keeping the same
+ * conventions:
+ *
+ *   - every buffer is allocated by the caller (Python/torch or any other host
+ *     runtime); the library never allocates device memory;
+ *   - plain pointers and sizes only, no torch types;
+ *   - everything is stream ordered on the `stream` argument (a cudaStream_t,
+ *     NULL = legacy default stream);
+ *   - return value 0 = success, > 0 = a cudaError_t, < 0 = a WVLT_E* contract
+ *     error.  wvlt_error_string() names both.
+ *
+ * Output layout is the reference's BitVector layout (bitvec.py:3-8): level l
+ * of a build over n symbols is ceil(n/64) uint64 words, bit j at word j>>6,
+ * in-word position j&63 (LSB first), unused high bits of the last word zero.
+ * All levels are packed back to back: level l starts at word l*ceil(n/64).
+ */
+#ifndef WVLT_B200_H
+#define WVLT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define WVLT_ABI_VERSION 1
+
+/* structure kinds, same codes as the wire format (structures.py:24) */
+#define WVLT_KIND_WT 0
+#define WVLT_KIND_WM 1
+
+/* contract errors (negative so they never collide with cudaError_t) */
+#define WVLT_E_ARG (-1)        /* bad argument (null pointer, bad kind, bad sym_bytes, ...) */
+#define WVLT_E_WIDTH (-2)      /* code width above WVLT_MAX_WIDTH */
+#define WVLT_E_WORKSPACE (-3)  /* workspace smaller than wvlt_workspace_bytes() */
+#define WVLT_E_RANGE (-4)      /* a symbol lies outside [0, sigma) (host-buffer entry only) */
+
+/* largest supported code width ceil(lg sigma); the histogram fold chain is 2^(w+1) int64 */
+#define WVLT_MAX_WIDTH 24
+
+/* Bit in *status set by the device build when a symbol lies outside [0, sigma). */
+#define WVLT_STATUS_RANGE 1
+
+int wvlt_abi_version(void);
+const char* wvlt_error_string(int code);
+
+/* ceil(lg sigma), 0 for sigma <= 1.  Replaces bitperm.code_width (bitperm.py:18-22). */
+int wvlt_code_width(int64_t sigma);
+
+/* Device workspace needed by wvlt_build_device for this problem (bytes). */
+size_t wvlt_workspace_bytes(int64_t n, int sym_bytes, int64_t sigma, int kind);
+
+/*
+ * Symbol histogram, padded to 2^width bins, plus the range check.
+ * Replaces hist_and_msb_bits / full_histogram (_kernels.py:23-42) and
+ * levelstats.symbol_histogram (levelstats.py:30-47).
+ *   text      device, n symbols of sym_bytes (1, 2 or 4) bytes, unsigned
+ *   hist      device int64[2^width], overwritten
+ *   status    device int32, WVLT_STATUS_RANGE is OR-ed in on a bad symbol (may be NULL)
+ */
+int wvlt_histogram(const void* text, int sym_bytes, int64_t n, int64_t sigma, int64_t* hist,
+                   int32_t* status, void* stream);
+
+/*
+ * Full device-resident build of one wavelet tree (kind WVLT_KIND_WT) or wavelet
+ * matrix (WVLT_KIND_WM).  Replaces build_by_prefix_counting / build_by_prefix_sorting
+ * (construct.py:292-387) and their kernels hist_and_msb_bits, fold_pairs,
+ * starts_identity, starts_ordered, sort_level_pass, scatter_by_prefix and
+ * write_bits_from_symbols (_kernels.py:23-193).
+ *   text         device, n symbols (sym_bytes = 1, 2 or 4), values must lie in [0, sigma)
+ *   level_words  device uint64[width * ceil(n/64)], fully overwritten
+ *   zeros        device int64[width] or NULL: WM zero counts Z[l] (construct.py:273-288);
+ *                for kind WT the same per-level zero counts are written
+ *   hist         device int64[2^width] or NULL: the padded symbol histogram
+ *   borders      device int64[max(2^width - 2, 0)] or NULL: node borders, level l
+ *                (1 <= l < width) at [2^l - 2, 2^(l+1) - 2), indexed by l-bit prefix.
+ *                WT: interval_starts(fold^(w-l)(hist)) (levelstats.py:58-73);
+ *                WM: the same with bit-reversed order, i.e. wt2wm.interval_start_table
+ *                (wt2wm.py:55-78)
+ *   workspace    device, >= wvlt_workspace_bytes(n, sym_bytes, sigma, kind) bytes
+ *   status       device int32 or NULL; set to 0 then WVLT_STATUS_RANGE on a bad symbol
+ * When status reports a bad symbol the level words are unspecified (the caller
+ * raises, like construct._validated, construct.py:183-187).
+ */
+int wvlt_build_device(const void* text, int sym_bytes, int64_t n, int64_t sigma, int kind,
+                      uint64_t* level_words, int64_t* zeros, int64_t* hist, int64_t* borders,
+                      void* workspace, size_t workspace_bytes, int32_t* status, void* stream);
+
+/*
+ * Same build with HOST input and HOST outputs: copies text host->device,
+ * builds, copies level words / zeros / histogram device->host and synchronizes
+ * `stream`.  Device buffers are caller-provided (dev_text: n*sym_bytes bytes,
+ * dev_level_words: width*ceil(n/64)*8 bytes, dev_small: (2^width + width + 1)*8 bytes).
+ * Host buffers should be page-locked for full copy bandwidth.  host_zeros and
+ * host_hist may be NULL.  Returns WVLT_E_RANGE when a symbol is out of range.
+ * This is the call a reference-side binding (ctypes / cgo / JNI) would make
+ * in place of construct.build_structure (construct.py:150-164).
+ */
+int wvlt_build_host(const void* host_text, int sym_bytes, int64_t n, int64_t sigma, int kind,
+                    uint64_t* host_level_words, int64_t* host_zeros, int64_t* host_hist,
+                    void* dev_text, uint64_t* dev_level_words, void* dev_small,
+                    void* workspace, size_t workspace_bytes, void* stream);
+
+/*
+ * Stream ordered bit intervals into whole destination words: destination bit
+ * range [bounds[t], bounds[t+1]) receives source bits starting at src_starts[t],
+ * for t < ntasks; the tasks tile [0, n_bits).  Writes destination words
+ * [word_lo, word_hi) whole (zero padding included).  Replaces gather_bits
+ * (_kernels.py:196-232), used by the domain-decomposed merge
+ * (construct.py:497-507) -- here the multi-GPU merge -- and by convert_wt_to_wm
+ * (wt2wm.py:225).
+ */
+int wvlt_merge_bits(uint64_t* dst_words, int64_t word_lo, int64_t word_hi, int64_t n_bits,
+                    const int64_t* bounds, const int64_t* src_starts, int64_t ntasks,
+                    const uint64_t* src_words, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* WVLT_B200_H */

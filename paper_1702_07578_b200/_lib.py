@@ -1,0 +1,74 @@
+"""ctypes binding of the in-tree CUDA library (include/wvlt_b200.h).
+
+There is no fallback: if the shared object is missing or cannot be loaded
+this raises, and every build entry point raises with it.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import re
+from pathlib import Path
+
+_PKG = Path(__file__).resolve().parent
+LIB_PATH = _PKG / "_wvlt_b200.so"
+HEADER = _PKG.parent / "include" / "wvlt_b200.h"
+
+KIND_WT = 0
+KIND_WM = 1
+KINDS = {"wt": KIND_WT, "wm": KIND_WM}
+E_ARG, E_WIDTH, E_WORKSPACE, E_RANGE = -1, -2, -3, -4
+STATUS_RANGE = 1
+MAX_WIDTH = 24
+
+_lib = None
+
+
+class WvltError(RuntimeError):
+    """A CUDA or contract error reported by the C ABI."""
+
+
+def load():
+    """Load the library; raises if it is absent (no CPU fallback exists)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LIB_PATH.exists():
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(nvcc, sm_100a); the wavelet construction path has no CPU fallback"
+        )
+    L = ctypes.CDLL(str(LIB_PATH))
+    i64, i32, vp, sz = ctypes.c_int64, ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t
+    L.wvlt_abi_version.argtypes = []
+    L.wvlt_abi_version.restype = i32
+    L.wvlt_error_string.argtypes = [i32]
+    L.wvlt_error_string.restype = ctypes.c_char_p
+    L.wvlt_code_width.argtypes = [i64]
+    L.wvlt_code_width.restype = i32
+    L.wvlt_workspace_bytes.argtypes = [i64, i32, i64, i32]
+    L.wvlt_workspace_bytes.restype = sz
+    L.wvlt_histogram.argtypes = [vp, i32, i64, i64, vp, vp, vp]
+    L.wvlt_histogram.restype = i32
+    L.wvlt_build_device.argtypes = [vp, i32, i64, i64, i32, vp, vp, vp, vp, vp, sz, vp, vp]
+    L.wvlt_build_device.restype = i32
+    L.wvlt_build_host.argtypes = [vp, i32, i64, i64, i32, vp, vp, vp, vp, vp, vp, vp, sz, vp]
+    L.wvlt_build_host.restype = i32
+    L.wvlt_merge_bits.argtypes = [vp, i64, i64, i64, vp, vp, i64, vp, vp]
+    L.wvlt_merge_bits.restype = i32
+    if L.wvlt_abi_version() != 1:
+        raise ImportError("wvlt_b200 ABI version mismatch")
+    _lib = L
+    return L
+
+
+def check(rc: int) -> None:
+    if rc:
+        msg = load().wvlt_error_string(rc).decode()
+        raise WvltError(f"{msg} (code {rc})")
+
+
+def declared_symbols() -> list[str]:
+    """Function names declared in include/wvlt_b200.h (the ABI contract)."""
+    text = HEADER.read_text()
+    return re.findall(r"^\s*(?:const\s+)?[A-Za-z_][A-Za-z0-9_]*\s*\*?\s*(wvlt_[a-z0-9_]+)\s*\(", text, re.M)

@@ -1,0 +1,191 @@
+"""Device-resident construction through the C ABI (include/wvlt_b200.h).
+
+PyTorch is used only for plumbing: device buffers (caching allocator), the
+current CUDA stream and host<->device copies.  All arithmetic runs in the
+hand-written sm_100a kernels of ``csrc/wvlt_b200.cu``.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .bitperm import code_width
+
+_TORCH = None
+
+
+def _torch():
+    global _TORCH
+    if _TORCH is None:
+        import torch
+
+        _TORCH = torch
+    return _TORCH
+
+
+def sym_dtype_for_sigma(sigma: int):
+    """Narrowest unsigned storage for symbols of [0, sigma) (cli._min_dtype, cli.py:59-66)."""
+    if sigma <= 1 << 8:
+        return np.uint8
+    if sigma <= 1 << 16:
+        return np.uint16
+    return np.uint32
+
+
+_TORCH_SYM = {1: "uint8", 2: "uint16", 4: "uint32"}
+
+
+@dataclass
+class DeviceBuild:
+    """One device-resident build.  Tensors live on the build's device."""
+
+    kind: str
+    n: int
+    sigma: int
+    width: int
+    level_words: object  # torch.int64 [width, ceil(n/64)] (bit pattern = uint64 words)
+    zeros: object        # torch.int64 [width]
+    hist: object         # torch.int64 [2^width]
+    borders: object      # torch.int64 [2^width - 2] or None
+
+    def to_host(self):
+        """(level_words uint64 ndarray, zeros list, hist ndarray) after a device->host copy."""
+        lw = self.level_words.cpu().numpy().view(np.uint64)
+        zeros = [int(z) for z in self.zeros.cpu().tolist()] if self.width else []
+        return lw, zeros, self.hist.cpu().numpy()
+
+
+class DeviceBuilder:
+    """Builds wavelet trees / matrices on one CUDA device, reusing a workspace."""
+
+    def __init__(self, device=None):
+        torch = _torch()
+        self.lib = _lib.load()
+        if not torch.cuda.is_available():
+            raise RuntimeError("the wavelet construction path needs a CUDA device (no CPU fallback)")
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        self._ws = None
+
+    # -- buffers -------------------------------------------------------------
+    def workspace(self, n: int, sym_bytes: int, sigma: int, kind: str):
+        torch = _torch()
+        need = int(self.lib.wvlt_workspace_bytes(int(n), int(sym_bytes), int(sigma), _lib.KINDS[kind]))
+        if need == 0 and code_width(sigma) > _lib.MAX_WIDTH:
+            raise ValueError(f"alphabet size {sigma} exceeds the supported code width {_lib.MAX_WIDTH}")
+        if self._ws is None or self._ws.numel() < need:
+            self._ws = torch.empty(max(need, 256), dtype=torch.uint8, device=self.device)
+        return self._ws, need
+
+    def alloc_outputs(self, n: int, sigma: int, borders: bool = False):
+        torch = _torch()
+        w = code_width(sigma)
+        nwords = (n + 63) >> 6
+        lw = torch.empty((w, nwords), dtype=torch.int64, device=self.device)
+        zeros = torch.empty(max(w, 1), dtype=torch.int64, device=self.device)[:w]
+        hist = torch.empty(1 << w, dtype=torch.int64, device=self.device)
+        bd = torch.empty(max((1 << w) - 2, 1), dtype=torch.int64, device=self.device) if borders and w >= 2 else None
+        status = torch.empty(1, dtype=torch.int32, device=self.device)
+        return lw, zeros, hist, bd, status
+
+    # -- builds --------------------------------------------------------------
+    def build(self, text, sigma: int, kind: str = "wm", *, borders: bool = False, outputs=None,
+              stream=None, check: bool = True) -> DeviceBuild:
+        """Build from a device tensor of uint8/uint16/uint32 symbols in [0, sigma).
+
+        ``outputs`` may pass preallocated (level_words, zeros, hist, borders, status)
+        from ``alloc_outputs`` (the benchmark does, to time the build alone).
+        With ``check`` the range status is read back (one device->host sync) and
+        a bad symbol raises ValueError like construct._validated (construct.py:183-187).
+        """
+        torch = _torch()
+        if kind not in _lib.KINDS:
+            raise ValueError(f"unknown structure kind {kind!r}")
+        if text.device.type != "cuda":
+            raise ValueError("DeviceBuilder.build expects a CUDA tensor")
+        if text.dim() != 1:
+            raise ValueError("text must be one-dimensional")
+        sb = text.element_size()
+        if text.dtype not in (torch.uint8, torch.uint16, torch.uint32) or sb not in (1, 2, 4):
+            raise ValueError("device text must be uint8, uint16 or uint32")
+        if not text.is_contiguous():
+            text = text.contiguous()
+        sigma = int(sigma)
+        if sigma < 1:
+            raise ValueError("alphabet size must be at least 1")
+        n = int(text.numel())
+        w = code_width(sigma)
+        if w > _lib.MAX_WIDTH:
+            raise ValueError(f"alphabet size {sigma} exceeds the supported code width {_lib.MAX_WIDTH}")
+        if outputs is None:
+            outputs = self.alloc_outputs(n, sigma, borders)
+        lw, zeros, hist, bd, status = outputs
+        ws, need = self.workspace(n, sb, sigma, kind)
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        rc = self.lib.wvlt_build_device(
+            text.data_ptr() if n else None, sb, n, sigma, _lib.KINDS[kind],
+            lw.data_ptr() if lw.numel() else None, zeros.data_ptr() if w else None, hist.data_ptr(),
+            bd.data_ptr() if bd is not None else None, ws.data_ptr(), need, status.data_ptr(), s.cuda_stream)
+        _lib.check(rc)
+        if check and int(status.item()) & _lib.STATUS_RANGE:
+            raise ValueError(f"symbols must lie in [0, {sigma})")
+        return DeviceBuild(kind, n, sigma, w, lw, zeros, hist, bd)
+
+    def build_host(self, arr: np.ndarray, sigma: int, kind: str, *, out_words: np.ndarray | None = None,
+                   stream=None):
+        """Host buffers in and out through wvlt_build_host (H2D, build, D2H, sync).
+
+        ``arr`` is a contiguous uint8/uint16/uint32 host array (page-locked for
+        full PCIe bandwidth).  Returns (level_words uint64[w, ceil(n/64)], zeros, hist).
+        """
+        torch = _torch()
+        if arr.dtype not in (np.uint8, np.uint16, np.uint32) or not arr.flags.c_contiguous:
+            raise ValueError("host text must be a contiguous uint8/uint16/uint32 array")
+        n = int(arr.size)
+        sb = arr.dtype.itemsize
+        w = code_width(sigma)
+        nwords = (n + 63) >> 6
+        if out_words is None:
+            out_words = np.empty((w, nwords), dtype=np.uint64)
+        zeros = np.zeros(max(w, 1), dtype=np.int64)
+        hist = np.zeros(1 << w, dtype=np.int64)
+        dev_text = torch.empty(max(n * sb, 16), dtype=torch.uint8, device=self.device)
+        dev_words = torch.empty(max(w * nwords, 1), dtype=torch.int64, device=self.device)
+        dev_small = torch.empty((1 << w) + w + 1, dtype=torch.int64, device=self.device)
+        ws, need = self.workspace(n, sb, sigma, kind)
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        rc = self.lib.wvlt_build_host(
+            arr.ctypes.data if n else None, sb, n, sigma, _lib.KINDS[kind],
+            out_words.ctypes.data if out_words.size else None, zeros.ctypes.data, hist.ctypes.data,
+            dev_text.data_ptr(), dev_words.data_ptr(), dev_small.data_ptr(), ws.data_ptr(), need, s.cuda_stream)
+        if rc == _lib.E_RANGE:
+            raise ValueError(f"symbols must lie in [0, {sigma})")
+        _lib.check(rc)
+        return out_words, [int(z) for z in zeros[:w]], hist
+
+    def merge_bits(self, dst_words, word_lo: int, word_hi: int, n_bits: int, bounds, src_starts, src_words,
+                   stream=None) -> None:
+        """gather_bits (_kernels.py:196-232) on device tensors (int64 views of uint64 words)."""
+        torch = _torch()
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        ntasks = int(bounds.numel()) - 1
+        rc = self.lib.wvlt_merge_bits(dst_words.data_ptr(), int(word_lo), int(word_hi), int(n_bits),
+                                      bounds.data_ptr() if ntasks > 0 else None,
+                                      src_starts.data_ptr() if ntasks > 0 else None, max(ntasks, 0),
+                                      src_words.data_ptr() if src_words.numel() else None, s.cuda_stream)
+        _lib.check(rc)
+
+
+_BUILDERS: dict = {}
+
+
+def default_builder(device=None) -> DeviceBuilder:
+    torch = _torch()
+    key = str(device) if device is not None else f"cuda:{torch.cuda.current_device()}" if torch.cuda.is_available() else "cuda"
+    b = _BUILDERS.get(key)
+    if b is None:
+        b = DeviceBuilder(device)
+        _BUILDERS[key] = b
+    return b

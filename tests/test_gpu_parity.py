@@ -1,0 +1,166 @@
+"""Parity of the CUDA path against the oracle and the reference's golden vectors.
+
+Every build here goes through the product API / C ABI on the GPU; the oracle
+(oracle/) and tests/golden (produced by the reference) are the checkers.
+Integer path: bit-exact equality of the wire-format bytes is required.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_1702_07578_b200 as wv
+from conftest import EXAMPLE_SIGMA, EXAMPLE_TEXT, SIGMA_GRID, dtype_for, golden, golden_cases, random_text
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover - CPU container
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+CASES = golden_cases()
+
+
+def ref_dump(text, sigma, kind):
+    words, zeros, _ = oracle.build(text, sigma, kind, "pc")
+    return oracle.dump(kind, int(np.asarray(text).size), max(int(sigma), 1), words, zeros)
+
+
+@pytest.mark.parametrize("kind", ["wt", "wm"])
+def test_golden_cases_bit_exact(kind):
+    g = golden()
+    for ci, n, sigma, dist in CASES:
+        st = wv.build_structure(g[f"text_{ci}"], sigma, kind)
+        assert wv.dump_structure(st) == g[f"dump_{kind}_{ci}"].tobytes(), (ci, n, sigma, dist)
+
+
+def test_running_example():
+    wt = wv.build_structure(EXAMPLE_TEXT, EXAMPLE_SIGMA, "wt")
+    wm = wv.build_structure(EXAMPLE_TEXT, EXAMPLE_SIGMA, "wm")
+    assert tuple(int(v.words[0]) for v in wt.levels) == (0x16C, 0x278, 0x136)
+    assert tuple(int(v.words[0]) for v in wm.levels) == (0x16C, 0x278, 0x14E)
+    assert wm.zeros == [5, 5, 5]
+
+
+@pytest.mark.parametrize("kind", ["wt", "wm"])
+@pytest.mark.parametrize("sigma", SIGMA_GRID + (4, 256, 1000, 1 << 16, 1 << 20))
+def test_tile_boundaries_vs_oracle(kind, sigma):
+    rng = np.random.default_rng(sigma * 7 + (kind == "wm"))
+    for n in (1, 31, 32, 33, 63, 64, 65, 4095, 4096, 4097, 8191, 8192, 8193, 16383, 16384, 16385, 40961,
+              int(rng.integers(100_000, 300_000))):
+        text = random_text(rng, n, sigma)
+        assert wv.dump_structure(wv.build_structure(text, sigma, kind)) == ref_dump(text, sigma, kind), (n, sigma)
+
+
+@pytest.mark.parametrize("kind", ["wt", "wm"])
+def test_distributions_vs_oracle(kind):
+    """Skewed / clustered inputs: Zipf heavy hitters, long runs (tiles inside one
+    node and tiles spanning many nodes), sorted, few distinct symbols."""
+    rng = np.random.default_rng(11)
+    for sigma in (5, 256, 1000, 70000, 1 << 20):
+        n = 200_003
+        dt = dtype_for(sigma)
+        ranks = rng.zipf(1.1, n) % sigma
+        perm = rng.permutation(sigma)
+        texts = {
+            "zipf": perm[ranks].astype(dt),
+            "runs": np.repeat(rng.integers(0, sigma, 200), rng.integers(1, 2000, 200))[:n].astype(dt),
+            "sorted": np.sort(rng.integers(0, sigma, n)).astype(dt),
+            "sparse": rng.choice(rng.choice(sigma, min(sigma, 3), replace=False), n).astype(dt),
+            "const": np.full(n, sigma - 1, dtype=dt),
+        }
+        for name, text in texts.items():
+            assert wv.dump_structure(wv.build_structure(text, sigma, kind)) == ref_dump(text, sigma, kind), (
+                sigma, name)
+
+
+def test_input_dtypes_and_layouts(rng):
+    # test_construct.py:64-72: list, int32, uint64, strided, plus wider-than-needed storage
+    base = random_text(rng, 5000, 16)
+    ref = ref_dump(base, 16, "wt")
+    assert wv.dump_structure(wv.build_by_prefix_counting(list(map(int, base)), 16, "wt")) == ref
+    for dt in (np.int32, np.uint64, np.uint16, np.uint32, np.int64):
+        assert wv.dump_structure(wv.build_by_prefix_counting(base.astype(dt), 16, "wt")) == ref, dt
+    strided = np.repeat(base, 2)[::2]
+    assert wv.dump_structure(wv.build_by_prefix_counting(strided, 16, "wt")) == ref
+    # u8 storage with a wide alphabet
+    small = random_text(rng, 9000, 256)
+    assert wv.dump_structure(wv.build_structure(small, 70000, "wm")) == ref_dump(small, 70000, "wm")
+    assert wv.dump_structure(wv.build_structure(small, 70000, "wt")) == ref_dump(small, 70000, "wt")
+
+
+def test_every_algorithm_and_thread_count_is_identical(rng):
+    # test_construct.py:43-51
+    for sigma in (2, 16, 70000):
+        text = random_text(rng, int(rng.integers(500, 30000)), sigma)
+        for kind in ("wt", "wm"):
+            ref = ref_dump(text, sigma, kind)
+            for algo in wv.ALGORITHMS:
+                for p in (1, 3, 8):
+                    assert wv.dump_structure(wv.build_structure(text, sigma, kind, algo, p)) == ref
+
+
+def test_out_of_range_symbols_raise(rng):
+    for sigma, dt in ((5, np.uint8), (200, np.uint8), (1000, np.uint16), (70000, np.uint32), (256, np.uint16)):
+        text = random_text(rng, 100_000, sigma).astype(dt)
+        text[77_777] = sigma
+        with pytest.raises(ValueError):
+            wv.build_structure(text, sigma, "wm")
+        with pytest.raises(ValueError):
+            wv.build_structure(text, sigma, "wt")
+
+
+def test_histogram_zeros_and_borders_vs_oracle(rng):
+    from paper_1702_07578_b200.device import default_builder
+
+    b = default_builder()
+    for sigma in (3, 5, 256, 1000, 70000):
+        text = random_text(rng, 300_000, sigma)
+        t = torch.from_numpy(text).cuda()
+        hist = oracle.histogram(text, sigma)
+        w = wv.code_width(sigma)
+        for kind in ("wt", "wm"):
+            res = b.build(t, sigma, kind, borders=True)
+            words, zeros, h = res.to_host()
+            assert np.array_equal(h, hist)
+            _, ozeros, _ = oracle.build(text, sigma, "wm", "pc")
+            assert zeros == ozeros
+            if w >= 2:
+                assert np.array_equal(res.borders.cpu().numpy()[: (1 << w) - 2], oracle.borders(hist, w, kind))
+
+
+def test_merge_bits_vs_reference_golden():
+    from paper_1702_07578_b200.device import default_builder
+
+    b = default_builder()
+    g = golden()
+    for gi in range(6):
+        nbits = int(g[f"gather_{gi}_nbits"][0])
+        nw = (nbits + 63) >> 6
+        dst = torch.full((nw,), -1, dtype=torch.int64, device="cuda")
+        src = torch.from_numpy(g[f"gather_{gi}_src"].view(np.int64)).cuda()
+        b.merge_bits(dst, 0, nw, nbits, torch.from_numpy(g[f"gather_{gi}_bounds"]).cuda(),
+                     torch.from_numpy(g[f"gather_{gi}_starts"]).cuda(), src)
+        assert np.array_equal(dst.cpu().numpy().view(np.uint64), g[f"gather_{gi}_dst"]), gi
+
+
+def test_device_builds_are_deterministic(rng):
+    from paper_1702_07578_b200.device import default_builder
+
+    b = default_builder()
+    text = torch.from_numpy(random_text(rng, 3_000_000, 256)).cuda()
+    for kind in ("wt", "wm"):
+        a = b.build(text, 256, kind).level_words.clone()
+        for _ in range(3):
+            assert torch.equal(b.build(text, 256, kind).level_words, a)
+
+
+@pytest.mark.slow
+def test_config_c1_vs_oracle():
+    """c1: n=2^20 uint8 sigma=256 uniform (BASELINE.json configs[0])."""
+    rng = np.random.default_rng(0x574C54)
+    text = rng.integers(0, 256, 1 << 20, dtype=np.uint8)
+    for kind in ("wt", "wm"):
+        assert wv.dump_structure(wv.build_structure(text, 256, kind)) == ref_dump(text, 256, kind)
