@@ -1,0 +1,358 @@
+"""Benchmark: WT/WM construction throughput on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2]
+
+One step = one full wavelet-matrix build of configs[1] (c2: n=2^30 uint8,
+sigma=256, Zipf(1.1)) with the text already resident in HBM: histogram (K1),
+tables (K2) and the fused level passes (K3), output level words + zero counts.
+Prints one JSON line (rank 0).
+
+``value``     whole-job symbols/s of the device-resident build, CUDA events on
+              the launch stream, max over ranks.
+``e2e``       the same metric through the reference-facing C-ABI call
+              wvlt_build_host with pinned HOST buffers: H2D of the text, build,
+              D2H of all level words + zeros + histogram, inside the timed region.
+``roofline``  the dominant kernel (longest stage, from per-stage CUDA events):
+              algorithmic bytes / its average duration vs MEASURED_PEAKS.json.
+``cpu_baseline`` the oracle's port of the reference ps builder
+              (construct.py:322-387) on all host cores over a bounded sample.
+``--impl reference`` times that CPU path alone (rank 0; other ranks exit 0).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "WT+WM build input symbols/sec (n=2^30, σ=256) and % of HBM bytes-moved roofline"
+UNIT = "symbols/s"
+KMAX = 4
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def code_width(sigma: int) -> int:
+    return max(sigma - 1, 0).bit_length()
+
+
+def pass_plan(n: int, sym_bytes: int, sigma: int, kind: str):
+    """Mirror of make_plan() in csrc/wvlt_b200.cu: (level, K, in_bytes, out_bytes) per pass."""
+    w = code_width(sigma)
+    vbits = 8 * sym_bytes
+    bb = lambda b: 1 if b <= 8 else 2 if b <= 16 else 4  # noqa: E731
+    out, ell = [], 0
+    while ell < w:
+        K = min(KMAX, w - ell)
+        live_in = (w - ell) if kind == "wm" else w
+        live_out = (w - ell - K) if kind == "wm" else w
+        ib = sym_bytes if ell == 0 else bb(min(live_in, vbits))
+        ob = bb(min(live_out, vbits)) if ell + K < w else 0
+        out.append((ell, K, ib, min(ob, ib)))
+        ell += K
+    return out
+
+
+def stage_bytes(name: str, n: int, sym_bytes: int, sigma: int, kind: str) -> float:
+    """Algorithmic bytes a stage must move."""
+    w = code_width(sigma)
+    if name == "hist":
+        return n * sym_bytes
+    if name == "memset":
+        return w * ((n + 63) // 64) * 8
+    if name.startswith("pass"):
+        ell, K, ib, ob = pass_plan(n, sym_bytes, sigma, kind)[int(name[4:])]
+        return n * ib + n * ob + K * ((n + 63) // 64) * 8
+    return 0.0
+
+
+def metric_bytes(n: int, sym_bytes: int, sigma: int) -> float:
+    """B = L (n s + 8 ceil(n/64)), text read once per level + level bits."""
+    w = code_width(sigma)
+    return w * (n * sym_bytes + 8 * ((n + 63) // 64))
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        time.sleep(0.15)
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            time.sleep(0.15)
+            self.proc.terminate()
+            out, _ = self.proc.communicate(timeout=10)
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+        return False
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in getattr(self, "lines", []):
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, flag in zip(names, parts[2:6]):
+                if flag.lower() == "active":
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        return os.cpu_count() or 1
+
+
+def cpu_baseline(text_host: np.ndarray, sigma: int, kind: str, sample: int, runs: int = 3):
+    """Oracle port of the reference ps builder on all host cores over text[:sample]."""
+    import oracle
+
+    threads = cpu_threads()
+    piece = np.ascontiguousarray(text_host[:sample])
+    oracle.build(piece[: 1 << 16], sigma, kind, "ps", threads)  # warm-up
+    times = []
+    for _ in range(runs):
+        t0 = time.perf_counter()
+        oracle.build(piece, sigma, kind, "ps", threads)
+        times.append(time.perf_counter() - t0)
+    t = statistics.median(times)
+    return {"value": piece.size / t, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"first {piece.size} symbols of the same {kind.upper()} text, oracle ps "
+                      f"(restatement of construct.py:322-387) with {threads} POSIX threads, median of {runs}",
+            "seconds_per_build": t}
+
+
+def run_reference(args):
+    """--impl reference: the reference's CPU path (oracle port, all host threads)."""
+    import torch
+    import workloads
+
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    cfg = workloads.CONFIGS[args.config]
+    sample = min(cfg["n"], args.cpu_sample)
+    text = workloads.generate(args.config, device="cuda" if torch.cuda.is_available() else "cpu", n=sample)
+    host = text.cpu().numpy()
+    kind = args.kind or cfg["kind"]
+    for _ in range(args.warmup):
+        cpu_baseline(host, cfg["sigma"], kind, min(sample, 1 << 20), runs=1)
+    times = []
+    for _ in range(args.steps):
+        r = cpu_baseline(host, cfg["sigma"], kind, sample, runs=1)
+        times.append(r["seconds_per_build"])
+    t = sum(times) / len(times)
+    value = sample / t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u8" if cfg["dtype"] == torch.uint8 else str(cfg["dtype"]),
+        "data": "synthetic", "config": {"workload": args.config, "description": workloads.DESCRIPTIONS[args.config],
+                                         "kind": kind, "n": sample, "sigma": cfg["sigma"]},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cpu_threads(), "kind": "port",
+                         "sample": f"first {sample} symbols per step (bounded sample of the {args.config} text); "
+                                   "oracle ps = restatement of the reference ps builder, all host threads"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--kind", default=None, choices=[None, "wt", "wm"])
+    ap.add_argument("--cpu-sample", type=int, default=1 << 28)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-wt", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    import workloads
+    from paper_1702_07578_b200 import _lib
+    from paper_1702_07578_b200.device import DeviceBuilder
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    cfg = workloads.CONFIGS[args.config]
+    kind = args.kind or cfg["kind"]
+    sigma, n = cfg["sigma"], cfg["n"]
+    sym_bytes = torch.empty(0, dtype=cfg["dtype"]).element_size()
+    # weak scaling: every rank builds its own n-symbol shard of the job
+    text = workloads.generate(args.config, device=dev, seed=workloads.SEED + 101 * rank)
+    builder = DeviceBuilder(dev)
+    outs = builder.alloc_outputs(n, sigma)
+    stream = torch.cuda.current_stream(dev)
+    npass = len(pass_plan(n, sym_bytes, sigma, kind))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def timed(kind_, steps, warmup):
+        for _ in range(warmup):
+            builder.build(text, sigma, kind_, outputs=outs, check=False)
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            builder.build(text, sigma, kind_, outputs=outs, check=False)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        ms = e0.elapsed_time(e1) / steps
+        if world > 1:
+            t = torch.tensor([ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    # correctness gate on the benchmark input: range status must be clean
+    builder.build(text, sigma, kind, outputs=outs, check=True)
+
+    with ClockSampler(local) as clk:
+        ms = timed(kind, args.steps, args.warmup)
+    clocks = clk.summary()
+
+    # per-stage profile (separate loop; events between stages)
+    _lib.profile_enable(True)
+    stage_ms: dict[str, list[float]] = {}
+    for _ in range(max(3, min(args.steps, 5))):
+        builder.build(text, sigma, kind, outputs=outs, check=False)
+        for name, t in _lib.profile_read():
+            stage_ms.setdefault(name, []).append(t)
+    _lib.profile_enable(False)
+    stages = {k: statistics.median(v) for k, v in stage_ms.items()}
+    dominant = max((k for k in stages if k != "memset"), key=lambda k: stages[k])
+    peak, peak_src = peaks()
+    dom_bytes = stage_bytes(dominant, n, sym_bytes, sigma, kind)
+    achieved = dom_bytes / (stages[dominant] * 1e-3) / 1e9
+    traffic = None
+    tf = ROOT / "profiles" / f"ncu_traffic_{args.config}_{kind}.json"
+    if tf.exists():
+        traffic = json.loads(tf.read_text()).get(dominant)
+
+    value = world * n / (ms * 1e-3)
+    mbytes = metric_bytes(n, sym_bytes, sigma)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": {1: "u8", 2: "u16", 4: "u32"}[sym_bytes], "data": "synthetic",
+        "config": {"workload": args.config, "description": workloads.DESCRIPTIONS[args.config], "kind": kind,
+                   "n_per_gpu": n, "sigma": sigma, "levels": code_width(sigma), "passes": npass,
+                   "l2": "inputs larger than L2 (text %d MiB per GPU vs 126 MB L2); no flush" % (n * sym_bytes >> 20),
+                   "parallelism": f"replicas{world}" if world > 1 else "single"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "kernel": dominant, "kernel_ms": stages[dominant],
+                     "algorithmic_bytes": dom_bytes, "peak_source": peak_src},
+        "metric_roofline": {"bytes_per_build": mbytes, "achieved_gbs": mbytes / (ms * 1e-3) / 1e9,
+                            "frac": mbytes / (ms * 1e-3) / 1e9 / peak,
+                            "definition": "SURVEY 8d: B = L (n s + n/8), text read once per level + level bits"},
+        "stages_ms": stages,
+        "clocks": clocks,
+        "gpu_launches": args.steps * (2 + npass),
+    }
+
+    if not args.no_wt and kind == "wm":
+        wt_ms = timed("wt", max(3, args.steps // 2), 2)
+        line["wt"] = {"value": world * n / (wt_ms * 1e-3), "unit": UNIT, "ms_per_step": wt_ms,
+                      "metric_roofline_frac": mbytes / (wt_ms * 1e-3) / 1e9 / peak}
+
+    if not args.no_e2e:
+        host = torch.empty(n, dtype=cfg["dtype"], pin_memory=True)
+        host.copy_(text)
+        w = code_width(sigma)
+        nwords = (n + 63) // 64
+        host_words = torch.empty((w, nwords), dtype=torch.int64, pin_memory=True)
+        harr = host.numpy()
+        hwords = host_words.numpy().view(np.uint64)
+        builder.build_host(harr, sigma, kind, out_words=hwords)  # warm-up
+        e2e_steps = max(2, min(args.steps, 5))
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            builder.build_host(harr, sigma, kind, out_words=hwords)
+        dt = (time.perf_counter() - t0) / e2e_steps
+        if world > 1:
+            t = torch.tensor([dt], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+        line["e2e"] = {"value": world * n / dt, "unit": UNIT, "ms_per_step": dt * 1e3,
+                       "h2d_bytes_per_step": n * sym_bytes,
+                       "d2h_bytes_per_step": w * nwords * 8 + w * 8 + (1 << w) * 8 + 4,
+                       "path": "wvlt_build_host (C ABI) with page-locked host buffers"}
+        line["gpu_launches"] += e2e_steps * (2 + npass)
+
+    if not args.no_cpu and rank == 0:
+        host_np = text[: min(n, args.cpu_sample)].cpu().numpy()
+        line["cpu_baseline"] = cpu_baseline(host_np, sigma, kind, min(n, args.cpu_sample))
+        line["cpu_baseline"].pop("seconds_per_build", None)
+
+    if rank == 0:
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

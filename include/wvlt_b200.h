@@ -122,6 +122,22 @@ int wvlt_merge_bits(uint64_t* dst_words, int64_t word_lo, int64_t word_hi, int64
                     const int64_t* bounds, const int64_t* src_starts, int64_t ntasks,
                     const uint64_t* src_words, void* stream);
 
+/*
+ * Optional per-stage timing (CUDA events on the build stream) of the calling
+ * thread's wvlt_build_device calls.  Stage ids: WVLT_STAGE_MEMSET (output and
+ * look-back reset), WVLT_STAGE_HIST (K1), WVLT_STAGE_TABLES (K2),
+ * WVLT_STAGE_SCAN0 + p (tile-prefix scan of pass p), WVLT_STAGE_PASS0 + p
+ * (fused level pass p).  wvlt_profile_read synchronizes
+ * on the last event and returns the number of stages written.
+ */
+#define WVLT_STAGE_MEMSET 0
+#define WVLT_STAGE_HIST 1
+#define WVLT_STAGE_TABLES 2
+#define WVLT_STAGE_PASS0 3
+#define WVLT_STAGE_SCAN0 64
+int wvlt_profile_enable(int on);
+int wvlt_profile_read(float* stage_ms, int* stage_ids, int max_stages);
+
 #ifdef __cplusplus
 }
 #endif

@@ -20,6 +20,7 @@ KINDS = {"wt": KIND_WT, "wm": KIND_WM}
 E_ARG, E_WIDTH, E_WORKSPACE, E_RANGE = -1, -2, -3, -4
 STATUS_RANGE = 1
 MAX_WIDTH = 24
+STAGE_MEMSET, STAGE_HIST, STAGE_TABLES, STAGE_PASS0, STAGE_SCAN0 = 0, 1, 2, 3, 64
 
 _lib = None
 
@@ -56,6 +57,10 @@ def load():
     L.wvlt_build_host.restype = i32
     L.wvlt_merge_bits.argtypes = [vp, i64, i64, i64, vp, vp, i64, vp, vp]
     L.wvlt_merge_bits.restype = i32
+    L.wvlt_profile_enable.argtypes = [i32]
+    L.wvlt_profile_enable.restype = i32
+    L.wvlt_profile_read.argtypes = [vp, vp, i32]
+    L.wvlt_profile_read.restype = i32
     if L.wvlt_abi_version() != 1:
         raise ImportError("wvlt_b200 ABI version mismatch")
     _lib = L
@@ -66,6 +71,26 @@ def check(rc: int) -> None:
     if rc:
         msg = load().wvlt_error_string(rc).decode()
         raise WvltError(f"{msg} (code {rc})")
+
+
+def profile_enable(on: bool) -> None:
+    load().wvlt_profile_enable(1 if on else 0)
+
+
+def profile_read(max_stages: int = 40) -> list[tuple[str, float]]:
+    """[(stage name, ms)] of the last profiled wvlt_build_device on this thread."""
+    ms = (ctypes.c_float * max_stages)()
+    ids = (ctypes.c_int * max_stages)()
+    k = load().wvlt_profile_read(ms, ids, max_stages)
+    if k < 0:
+        raise WvltError(f"profile read failed ({k})")
+    names = {STAGE_MEMSET: "memset", STAGE_HIST: "hist", STAGE_TABLES: "tables"}
+    def name(i):
+        if i in names:
+            return names[i]
+        return f"scan{i - STAGE_SCAN0}" if i >= STAGE_SCAN0 else f"pass{i - STAGE_PASS0}"
+
+    return [(name(ids[i]), float(ms[i])) for i in range(k)]
 
 
 def declared_symbols() -> list[str]:

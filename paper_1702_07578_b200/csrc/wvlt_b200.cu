@@ -4,34 +4,38 @@
 // (pkg/src/wvlt/construct.py:242-387, kernels in pkg/src/wvlt/_kernels.py).
 // This file re-designs that hot path for B200:
 //
-//   K1  symbol histogram + range check, one read of the text
+//   K1  symbol histogram + range check, one read of the text; it also counts,
+//       per tile of the first level pass, the digits that pass splits on
 //       (replaces hist_and_msb_bits / full_histogram, _kernels.py:23-42)
 //   K2  one small kernel deriving every table from that histogram: the fold
 //       chain (fold_pairs, _kernels.py:45-49), per-level zero counts
 //       (construct.py:238-239,273-288), node borders (starts_identity /
 //       starts_ordered, _kernels.py:52-72) and the per-pass placement tables
+//   S   per pass, an exclusive scan of the per-tile digit counts over tiles
+//       (the interleaved (prefix, core) scan of levelstats.py:76-137 with
+//       cores -> tiles)
 //   K3  fused level pass: K levels per read of the current symbol order.  A
-//       tile of the order is staged in shared memory, split stably by one bit
-//       per level (the wavelet-matrix refinement, structures.py:176-182),
-//       every level's bits are taken with __ballot_sync in the tile-local
-//       order, tile offsets come from one single-pass decoupled look-back over
-//       the 2^K digit counts, and the bits are emitted as aligned 64-bit words
-//       (replaces sort_level_pass / scatter_by_prefix / write_bits_from_symbols,
-//       _kernels.py:146-193).  The order after K levels is written back to HBM
-//       narrowed to the bits still live.
+//       tile is staged in shared memory and split stably by one bit per level
+//       (the wavelet-matrix refinement, structures.py:176-182); every level's
+//       bits are taken with __ballot_sync in the tile-local order and emitted
+//       as aligned 64-bit words at their global place; the order after K
+//       levels is scattered to HBM narrowed to the bits still live, counting
+//       the next pass's digits on the way (replaces sort_level_pass /
+//       scatter_by_prefix / write_bits_from_symbols, _kernels.py:146-193).
+//       Tiles never wait on each other: their digit prefixes are known at start.
 //   K5  bit-interval shift-merge (replaces gather_bits, _kernels.py:196-232).
 //
-// Position algebra (derivation in DESIGN.md §3).  Let A_l be the level-l
-// order, b_i(v) the i-th code bit of v (MSB first) and, for a pass starting at
-// level l, d_j(v) = sum_{i<j} b_{l+i}(v) << i (an LSD digit).  Then
+// Position algebra.  Let A_l be the level-l order,
+// b_i(v) the i-th code bit of v (MSB first) and, for a pass starting at level
+// l, d_j(v) = sum_{i<j} b_{l+i}(v) << i (an LSD digit).  Then
 //   WM: A_{l+j} = stable sort of A_l by d_j, so
 //       pos_{l+j}(x) = G_j[d] + C_j[d](x)
 //   WT: A_{l+j} = stable sort of A_l by the (l+j)-bit prefix P, and
 //       pos_{l+j}(x) = corr_j[P] + C_j[d](x)
-// where C_j[d](x) counts symbols of A_l before x with digit d (tile look-back
-// prefix + rank inside the tile), G_j is the exclusive scan of the global
-// digit counts and corr_j[P] = wtstart_{l+j}[P] - sum_{q'<q} cnt_{l+j}[q'2^j+e]
-// for P = q 2^j + e.  Both tables come from the histogram alone (K2).
+// where C_j[d](x) counts symbols of A_l before x with digit d (tile prefix +
+// rank inside the tile), G_j is the exclusive scan of the global digit counts
+// and corr_j[P] = wtstart_{l+j}[P] - sum_{q'<q} cnt_{l+j}[q'2^j+e] for
+// P = q 2^j + e.  Both tables come from the histogram alone (K2).
 
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -56,16 +60,6 @@ __device__ __forceinline__ unsigned lanemask_lt() {
   return m;
 }
 
-__device__ __forceinline__ uint64_t ld_relaxed_u64(const uint64_t* p) {
-  uint64_t v;
-  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-
-__device__ __forceinline__ void st_relaxed_u64(uint64_t* p, uint64_t v) {
-  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-
 template <typename T>
 __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll
@@ -73,99 +67,136 @@ __device__ __forceinline__ T warp_sum(T v) {
   return v;
 }
 
-__device__ __forceinline__ unsigned rev_bits(unsigned d, int j) {  // j >= 1
+__host__ __device__ __forceinline__ unsigned rev_bits(unsigned d, int j) {  // j >= 1
+#ifdef __CUDA_ARCH__
   return __brev(d) >> (32 - j);
+#else
+  unsigned r = 0;
+  for (int i = 0; i < j; ++i) r |= ((d >> i) & 1u) << (j - 1 - i);
+  return r;
+#endif
 }
 
-// look-back status word: [63:62] state (1 aggregate, 2 inclusive), [61:42] epoch, [41:0] value
-constexpr uint64_t ST_VALUE_MASK = (1ull << 42) - 1;
-__device__ __forceinline__ uint64_t pack_status(unsigned state, unsigned epoch, uint64_t v) {
-  return ((uint64_t)state << 62) | ((uint64_t)(epoch & 0xFFFFFu) << 42) | (v & ST_VALUE_MASK);
-}
-__device__ __forceinline__ unsigned status_state(uint64_t s, unsigned epoch) {
-  return (((s >> 42) & 0xFFFFFu) == (epoch & 0xFFFFFu)) ? (unsigned)(s >> 62) : 0u;
+__device__ __forceinline__ void bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
 // ---------------------------------------------------------------------------
-// K1: histogram.  Byte texts with width <= 8 use a bit-sliced counter: per
-// 32-symbol warp chunk, one ballot per code bit, and lane b counts bins
-// b + 32i as popc of the AND of the matching ballots (no shared-memory
-// atomics, no contention on Zipf heavy hitters).
+// K1: histogram + first-pass tile digit counts.  Byte texts with width <= 8:
+// one warp per tile; every lane owns a private column of 16-bit counters in
+// shared memory (two bins per 32-bit word at (v >> 1) * 32 + lane, so a
+// warp's 32 increments always hit 32 distinct banks): no atomics, no
+// contention on Zipf heavy hitters.  After each tile the warp sums the columns
+// (mod 2^16, as differences to the previous sums, so counters may wrap) to get
+// the tile's bin counts, folds them to the pass-0 digit counts and keeps
+// running totals in registers for the global histogram.
 // ---------------------------------------------------------------------------
+constexpr int HIST_WARPS = 4;
+constexpr int TILE_U8 = PASS_THREADS * 16;  // tile of pass 0 for byte symbols
+
 template <int W>
-__global__ void __launch_bounds__(256) hist_u8_kernel(const uint8_t* __restrict__ text, int64_t n,
-                                                      unsigned long long* __restrict__ hist,
-                                                      int32_t* __restrict__ status) {
+__global__ void __launch_bounds__(HIST_WARPS * 32) hist_u8_kernel(const uint8_t* __restrict__ text, int64_t n,
+                                                                 int dshift, int nd0,
+                                                                 unsigned long long* __restrict__ hist,
+                                                                 uint32_t* __restrict__ tcnt0, int64_t ntiles,
+                                                                 int32_t* __restrict__ status) {
   constexpr int NB = 1 << W;
-  constexpr int PER = (NB + 31) / 32;
-  constexpr int LOWB = W < 5 ? W : 5;
-  __shared__ unsigned s_hist[NB];
-  for (int i = threadIdx.x; i < NB; i += blockDim.x) s_hist[i] = 0;
-  __syncthreads();
-
-  const int lane = threadIdx.x & 31;
-  unsigned sel[LOWB];
+  constexpr int NPAIR = (NB + 1) / 2;
+  constexpr int WORDS = NPAIR * 32;              // per warp
+  constexpr int PER = (NPAIR + 31) / 32;         // pairs per lane
+  extern __shared__ __align__(16) uint32_t s_cols[];
+  __shared__ uint32_t s_dig[HIST_WARPS][NDIG];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint32_t* c32 = s_cols + (size_t)wid * WORDS;
+  for (int i = lane; i < WORDS; i += 32) c32[i] = 0;
+  if (lane < NDIG) s_dig[wid][lane] = 0;
+  __syncwarp();
+  // byte address of this lane's counter for bin v: ((v >> 1) * 32 + lane) * 4 + (v & 1) * 2
+  //   = 2 v + 124 (v >> 1) + 4 lane
+  unsigned char* cbase = reinterpret_cast<unsigned char*>(c32) + 4 * lane;
+  uint32_t prev[PER][2], tot[PER][2];
 #pragma unroll
-  for (int k = 0; k < LOWB; ++k) sel[k] = ((lane >> k) & 1) ? 0u : FULL;
-  unsigned cnt[PER];
-#pragma unroll
-  for (int i = 0; i < PER; ++i) cnt[i] = 0;
-  unsigned bad = 0;
-
-  const int64_t nvec = (n + 15) >> 4;
+  for (int i = 0; i < PER; ++i) prev[i][0] = prev[i][1] = tot[i][0] = tot[i][1] = 0;
+  uint32_t bad = 0;
+  const uint32_t badmask = ((0xFFu << W) & 0xFFu) * 0x01010101u;
   const bool aligned = (((uintptr_t)text) & 15) == 0;
-  const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t wv = gwarp * 32; wv < nvec; wv += nwarps * 32) {
-    const int64_t vi = wv + lane;
-    const int64_t first = vi * 16;
-    uint32_t word[4] = {0, 0, 0, 0};
-    int nvalid = 0;
-    if (vi < nvec) {
-      nvalid = (int)min((int64_t)16, n - first);
-      if (aligned && nvalid == 16) {
-        const uint4 q = __ldcs(reinterpret_cast<const uint4*>(text) + vi);
-        word[0] = q.x; word[1] = q.y; word[2] = q.z; word[3] = q.w;
-      } else {
-        for (int e = 0; e < nvalid; ++e) word[e >> 2] |= (uint32_t)text[first + e] << (8 * (e & 3));
+  const int64_t gw = (int64_t)blockIdx.x * HIST_WARPS + wid;
+  const int64_t nwarps = (int64_t)gridDim.x * HIST_WARPS;
+  for (int64_t t = gw; t < ntiles; t += nwarps) {
+    const int64_t first = t * TILE_U8;
+    const int cnt = (int)min((int64_t)TILE_U8, n - first);
+    if (cnt == TILE_U8 && aligned) {
+      const uint4* v4 = reinterpret_cast<const uint4*>(text + first);
+#pragma unroll 2
+      for (int k0 = 0; k0 < TILE_U8 / 16 / 32; k0 += 4) {
+        uint4 q[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) q[k] = __ldcs(v4 + (k0 + k) * 32 + lane);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t wd[4] = {q[k].x, q[k].y, q[k].z, q[k].w};
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if (W < 8) bad |= wd[u] & badmask;
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+              const uint32_t v = __byte_perm(wd[u], 0, 0x4440 + b) & (NB - 1);
+              uint16_t* ctr = reinterpret_cast<uint16_t*>(cbase + 2 * v + 124 * (v >> 1));
+              *ctr = (uint16_t)(*ctr + 1);
+            }
+          }
+        }
       }
-    }
-#pragma unroll
-    for (int wd = 0; wd < 4; ++wd) {
-      if (W < 8) bad |= word[wd] & (((0xFFu << W) & 0xFFu) * 0x01010101u);
-    }
-#pragma unroll
-    for (int e = 0; e < 16; ++e) {
-      const unsigned byte = (word[e >> 2] >> (8 * (e & 3))) & 0xFFu;
-      const unsigned V = __ballot_sync(FULL, e < nvalid);
-      unsigned B[W];
-#pragma unroll
-      for (int k = 0; k < W; ++k) B[k] = __ballot_sync(FULL, (byte >> k) & 1u);
-      unsigned low = V;
-#pragma unroll
-      for (int k = 0; k < LOWB; ++k) low &= B[k] ^ sel[k];
-      if (W <= 5) {
-        cnt[0] += __popc(low);
-      } else {
-#pragma unroll
-        for (int i = 0; i < PER; ++i) {
-          unsigned m = low;
-#pragma unroll
-          for (int k = 5; k < W; ++k) m &= ((i >> (k - 5)) & 1) ? B[k] : ~B[k];
-          cnt[i] += __popc(m);
+    } else {
+      for (int i = lane; i < cnt; i += 32) {
+        const uint32_t v = text[first + i];
+        if (v >> W) {
+          bad = 1;
+        } else {
+          uint16_t* ctr = reinterpret_cast<uint16_t*>(cbase + 2 * v + 124 * (v >> 1));
+          *ctr = (uint16_t)(*ctr + 1);
         }
       }
     }
+    __syncwarp();
+    // column sums of this lane's pairs -> the tile's bin counts
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const int pr = lane + 32 * i;
+      if (pr < NPAIR) {
+        const uint4* col = reinterpret_cast<const uint4*>(c32 + pr * 32);
+        uint32_t lo = 0, hi = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint4 q = col[k];
+          lo += (q.x & 0xFFFFu) + (q.y & 0xFFFFu) + (q.z & 0xFFFFu) + (q.w & 0xFFFFu);
+          hi += (q.x >> 16) + (q.y >> 16) + (q.z >> 16) + (q.w >> 16);
+        }
+        const uint32_t d0 = (lo - prev[i][0]) & 0xFFFFu, d1 = (hi - prev[i][1]) & 0xFFFFu;
+        prev[i][0] = lo;
+        prev[i][1] = hi;
+        tot[i][0] += d0;
+        tot[i][1] += d1;
+        if (d0) atomicAdd(&s_dig[wid][(2 * pr) >> dshift], d0);
+        if (d1 && 2 * pr + 1 < NB) atomicAdd(&s_dig[wid][(2 * pr + 1) >> dshift], d1);
+      }
+    }
+    __syncwarp();
+    if (lane < nd0) {
+      tcnt0[(int64_t)lane * ntiles + t] = s_dig[wid][lane];
+      s_dig[wid][lane] = 0;
+    }
+    __syncwarp();
   }
 #pragma unroll
   for (int i = 0; i < PER; ++i) {
-    const int bin = lane + 32 * i;
-    if (bin < NB && cnt[i]) atomicAdd(&s_hist[bin], cnt[i]);
+    const int pr = lane + 32 * i;
+    if (pr < NPAIR) {
+      if (tot[i][0]) atomicAdd(&hist[2 * pr], (unsigned long long)tot[i][0]);
+      if (tot[i][1] && 2 * pr + 1 < NB) atomicAdd(&hist[2 * pr + 1], (unsigned long long)tot[i][1]);
+    }
   }
   if (bad) atomicOr(status, WVLT_STATUS_RANGE);
-  __syncthreads();
-  for (int i = threadIdx.x; i < NB; i += blockDim.x)
-    if (s_hist[i]) atomicAdd(&hist[i], (unsigned long long)s_hist[i]);
 }
 
 // Generic histogram for wide symbols / wide alphabets: shared-memory bins when
@@ -212,24 +243,71 @@ __global__ void __launch_bounds__(256) hist_generic_kernel(const TIn* __restrict
 
 __global__ void fill_i64_kernel(int64_t* p, int64_t v) { *p = v; }
 
+// Pass-0 tile digit counts for the generic path (wide symbols or alphabets):
+// one warp per tile, lane-private 32-bit counters (bank = lane).
+__global__ void __launch_bounds__(256) digits_kernel(const void* __restrict__ text, int sym_bytes, int64_t n, int tile,
+                                                     int dshift, int nd0, int64_t ntiles,
+                                                     uint32_t* __restrict__ tcnt0) {
+  __shared__ uint32_t s_c[8][NDIG * 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint32_t* c = s_c[wid];
+  const int64_t gw = (int64_t)blockIdx.x * 8 + wid;
+  const int64_t nwarps = (int64_t)gridDim.x * 8;
+  for (int64_t t = gw; t < ntiles; t += nwarps) {
+    for (int i = lane; i < NDIG * 32; i += 32) c[i] = 0;
+    __syncwarp();
+    const int64_t first = t * tile;
+    const int cnt = (int)min((int64_t)tile, n - first);
+    for (int i = lane; i < cnt; i += 32) {
+      uint32_t v;
+      if (sym_bytes == 1) v = ((const uint8_t*)text)[first + i];
+      else if (sym_bytes == 2) v = ((const uint16_t*)text)[first + i];
+      else v = ((const uint32_t*)text)[first + i];
+      const uint32_t e = (dshift >= 32 ? 0u : (v >> dshift)) & (uint32_t)(nd0 - 1);
+      c[e * 32 + lane] += 1;
+    }
+    __syncwarp();
+    if (lane < nd0) {
+      uint32_t s = 0;
+      for (int l = 0; l < 32; ++l) s += c[lane * 32 + l];
+      tcnt0[(int64_t)lane * ntiles + t] = s;
+    }
+    __syncwarp();
+  }
+}
+
+// Widen symbols stored narrower than the code width (e.g. uint8 storage with
+// sigma > 256) so the all-ones tail sentinel of the pass kernel covers every
+// code bit.
+template <typename TI, typename TO>
+__global__ void widen_kernel(const TI* __restrict__ in, TO* __restrict__ out, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (TO)in[i];
+}
+
+
+
 // ---------------------------------------------------------------------------
-// Build plan shared by host and the tables kernel
+// Build plan shared by host and kernels
 // ---------------------------------------------------------------------------
 struct Plan {
   int width;
   int kind;
   int npass;
+  int widen_bytes;      // > 0: text is widened to this many bytes before pass 0
   int lvl[MAXP];        // first level of the pass
   int K[MAXP];          // levels in the pass
   int in_bytes[MAXP];   // element bytes of A_lvl
   int out_bytes[MAXP];  // element bytes of A_{lvl+K} (0 = no output)
   int tile[MAXP];       // symbols per tile
+  int tshift[MAXP];     // log2(tile)
   int64_t ntiles[MAXP];
   int64_t corr_off[MAXP][KMAX + 1];  // WT placement tables (int64 offsets into corr)
   int64_t corr_total;
   // workspace carve (byte offsets)
-  size_t off_chain, off_wtstart, off_wmbase, off_corr, off_counter, off_status, off_buf0, off_buf1;
-  size_t status_bytes, buf_bytes, total;
+  size_t off_chain, off_wtstart, off_wmbase, off_corr, off_scratch, off_tcnt[MAXP], off_tpre[MAXP], off_bsum,
+      off_buf0, off_buf1, off_wide;
+  size_t tcnt_bytes, buf_bytes, total;
 };
 
 __host__ __device__ inline int64_t chain_off(int k) { return (1ll << k) - 1; }  // level-k table in a 2^(w+1)-1 array
@@ -250,7 +328,6 @@ struct TablesArgs {
   int64_t* wtstart;
   int64_t* wm_base;  // [MAXP][KMAX+1][NDIG]
   int64_t* corr;
-  uint32_t* counters;
   int64_t* zeros_out;    // may be null
   int64_t* hist_out;     // may be null
   int64_t* borders_out;  // may be null
@@ -327,9 +404,6 @@ __global__ void __launch_bounds__(TAB_THREADS) tables_kernel(const TablesArgs a)
   const int w = P.width;
   const int tid = threadIdx.x;
   const int64_t nb = 1ll << w;
-
-  // counters for the passes' dynamic tile ids
-  if (tid < MAXP) a.counters[tid] = 0;
 
   // 1. chain level w = histogram; range check of bins at or above sigma
   int64_t* cw = a.chain + chain_off(w);
@@ -432,6 +506,95 @@ __global__ void __launch_bounds__(TAB_THREADS) tables_kernel(const TablesArgs a)
 }
 
 // ---------------------------------------------------------------------------
+// S: exclusive scan of the per-tile digit counts over tiles, digit-major
+// layout cnt[e][tile] -> pre[e][tile].  Two launches: block totals, then each
+// block adds the totals of the blocks before it and scans its own range.
+// ---------------------------------------------------------------------------
+constexpr int SCAN_THREADS = 256;
+constexpr int SCAN_ITEMS = 8;
+constexpr int SCAN_TILE = SCAN_THREADS * SCAN_ITEMS;
+
+__global__ void __launch_bounds__(SCAN_THREADS) scan_reduce_kernel(const uint32_t* __restrict__ cnt, int64_t ntiles,
+                                                                   int64_t nblk, int64_t* __restrict__ bsum) {
+  __shared__ int64_t s_red[32];
+  const int e = blockIdx.y;
+  const int64_t b = blockIdx.x;
+  const uint32_t* row = cnt + (int64_t)e * ntiles;
+  int64_t s = 0;
+  for (int k = 0; k < SCAN_ITEMS; ++k) {
+    const int64_t i = b * SCAN_TILE + (int64_t)k * SCAN_THREADS + threadIdx.x;
+    if (i < ntiles) s += row[i];
+  }
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    int64_t v = threadIdx.x < SCAN_THREADS / 32 ? s_red[threadIdx.x] : 0;
+    v = warp_sum(v);
+    if (threadIdx.x == 0) bsum[(int64_t)e * nblk + b] = v;
+  }
+}
+
+__global__ void __launch_bounds__(SCAN_THREADS) scan_apply_kernel(const uint32_t* __restrict__ cnt, int64_t ntiles,
+                                                                  int64_t nblk, const int64_t* __restrict__ bsum,
+                                                                  int64_t* __restrict__ pre) {
+  __shared__ int64_t s_red[33];
+  const int e = blockIdx.y;
+  const int64_t b = blockIdx.x;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  // offset = totals of the blocks before b
+  int64_t off = 0;
+  for (int64_t i = threadIdx.x; i < b; i += SCAN_THREADS) off += bsum[(int64_t)e * nblk + i];
+  off = warp_sum(off);
+  if (lane == 0) s_red[wid] = off;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t t = 0;
+    for (int w = 0; w < SCAN_THREADS / 32; ++w) t += s_red[w];
+    s_red[32] = t;
+  }
+  __syncthreads();
+  const int64_t boff = s_red[32];
+  __syncthreads();
+  // block scan, SCAN_ITEMS consecutive tiles per thread
+  const uint32_t* row = cnt + (int64_t)e * ntiles;
+  int64_t* out = pre + (int64_t)e * ntiles;
+  const int64_t i0 = b * SCAN_TILE + (int64_t)threadIdx.x * SCAN_ITEMS;
+  uint32_t v[SCAN_ITEMS];
+  int64_t ts = 0;
+#pragma unroll
+  for (int k = 0; k < SCAN_ITEMS; ++k) {
+    v[k] = (i0 + k < ntiles) ? row[i0 + k] : 0u;
+    ts += v[k];
+  }
+  int64_t incl = ts;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t t = __shfl_up_sync(FULL, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) s_red[wid] = incl;
+  __syncthreads();
+  if (wid == 0) {
+    const int64_t x = lane < SCAN_THREADS / 32 ? s_red[lane] : 0;
+    int64_t sc = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t t = __shfl_up_sync(FULL, sc, o);
+      if (lane >= o) sc += t;
+    }
+    if (lane < SCAN_THREADS / 32) s_red[lane] = sc - x;
+  }
+  __syncthreads();
+  int64_t run = boff + s_red[wid] + incl - ts;
+#pragma unroll
+  for (int k = 0; k < SCAN_ITEMS; ++k) {
+    if (i0 + k < ntiles) out[i0 + k] = run;
+    run += v[k];
+  }
+}
+
+// ---------------------------------------------------------------------------
 // K3: fused level pass
 // ---------------------------------------------------------------------------
 struct PassArgs {
@@ -440,10 +603,14 @@ struct PassArgs {
   uint64_t* words;  // level words base (level L at words + L * nwords)
   int64_t nwords;
   int64_t n;
+  int64_t ntiles;
   int level, width, kind, has_out;
-  uint64_t* status;
-  uint32_t* counter;
-  unsigned epoch;
+  const uint32_t* tcnt;  // this pass: [2^K][ntiles] digit counts (numeric digit)
+  const int64_t* tpre;   // this pass: [2^K][ntiles] exclusive prefixes over tiles
+  uint32_t* ncnt;        // next pass: [2^K'][ntiles'] digit counts (accumulated here), or null
+  int64_t nntiles;
+  int ntshift;           // log2(next tile)
+  int nK;                // next pass K
   const int64_t* wm_base;  // this pass: [KMAX+1][NDIG]
   const int64_t* corr;     // WT tables of this pass: table j at corr + corr_off[j]
   int64_t corr_off[KMAX + 1];
@@ -453,10 +620,11 @@ template <typename TIn, int K, int E>
 struct PassSmem {
   static constexpr int T = PASS_THREADS * E;
   static constexpr int NC = T / 32;
-  static constexpr size_t buf_bytes = (size_t)(K + 1) * T * sizeof(TIn);
-  static constexpr size_t bits_bytes = (size_t)K * (NC + 2) * 4;
-  static constexpr size_t scan_bytes = (size_t)(NC + 1) * 4;
-  static constexpr size_t total = buf_bytes + bits_bytes + scan_bytes;
+  // order buffers A_l .. A_{l+K-1} in the tile-local digit orders d_0 .. d_{K-1}
+  static constexpr size_t buf_bytes = (size_t)K * T * sizeof(TIn);
+  // ballot words of every level in its local order (+pad words for extract_bits)
+  static constexpr size_t bits_bytes = (size_t)K * (NC + 4) * 4;
+  static constexpr size_t total = buf_bytes + bits_bytes;
 };
 
 __device__ __forceinline__ uint64_t extract_bits(const uint32_t* L, int off, int cnt) {
@@ -466,13 +634,13 @@ __device__ __forceinline__ uint64_t extract_bits(const uint32_t* L, int off, int
   return cnt >= 64 ? v : (v & ((1ull << cnt) - 1));
 }
 
-// Copy runs of the tile-local bit string L to the level's global words:
-// run r = local bits [ls[r], ls[r]+len[r]) -> global bits [gs[r], gs[r]+len[r]).
-// Whole destination words are stored, words shared with another run are OR-ed
+// Copy runs of the tile-local bit string L to the level's global words: run
+// r = local bits [ls[r], ls[r]+len[r]) -> global bits [gs[r], gs[r]+len[r]).
+// Whole destination words are stored; words shared with another run are OR-ed
 // into the pre-zeroed level (the "owner writes whole words" rule of
 // gather_bits, _kernels.py:197-205, relaxed to atomics at run edges).
-__device__ void emit_runs(const uint32_t* L, int R, const int* ls, const int* len, const int64_t* gs,
-                          uint64_t* gw, int* s_wpre) {
+__device__ void emit_runs(const uint32_t* L, int R, const int* ls, const int* len, const int64_t* gs, uint64_t* gw,
+                          int* s_wpre) {
   if (threadIdx.x == 0) {
     int acc = 0;
     for (int r = 0; r < R; ++r) {
@@ -483,7 +651,7 @@ __device__ void emit_runs(const uint32_t* L, int R, const int* ls, const int* le
   }
   __syncthreads();
   const int total = s_wpre[R];
-  for (int f = threadIdx.x; f < total; f += blockDim.x) {
+  for (int f = threadIdx.x; f < total; f += PASS_THREADS) {
     int r = 0;
     while (s_wpre[r + 1] <= f) ++r;
     const int64_t g = gs[r];
@@ -505,44 +673,45 @@ __device__ void emit_runs(const uint32_t* L, int R, const int* ls, const int* le
 
 template <typename TIn>
 __device__ __forceinline__ unsigned digit_of(TIn x, int top_shift, int j) {
-  // d_j = sum_{i<j} bit(top_shift - i) << i
+  // LSD digit d_j = sum_{i<j} bit(top_shift - i) << i
   unsigned d = 0;
   for (int i = 0; i < j; ++i) d |= (((uint32_t)x >> (top_shift - i)) & 1u) << i;
   return d;
 }
 
+// One CTA = one tile of T = 512 * E symbols of A_l; CTAs are independent.
 template <typename TIn, typename TOut, int K, int E>
-__global__ void __launch_bounds__(PASS_THREADS) level_pass_kernel(const PassArgs a) {
+__global__ void __launch_bounds__(PASS_THREADS, 2) level_pass_kernel(const PassArgs a) {
   using S = PassSmem<TIn, K, E>;
   constexpr int T = S::T;
   constexpr int NC = S::NC;
   constexpr int NW = PASS_THREADS / 32;
+  constexpr int nd = 1 << K;
   extern __shared__ __align__(16) unsigned char smem[];
   TIn* buf = reinterpret_cast<TIn*>(smem);
   uint32_t* bits = reinterpret_cast<uint32_t*>(smem + S::buf_bytes);
-  uint32_t* scan = reinterpret_cast<uint32_t*>(smem + S::buf_bytes + S::bits_bytes);
 
+  __shared__ __align__(16) uint32_t s_wtot[2][NW];
   __shared__ int s_cnt[K + 1][NDIG];
   __shared__ int s_ls[K + 1][NDIG];
   __shared__ int64_t s_lb[K + 1][NDIG];
-  __shared__ int64_t s_gs[NDIG];
+  __shared__ int64_t s_gs[K + 1][NDIG];
+  __shared__ int64_t s_off[NDIG];  // output offset by numeric K-bit digit (uniform tiles)
+  __shared__ int64_t s_ft[NDIG];   // first next-pass tile of each output run (numeric digit)
+  __shared__ uint32_t s_ncnt[2 * NDIG][NDIG];  // next-pass digit counts per (run, next tile)
   __shared__ int s_wpre[NDIG + 1];
-  __shared__ uint32_t s_wtot[NW + 1];
-  __shared__ int s_tile;
   __shared__ int s_q1;
   __shared__ int64_t s_q;
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int w = a.width, l0 = a.level;
-
-  if (tid == 0) s_tile = (int)atomicAdd(a.counter, 1u);
-  __syncthreads();
-  const int64_t tile = s_tile;
+  const bool wm = a.kind == WVLT_KIND_WM;
+  const int64_t tile = blockIdx.x;
   const int64_t base = tile * T;
   const int cnt = (int)min((int64_t)T, a.n - base);
-  const TIn* src = reinterpret_cast<const TIn*>(a.src) + base;
 
   // ---- stage the tile (invalid tail slots = all ones so they sort last) ----
+  const TIn* src = reinterpret_cast<const TIn*>(a.src) + base;
   if (cnt == T && ((((uintptr_t)src) & 15) == 0)) {
     const uint4* s4 = reinterpret_cast<const uint4*>(src);
     uint4* d4 = reinterpret_cast<uint4*>(buf);
@@ -550,191 +719,209 @@ __global__ void __launch_bounds__(PASS_THREADS) level_pass_kernel(const PassArgs
   } else {
     for (int p = tid; p < T; p += PASS_THREADS) buf[p] = p < cnt ? src[p] : (TIn)~(TIn)0;
   }
-  if (tid == 0) {
-    s_cnt[0][0] = cnt;
-    s_ls[0][0] = 0;
+  if (tid < 2 * NDIG * NDIG) (&s_ncnt[0][0])[tid] = 0;
+  if (wid == 0) {
+    // tile digit counts / prefixes (numeric digit e = lane) -> per LSD digit d
+    if (lane < nd) {
+      const int d = (int)rev_bits((unsigned)lane, K);
+      s_cnt[K][d] = (int)a.tcnt[(int64_t)lane * a.ntiles + tile];
+      s_lb[K][d] = a.tpre[(int64_t)lane * a.ntiles + tile];
+    }
+    __syncwarp();
+    // every shorter digit: sums over the digits sharing the low j bits
+    for (int j = 0; j < K; ++j) {
+      if (lane < (1 << j)) {
+        int c = 0;
+        int64_t lb = 0;
+        for (int e = lane; e < nd; e += (1 << j)) {
+          c += s_cnt[K][e];
+          lb += s_lb[K][e];
+        }
+        s_cnt[j][lane] = c;
+        s_lb[j][lane] = lb;
+      }
+    }
+    __syncwarp();
+    // group starts in the tile-local orders (groups by increasing LSD digit)
+    for (int j = 0; j <= K; ++j) {
+      const int mj = 1 << j;
+      const int c = lane < mj ? s_cnt[j][lane] : 0;
+      int incl = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += t;
+      }
+      if (lane < mj) s_ls[j][lane] = incl - c;
+    }
+  }
+  __syncthreads();
+  if (wid == 0) {
+    bool q1 = true;
+    int64_t q = 0;
+    if (!wm) {
+      const int sh = w - l0;
+      const uint64_t qf = sh >= 32 ? 0 : ((uint64_t)(uint32_t)buf[0] >> sh);
+      const uint64_t ql = sh >= 32 ? 0 : ((uint64_t)(uint32_t)buf[cnt - 1] >> sh);
+      q1 = qf == ql;
+      q = (int64_t)qf;
+    }
+    if (lane == 0) {
+      s_q1 = q1;
+      s_q = q;
+    }
+    if (q1) {  // placement is a per-digit constant in this tile
+      for (int j = 1; j <= K; ++j) {
+        if (lane < (1 << j)) {
+          const int d = lane;
+          const int64_t tb = wm ? a.wm_base[j * NDIG + d]
+                                : a.corr[a.corr_off[j] + (q << j) + (int64_t)rev_bits((unsigned)d, j)];
+          s_gs[j][d] = tb + s_lb[j][d];
+        }
+      }
+      __syncwarp();
+      if (lane < nd) {
+        const int d = (int)rev_bits((unsigned)lane, K);  // lane = numeric digit
+        s_off[lane] = s_gs[K][d] - s_ls[K][d];
+        s_ft[lane] = s_gs[K][d] >> a.ntshift;
+      }
+    }
   }
   __syncthreads();
 
-  // WT: does the tile lie inside one level-l0 node?
-  if (a.kind == WVLT_KIND_WT && tid == 0) {
-    const int sh = w - l0;
-    const uint64_t qf = sh >= 32 ? 0 : ((uint64_t)(uint32_t)buf[0] >> sh);
-    const uint64_t ql = sh >= 32 ? 0 : ((uint64_t)(uint32_t)buf[cnt - 1] >> sh);
-    s_q1 = qf == ql;
-    s_q = (int64_t)qf;
-  }
-
-  // ---- K stable one-bit splits in shared memory ----
+  const unsigned lt = lanemask_lt();
+  const int pbase = wid * E * 32;  // this warp's first symbol (warp-contiguous chunks)
   TIn x[E];
   uint32_t m[E];
+
 #pragma unroll 1
   for (int j = 0; j < K; ++j) {
-    const TIn* cur = buf + (size_t)j * T;
-    uint32_t* bj = bits + j * (NC + 2);
     const int sh = w - 1 - l0 - j;
+    const TIn* cur = buf + (size_t)j * T;
 #pragma unroll
     for (int e = 0; e < E; ++e) {
-      const int p = e * PASS_THREADS + tid;
-      x[e] = cur[p];
+      x[e] = cur[pbase + e * 32 + lane];
       m[e] = __ballot_sync(FULL, ((uint32_t)x[e] >> sh) & 1u);
-      if (lane == 0) {
-        bj[p >> 5] = m[e];
-        scan[p >> 5] = __popc(m[e]);
-      }
     }
-    if (tid < 2) bj[NC + tid] = 0;
-    __syncthreads();
-    // exclusive scan of the chunk popcounts (NC <= PASS_THREADS)
-    {
-      const uint32_t v = tid < NC ? scan[tid] : 0u;
-      uint32_t incl = v;
+    // this level's ballot words: lane e keeps m[e]
+    uint32_t mine = 0;
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t t = __shfl_up_sync(FULL, incl, o);
-        if (lane >= o) incl += t;
-      }
-      if (lane == 31) s_wtot[wid] = incl;
-      __syncthreads();
-      if (wid == 0) {
-        const uint32_t t = lane < NW ? s_wtot[lane] : 0u;
-        uint32_t s = t;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const uint32_t u = __shfl_up_sync(FULL, s, o);
-          if (lane >= o) s += u;
-        }
-        if (lane < NW) s_wtot[lane] = s - t;
-        if (lane == NW - 1) s_wtot[NW] = s;
-      }
-      __syncthreads();
-      if (tid < NC) scan[tid] = incl - v + s_wtot[wid];
-      if (tid == 0) scan[NC] = s_wtot[NW];
-      __syncthreads();
-    }
-    // group sizes of the next digit: split each d_j group by this bit
-    if (tid < (1 << j)) {
-      const int d = tid;
-      const int gs0 = s_ls[j][d], c0 = s_cnt[j][d];
-      auto rank1 = [&](int p) -> int {
-        const int c = p >> 5, r = p & 31;
-        return (int)scan[c] + (r ? __popc(bj[c] & ((1u << r) - 1u)) : 0);
-      };
-      const int ones = rank1(gs0 + c0) - rank1(gs0);
-      s_cnt[j + 1][d] = c0 - ones;
-      s_cnt[j + 1][d + (1 << j)] = ones;
-    }
-    // scatter into the next order
-    if (j + 1 < K || a.has_out) {
-      const int Z = T - (int)scan[NC];
-      TIn* nxt = buf + (size_t)(j + 1) * T;
-      const unsigned lt = lanemask_lt();
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-        const int p = e * PASS_THREADS + tid;
-        const int r1 = (int)scan[p >> 5] + __popc(m[e] & lt);
-        const int dst = ((m[e] >> lane) & 1u) ? Z + r1 : p - r1;
-        nxt[dst] = x[e];
-      }
-    }
-    __syncthreads();
-    if (tid == 0) {
-      int run = 0;
-      for (int d = 0; d < (2 << j); ++d) {
-        s_ls[j + 1][d] = run;
-        run += s_cnt[j + 1][d];
-      }
-    }
-    // level l0 bits are already in global order: aligned word stores
+    for (int e = 0; e < E; ++e)
+      if (lane == e) mine = m[e];
     if (j == 0) {
+      // level l0 is in global order already: aligned word stores
       uint32_t* g32 = reinterpret_cast<uint32_t*>(a.words + (int64_t)l0 * a.nwords);
       const int64_t lim = 2 * a.nwords;
-      for (int c = tid; c < NC; c += PASS_THREADS) {
+      if (lane < E) {
+        const int c = wid * E + lane;
         const int64_t gi = (base >> 5) + c;
         if (gi < lim) {
           const int first = c * 32;
-          uint32_t v = bj[c];
+          uint32_t v = mine;
           if (first + 32 > cnt) v = first >= cnt ? 0u : (v & ((1u << (cnt - first)) - 1u));
           g32[gi] = v;
         }
       }
+    } else if (lane < E) {
+      bits[j * (NC + 4) + wid * E + lane] = mine;
     }
+    const bool scatter = (j + 1 < K) || a.has_out;
+    if (!scatter) break;
+    // warp-local chunk prefixes in registers, CTA-wide warp prefix via smem
+    uint32_t wtot = 0;
+#pragma unroll
+    for (int e = 0; e < E; ++e) wtot += __popc(m[e]);
+    if (lane == 0) s_wtot[j & 1][wid] = wtot;
     __syncthreads();
-  }
-
-  // ---- decoupled look-back over the 2^K digit counts ----
-  const int nd = 1 << K;
-  if (wid == 0) {
-    uint64_t* st = a.status + tile * NDIG;
-    if (lane < nd) st_relaxed_u64(st + lane, pack_status(tile == 0 ? 2u : 1u, a.epoch, (uint64_t)s_cnt[K][lane]));
-    int64_t acc = 0;
-    if (tile > 0) {
-      unsigned pending = (1u << nd) - 1u;
-      int64_t wb = tile - 1;
-      while (pending) {
-        const int64_t tt = wb - lane;
-#pragma unroll 1
-        for (int d = 0; d < nd; ++d) {
-          if (!((pending >> d) & 1u)) continue;
-          uint64_t s;
-          unsigned state;
-          if (tt < 0) {
-            s = 0;
-            state = 2;
-          } else {
-            s = ld_relaxed_u64(a.status + tt * NDIG + d);
-            state = status_state(s, a.epoch);
-            while (state == 0) {
-              __nanosleep(64);
-              s = ld_relaxed_u64(a.status + tt * NDIG + d);
-              state = status_state(s, a.epoch);
-            }
+    uint32_t wpre = 0, tot = 0;
+#pragma unroll
+    for (int q4 = 0; q4 < NW / 4; ++q4) {
+      const uint4 v = reinterpret_cast<const uint4*>(s_wtot[j & 1])[q4];
+      const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        wpre += (q4 * 4 + k) < wid ? vv[k] : 0u;
+        tot += vv[k];
+      }
+    }
+    const int Z = T - (int)tot;
+    uint32_t r = wpre;
+    if (j + 1 < K) {
+      TIn* nxt = buf + (size_t)(j + 1) * T;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int p = pbase + e * 32 + lane;
+        const int r1 = (int)r + __popc(m[e] & lt);
+        const int dst = ((m[e] >> lane) & 1u) ? Z + r1 : p - r1;
+        nxt[dst] = x[e];
+        r += __popc(m[e]);
+      }
+      __syncthreads();
+    } else {
+      // last split: straight to HBM, counting the next pass's digits per (run, next tile)
+      TOut* dst = reinterpret_cast<TOut*>(a.dst);
+      const uint32_t keep = wm ? ((w - l0 - K) >= 32 ? FULL : ((1u << (w - l0 - K)) - 1u)) : FULL;
+      const int eshift = w - l0 - K;
+      const int nshift = w - l0 - K - a.nK;  // next pass digit = bits l0+K .. l0+K+nK-1
+      const unsigned nmask = (1u << a.nK) - 1u;
+      if (s_q1) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int p = pbase + e * 32 + lane;
+          const int r1 = (int)r + __popc(m[e] & lt);
+          const int pos = ((m[e] >> lane) & 1u) ? Z + r1 : p - r1;
+          if (pos < cnt) {
+            const uint32_t xv = (uint32_t)x[e];
+            const unsigned dig = (xv >> eshift) & (nd - 1);
+            const int64_t gpos = s_off[dig] + pos;
+            dst[gpos] = (TOut)(xv & keep);
+            const int h = (int)((gpos >> a.ntshift) - s_ft[dig]);
+            atomicAdd(&s_ncnt[2 * dig + h][(xv >> nshift) & nmask], 1u);
           }
-          const unsigned im = __ballot_sync(FULL, state == 2u);
-          const int k = im ? __ffs(im) - 1 : 31;
-          uint64_t v = (lane <= k) ? (s & ST_VALUE_MASK) : 0ull;
-          v = warp_sum(v);
-          if (lane == d) acc += (int64_t)v;
-          if (im) pending &= ~(1u << d);
+          r += __popc(m[e]);
         }
-        wb -= 32;
+      } else {
+        const int64_t* ctab = a.corr + a.corr_off[K];
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int p = pbase + e * 32 + lane;
+          const int r1 = (int)r + __popc(m[e] & lt);
+          const int pos = ((m[e] >> lane) & 1u) ? Z + r1 : p - r1;
+          if (pos < cnt) {
+            const uint32_t xv = (uint32_t)x[e];
+            const unsigned d = rev_bits((xv >> eshift) & (nd - 1), K);
+            const uint64_t P = eshift >= 32 ? 0 : ((uint64_t)xv >> eshift);
+            const int64_t gpos = ctab[P] + s_lb[K][d] + pos - s_ls[K][d];
+            dst[gpos] = (TOut)(xv & keep);
+            atomicAdd(&a.ncnt[(int64_t)((xv >> nshift) & nmask) * a.nntiles + (gpos >> a.ntshift)], 1u);
+          }
+          r += __popc(m[e]);
+        }
       }
-      if (lane < nd) st_relaxed_u64(st + lane, pack_status(2u, a.epoch, (uint64_t)(acc + s_cnt[K][lane])));
-    }
-    if (lane < nd) s_lb[K][lane] = acc;
-  }
-  __syncthreads();
-  // fold the digit prefixes to every shorter digit
-  if (tid < NDIG) {
-    for (int j = 1; j < K; ++j) {
-      if (tid < (1 << j)) {
-        int64_t s = 0;
-        for (int e = tid; e < nd; e += (1 << j)) s += s_lb[K][e];
-        s_lb[j][tid] = s;
+      __syncthreads();
+      if (s_q1) {
+        const int ncount = 2 * nd * (1 << a.nK);
+        for (int i = tid; i < ncount; i += PASS_THREADS) {
+          const int slot = i >> a.nK, ne = i & (int)nmask;
+          const uint32_t v = s_ncnt[slot][ne];
+          if (v) {
+            const int64_t nt = s_ft[slot >> 1] + (slot & 1);
+            atomicAdd(&a.ncnt[(int64_t)ne * a.nntiles + nt], v);
+          }
+        }
       }
     }
   }
-  __syncthreads();
-
-  const bool wm = a.kind == WVLT_KIND_WM;
-  const bool uniform = wm || s_q1;  // placement is a per-digit constant in this tile
 
   // ---- emit levels l0+1 .. l0+K-1 ----
+  const bool uniform = s_q1;
 #pragma unroll 1
   for (int j = 1; j < K; ++j) {
     const int mj = 1 << j;
     uint64_t* gw = a.words + (int64_t)(l0 + j) * a.nwords;
-    const uint32_t* L = bits + j * (NC + 2);
+    const uint32_t* L = bits + j * (NC + 4);
     if (uniform) {
-      if (tid < mj) {
-        const int d = tid;
-        const int64_t tb =
-            wm ? a.wm_base[j * NDIG + d]
-               : a.corr[a.corr_off[j] + (s_q << j) + (int64_t)rev_bits((unsigned)d, j)];
-        s_gs[d] = tb + s_lb[j][d];
-      }
-      __syncthreads();
-      emit_runs(L, mj, s_ls[j], s_cnt[j], s_gs, gw, s_wpre);
+      emit_runs(L, mj, s_ls[j], s_cnt[j], s_gs[j], gw, s_wpre);
     } else {
       // WT tile spanning several nodes: per-symbol placement, runs found by
       // contiguity of the global position inside each warp chunk
@@ -744,7 +931,7 @@ __global__ void __launch_bounds__(PASS_THREADS) level_pass_kernel(const PassArgs
       const int64_t* ctab = a.corr + a.corr_off[j];
 #pragma unroll 1
       for (int e = 0; e < E; ++e) {
-        const int p = e * PASS_THREADS + tid;
+        const int p = pbase + e * 32 + lane;
         const bool valid = p < cnt;
         const TIn xv = cur[p];
         int64_t gpos = 0;
@@ -776,53 +963,10 @@ __global__ void __launch_bounds__(PASS_THREADS) level_pass_kernel(const PassArgs
           }
         }
       }
-      __syncthreads();
-    }
-  }
-
-  // ---- write A_{l0+K}, narrowed to the bits still needed ----
-  if (a.has_out) {
-    const TIn* fin = buf + (size_t)K * T;
-    TOut* dst = reinterpret_cast<TOut*>(a.dst);
-    const uint32_t keep = wm ? ((w - l0 - K) >= 32 ? FULL : ((1u << (w - l0 - K)) - 1u)) : FULL;
-    if (uniform) {
-      if (tid < nd) {
-        const int d = tid;
-        const int64_t tb = wm ? a.wm_base[K * NDIG + d]
-                              : a.corr[a.corr_off[K] + (s_q << K) + (int64_t)rev_bits((unsigned)d, K)];
-        s_gs[d] = tb + s_lb[K][d] - s_ls[K][d];
-      }
-      __syncthreads();
-      // group d occupies [ls_K[d], ls_K[d+1]) of the final order; find it by a
-      // short search (<= 16 groups), then one coalesced store per symbol
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-        const int p = e * PASS_THREADS + tid;
-        if (p < cnt) {
-          int d = 0;
-          while (d + 1 < nd && s_ls[K][d + 1] <= p) ++d;
-          dst[s_gs[d] + p] = (TOut)((uint32_t)fin[p] & keep);
-        }
-      }
-    } else {
-      const int tshift = w - 1 - l0;
-      const int pshift = w - l0 - K;
-      const int64_t* ctab = a.corr + a.corr_off[K];
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-        const int p = e * PASS_THREADS + tid;
-        if (p < cnt) {
-          const TIn xv = fin[p];
-          const unsigned d = digit_of(xv, tshift, K);
-          const uint64_t P = pshift >= 32 ? 0 : ((uint64_t)(uint32_t)xv >> pshift);
-          dst[ctab[P] + s_lb[K][d] + p - s_ls[K][d]] = (TOut)((uint32_t)xv & keep);
-        }
-      }
     }
   }
 }
 
-// ---------------------------------------------------------------------------
 // K5: merge (gather_bits)
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) merge_bits_kernel(uint64_t* __restrict__ dst, int64_t wlo, int64_t whi,
@@ -883,6 +1027,11 @@ int bytes_for_bits(int bits) { return bits <= 8 ? 1 : (bits <= 16 ? 2 : 4); }
 inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 int tile_for(int in_bytes) { return in_bytes == 4 ? PASS_THREADS * 8 : PASS_THREADS * 16; }
+int log2i(int v) {
+  int r = 0;
+  while ((1 << r) < v) ++r;
+  return r;
+}
 
 bool make_plan(int64_t n, int sym_bytes, int64_t sigma, int kind, Plan* P) {
   memset(P, 0, sizeof(*P));
@@ -890,10 +1039,15 @@ bool make_plan(int64_t n, int sym_bytes, int64_t sigma, int kind, Plan* P) {
   P->width = w;
   P->kind = kind;
   if (w > WVLT_MAX_WIDTH) return false;
-  const int vbits = sym_bytes * 8;  // symbols never need more bits than their storage
+  // symbols stored narrower than the code width are widened first (the tail
+  // sentinel of the pass kernel must set every code bit)
+  int sb = sym_bytes;
+  if (8 * sym_bytes < w) {
+    P->widen_bytes = bytes_for_bits(w);
+    sb = P->widen_bytes;
+  }
   int l = 0, p = 0;
   int64_t corr = 0;
-  int64_t max_tiles = 0;
   size_t max_buf = 0;
   while (l < w) {
     const int K = (w - l) < KMAX ? (w - l) : KMAX;
@@ -901,12 +1055,12 @@ bool make_plan(int64_t n, int sym_bytes, int64_t sigma, int kind, Plan* P) {
     P->K[p] = K;
     const int live_in = kind == WVLT_KIND_WM ? (w - l) : w;
     const int live_out = kind == WVLT_KIND_WM ? (w - l - K) : w;
-    P->in_bytes[p] = p == 0 ? sym_bytes : bytes_for_bits(live_in < vbits ? live_in : vbits);
-    P->out_bytes[p] = (l + K < w) ? bytes_for_bits(live_out < vbits ? live_out : vbits) : 0;
+    P->in_bytes[p] = p == 0 ? sb : bytes_for_bits(live_in);
+    P->out_bytes[p] = (l + K < w) ? bytes_for_bits(live_out) : 0;
     if (P->out_bytes[p] > P->in_bytes[p]) P->out_bytes[p] = P->in_bytes[p];
     P->tile[p] = tile_for(P->in_bytes[p]);
+    P->tshift[p] = log2i(P->tile[p]);
     P->ntiles[p] = (n + P->tile[p] - 1) / P->tile[p];
-    if (P->ntiles[p] > max_tiles) max_tiles = P->ntiles[p];
     if ((size_t)P->out_bytes[p] * (size_t)n > max_buf) max_buf = (size_t)P->out_bytes[p] * (size_t)n;
     if (kind == WVLT_KIND_WT) {
       for (int j = 1; j <= K; ++j) {
@@ -929,16 +1083,30 @@ bool make_plan(int64_t n, int sym_bytes, int64_t sigma, int kind, Plan* P) {
   off = align_up(off + (size_t)MAXP * (KMAX + 1) * NDIG * 8, 256);
   P->off_corr = off;
   off = align_up(off + (size_t)(corr ? corr : 1) * 8, 256);
-  P->off_counter = off;  // MAXP pass counters + one scratch status word
-  off = align_up(off + (MAXP + 1) * 4, 256);
-  P->off_status = off;
-  P->status_bytes = (size_t)(max_tiles ? max_tiles : 1) * NDIG * 8;
-  off = align_up(off + P->status_bytes, 256);
+  P->off_scratch = off;  // scratch status word
+  off = align_up(off + 64, 256);
+  const size_t tcnt_start = off;
+  int64_t max_nblk = 1;
+  for (int q = 0; q < P->npass; ++q) {
+    P->off_tcnt[q] = off;
+    off = align_up(off + (size_t)(1 << P->K[q]) * P->ntiles[q] * 4, 256);
+    const int64_t nblk = (P->ntiles[q] + SCAN_TILE - 1) / SCAN_TILE;
+    if (nblk > max_nblk) max_nblk = nblk;
+  }
+  P->tcnt_bytes = off - tcnt_start;
+  for (int q = 0; q < P->npass; ++q) {
+    P->off_tpre[q] = off;
+    off = align_up(off + (size_t)(1 << P->K[q]) * P->ntiles[q] * 8, 256);
+  }
+  P->off_bsum = off;
+  off = align_up(off + (size_t)NDIG * max_nblk * 8, 256);
   P->buf_bytes = align_up(max_buf ? max_buf : 16, 256);
   P->off_buf0 = off;
   off += P->buf_bytes;
   P->off_buf1 = off;
   off += P->buf_bytes;
+  P->off_wide = off;
+  if (P->widen_bytes) off += align_up((size_t)n * P->widen_bytes, 256);
   P->total = off;
   return true;
 }
@@ -991,23 +1159,10 @@ int sm_count() {
   return sms;
 }
 
-cudaError_t launch_hist(const void* text, int sym_bytes, int64_t n, int w, unsigned long long* hist,
-                        int32_t* status, cudaStream_t s) {
+// Generic full histogram (wide symbols / alphabets) or the range check alone (hist == null).
+cudaError_t launch_hist_generic(const void* text, int sym_bytes, int64_t n, int w, unsigned long long* hist,
+                                int32_t* status, cudaStream_t s) {
   const int blocks = sm_count() * 4;
-  if (sym_bytes == 1 && w <= 8 && w >= 1) {
-    const uint8_t* t = (const uint8_t*)text;
-    switch (w) {
-      case 1: hist_u8_kernel<1><<<blocks, 256, 0, s>>>(t, n, hist, status); break;
-      case 2: hist_u8_kernel<2><<<blocks, 256, 0, s>>>(t, n, hist, status); break;
-      case 3: hist_u8_kernel<3><<<blocks, 256, 0, s>>>(t, n, hist, status); break;
-      case 4: hist_u8_kernel<4><<<blocks, 256, 0, s>>>(t, n, hist, status); break;
-      case 5: hist_u8_kernel<5><<<blocks, 256, 0, s>>>(t, n, hist, status); break;
-      case 6: hist_u8_kernel<6><<<blocks, 256, 0, s>>>(t, n, hist, status); break;
-      case 7: hist_u8_kernel<7><<<blocks, 256, 0, s>>>(t, n, hist, status); break;
-      default: hist_u8_kernel<8><<<blocks, 256, 0, s>>>(t, n, hist, status); break;
-    }
-    return cudaGetLastError();
-  }
   const bool smem = w <= 14;
   const size_t sb = smem ? ((size_t)4 << w) : 0;
   if (smem && sb > 48 * 1024) {
@@ -1025,6 +1180,76 @@ cudaError_t launch_hist(const void* text, int sym_bytes, int64_t n, int w, unsig
   else WVLT_HG(uint32_t);
 #undef WVLT_HG
   return cudaGetLastError();
+}
+
+// K1 for a build: histogram of the text plus pass-0 tile digit counts.
+cudaError_t launch_hist_build(const void* text, int sym_bytes, int64_t n, int w, int K0, int tile0, int64_t ntiles0,
+                              unsigned long long* hist, uint32_t* tcnt0, int32_t* status, cudaStream_t s) {
+  const bool fast = sym_bytes == 1 && w >= 1 && w <= 8 && tile0 == TILE_U8 && (((uintptr_t)text) & 15) == 0;
+  if (fast) {
+    const uint8_t* t = (const uint8_t*)text;
+    const size_t sb = (size_t)HIST_WARPS * ((((size_t)1 << w) + 1) / 2) * 32 * 4;
+    const int hb = sm_count() * 3;
+    const int dshift = w - K0;
+    const int nd0 = 1 << K0;
+#define WVLT_H8(WW)                                                                                         \
+  do {                                                                                                      \
+    static bool set = false;                                                                                \
+    if (!set) {                                                                                             \
+      cudaFuncSetAttribute(hist_u8_kernel<WW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);       \
+      set = true;                                                                                           \
+    }                                                                                                       \
+    hist_u8_kernel<WW><<<hb, HIST_WARPS * 32, sb, s>>>(t, n, dshift, nd0, hist, tcnt0, ntiles0, status);    \
+  } while (0)
+    switch (w) {
+      case 1: WVLT_H8(1); break;
+      case 2: WVLT_H8(2); break;
+      case 3: WVLT_H8(3); break;
+      case 4: WVLT_H8(4); break;
+      case 5: WVLT_H8(5); break;
+      case 6: WVLT_H8(6); break;
+      case 7: WVLT_H8(7); break;
+      default: WVLT_H8(8); break;
+    }
+#undef WVLT_H8
+    return cudaGetLastError();
+  }
+  cudaError_t e = launch_hist_generic(text, sym_bytes, n, w, hist, status, s);
+  if (e != cudaSuccess) return e;
+  const int blocks = sm_count() * 8;
+  digits_kernel<<<blocks, 256, 0, s>>>(text, sym_bytes, n, tile0, w - K0, 1 << K0, ntiles0, tcnt0);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scan(const uint32_t* cnt, int K, int64_t ntiles, int64_t* bsum, int64_t* pre, cudaStream_t s) {
+  const int64_t nblk = (ntiles + SCAN_TILE - 1) / SCAN_TILE;
+  dim3 g((unsigned)nblk, 1u << K);
+  scan_reduce_kernel<<<g, SCAN_THREADS, 0, s>>>(cnt, ntiles, nblk, bsum);
+  scan_apply_kernel<<<g, SCAN_THREADS, 0, s>>>(cnt, ntiles, nblk, bsum, pre);
+  return cudaGetLastError();
+}
+
+// optional per-stage CUDA-event timing of wvlt_build_device (bench / profiling)
+constexpr int PROF_MAX = 3 + 2 * MAXP + 1;
+struct Prof {
+  bool on = false;
+  int n = 0;
+  int ids[PROF_MAX];
+  cudaEvent_t ev[PROF_MAX + 1];
+  bool created = false;
+};
+thread_local Prof g_prof;
+
+void prof_mark(cudaStream_t s, int stage_id) {
+  Prof& P = g_prof;
+  if (!P.on || P.n > PROF_MAX) return;
+  if (!P.created) {
+    for (int i = 0; i <= PROF_MAX; ++i) cudaEventCreate(&P.ev[i]);
+    P.created = true;
+  }
+  if (stage_id >= 0 && P.n > 0) P.ids[P.n - 1] = stage_id;
+  cudaEventRecord(P.ev[P.n], s);
+  ++P.n;
 }
 
 }  // namespace
@@ -1049,6 +1274,27 @@ const char* wvlt_error_string(int code) {
 
 int wvlt_code_width(int64_t sigma) { return code_width_host(sigma); }
 
+int wvlt_profile_enable(int on) {
+  g_prof.on = on != 0;
+  g_prof.n = 0;
+  return 0;
+}
+
+int wvlt_profile_read(float* stage_ms, int* stage_ids, int max_stages) {
+  Prof& P = g_prof;
+  if (!P.on || P.n < 2) return 0;
+  cudaError_t e = cudaEventSynchronize(P.ev[P.n - 1]);
+  if (e != cudaSuccess) return -(int)e;
+  int k = 0;
+  for (int i = 0; i + 1 < P.n && k < max_stages; ++i, ++k) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, P.ev[i], P.ev[i + 1]);
+    if (stage_ms) stage_ms[k] = ms;
+    if (stage_ids) stage_ids[k] = P.ids[i];
+  }
+  return k;
+}
+
 size_t wvlt_workspace_bytes(int64_t n, int sym_bytes, int64_t sigma, int kind) {
   Plan P;
   if (n < 0 || !(sym_bytes == 1 || sym_bytes == 2 || sym_bytes == 4)) return 0;
@@ -1066,12 +1312,7 @@ int wvlt_histogram(const void* text, int sym_bytes, int64_t n, int64_t sigma, in
   cudaError_t e = cudaMemsetAsync(hist, 0, ((size_t)1 << w) * 8, s);
   if (e != cudaSuccess) return (int)e;
   if (n == 0) return 0;
-  if (w == 0) {  // a single bin holding every symbol; range = all zero
-    int32_t* st = status;
-    e = launch_hist(text, sym_bytes, n, 0, (unsigned long long*)hist, st, s);
-    return (int)e;
-  }
-  e = launch_hist(text, sym_bytes, n, w, (unsigned long long*)hist, status, s);
+  e = launch_hist_generic(text, sym_bytes, n, w, (unsigned long long*)hist, status, s);
   return (int)e;
 }
 
@@ -1104,12 +1345,12 @@ int wvlt_build_device(const void* text, int sym_bytes, int64_t n, int64_t sigma,
       e = cudaMemsetAsync(zeros, 0, (size_t)w * 8, s);
       if (e != cudaSuccess) return (int)e;
     }
-    if (w > 0 && borders && w >= 2) {
+    if (w >= 2 && borders) {
       e = cudaMemsetAsync(borders, 0, (((size_t)1 << w) - 2) * 8, s);
       if (e != cudaSuccess) return (int)e;
     }
     if (w == 0 && n > 0 && status) {  // range check still applies: every symbol must be 0
-      e = launch_hist(text, sym_bytes, n, 0, nullptr, status, s);
+      e = launch_hist_generic(text, sym_bytes, n, 0, nullptr, status, s);
       if (e != cudaSuccess) return (int)e;
     }
     return 0;
@@ -1121,21 +1362,39 @@ int wvlt_build_device(const void* text, int sym_bytes, int64_t n, int64_t sigma,
   int64_t* wtstart = (int64_t*)(ws + P.off_wtstart);
   int64_t* wm_base = (int64_t*)(ws + P.off_wmbase);
   int64_t* corr = (int64_t*)(ws + P.off_corr);
-  uint32_t* counters = (uint32_t*)(ws + P.off_counter);
-  uint64_t* stat = (uint64_t*)(ws + P.off_status);
+  int64_t* bsum = (int64_t*)(ws + P.off_bsum);
   void* bufs[2] = {ws + P.off_buf0, ws + P.off_buf1};
-  int32_t* st_flag = status;
-  if (!st_flag) st_flag = (int32_t*)(counters + MAXP);  // scratch status word
+  int32_t* st_flag = status ? status : (int32_t*)(ws + P.off_scratch);
 
+  g_prof.n = 0;
+  prof_mark(s, -1);
   e = cudaMemsetAsync(level_words, 0, (size_t)w * nwords * 8, s);
   if (e != cudaSuccess) return (int)e;
-  e = cudaMemsetAsync(stat, 0, P.status_bytes, s);
+  e = cudaMemsetAsync(ws + P.off_tcnt[0], 0, P.tcnt_bytes, s);
   if (e != cudaSuccess) return (int)e;
   unsigned long long* hw = (unsigned long long*)(chain + chain_off(w));
   e = cudaMemsetAsync(hw, 0, ((size_t)1 << w) * 8, s);
   if (e != cudaSuccess) return (int)e;
-  e = launch_hist(text, sym_bytes, n, w, hw, st_flag, s);
+  if (!status) {
+    e = cudaMemsetAsync(st_flag, 0, 4, s);
+    if (e != cudaSuccess) return (int)e;
+  }
+  const void* src0 = text;
+  if (P.widen_bytes) {
+    void* wide = ws + P.off_wide;
+    const int blocks = sm_count() * 8;
+    if (P.widen_bytes == 2) widen_kernel<uint8_t, uint16_t><<<blocks, 256, 0, s>>>((const uint8_t*)text, (uint16_t*)wide, n);
+    else if (sym_bytes == 1) widen_kernel<uint8_t, uint32_t><<<blocks, 256, 0, s>>>((const uint8_t*)text, (uint32_t*)wide, n);
+    else widen_kernel<uint16_t, uint32_t><<<blocks, 256, 0, s>>>((const uint16_t*)text, (uint32_t*)wide, n);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return (int)e;
+    src0 = wide;
+  }
+  prof_mark(s, WVLT_STAGE_MEMSET);
+  e = launch_hist_build(src0, P.in_bytes[0], n, w, P.K[0], P.tile[0], P.ntiles[0], hw,
+                        (uint32_t*)(ws + P.off_tcnt[0]), st_flag, s);
   if (e != cudaSuccess) return (int)e;
+  prof_mark(s, WVLT_STAGE_HIST);
 
   TablesArgs ta;
   memset(&ta, 0, sizeof(ta));
@@ -1147,7 +1406,6 @@ int wvlt_build_device(const void* text, int sym_bytes, int64_t n, int64_t sigma,
   ta.wtstart = wtstart;
   ta.wm_base = wm_base;
   ta.corr = corr;
-  ta.counters = counters;
   ta.zeros_out = zeros;
   ta.hist_out = hist;
   ta.borders_out = (w >= 2) ? borders : nullptr;
@@ -1155,9 +1413,15 @@ int wvlt_build_device(const void* text, int sym_bytes, int64_t n, int64_t sigma,
   tables_kernel<<<1, TAB_THREADS, 0, s>>>(ta);
   e = cudaGetLastError();
   if (e != cudaSuccess) return (int)e;
+  prof_mark(s, WVLT_STAGE_TABLES);
 
-  const void* cur = text;
+  const void* cur = src0;
   for (int p = 0; p < P.npass; ++p) {
+    uint32_t* tcnt = (uint32_t*)(ws + P.off_tcnt[p]);
+    int64_t* tpre = (int64_t*)(ws + P.off_tpre[p]);
+    e = launch_scan(tcnt, P.K[p], P.ntiles[p], bsum, tpre, s);
+    if (e != cudaSuccess) return (int)e;
+    prof_mark(s, WVLT_STAGE_SCAN0 + p);
     PassArgs pa;
     memset(&pa, 0, sizeof(pa));
     pa.src = cur;
@@ -1165,18 +1429,25 @@ int wvlt_build_device(const void* text, int sym_bytes, int64_t n, int64_t sigma,
     pa.words = level_words;
     pa.nwords = nwords;
     pa.n = n;
+    pa.ntiles = P.ntiles[p];
     pa.level = P.lvl[p];
     pa.width = w;
     pa.kind = kind;
     pa.has_out = P.out_bytes[p] ? 1 : 0;
-    pa.status = stat;
-    pa.counter = counters + p;
-    pa.epoch = (unsigned)(p + 1);
+    pa.tcnt = tcnt;
+    pa.tpre = tpre;
+    if (pa.has_out) {
+      pa.ncnt = (uint32_t*)(ws + P.off_tcnt[p + 1]);
+      pa.nntiles = P.ntiles[p + 1];
+      pa.ntshift = P.tshift[p + 1];
+      pa.nK = P.K[p + 1];
+    }
     pa.wm_base = wm_base + (int64_t)p * (KMAX + 1) * NDIG;
     pa.corr = corr;
     for (int j = 0; j <= KMAX; ++j) pa.corr_off[j] = P.corr_off[p][j];
     e = launch_pass(P.in_bytes[p], P.out_bytes[p], P.K[p], pa, P.ntiles[p], s);
     if (e != cudaSuccess) return (int)e;
+    prof_mark(s, WVLT_STAGE_PASS0 + p);
     cur = pa.dst;
   }
   return 0;
