@@ -77,8 +77,43 @@ __host__ __device__ __forceinline__ unsigned rev_bits(unsigned d, int j) {  // j
 #endif
 }
 
+// Keep a value opaque to the optimizer (so `x & mask` stays one LOP3 with a
+// predicate output instead of being rewritten into shift/and/compare).
+__device__ __forceinline__ uint32_t opaque(uint32_t v) {
+  asm volatile("mov.b32 %0, %0;" : "+r"(v));
+  return v;
+}
+
+// Two-stream split store: `one ? smem[a1] = v : smem[a0] = v` as two predicated
+// st.shared, so the zeros and the ones stream (each contiguous) are separate
+// conflict-free wavefronts instead of one store with a selected address.
+__device__ __forceinline__ void st_split_u8(uint32_t a1, uint32_t a0, uint32_t one, uint32_t v) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p st.shared.u8 [%0], %3;\n\t@!p st.shared.u8 [%1], %3;\n\t}"
+      ::"r"(a1), "r"(a0), "r"(one), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_split_u16(uint32_t a1, uint32_t a0, uint32_t one, uint32_t v) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p st.shared.u16 [%0], %3;\n\t@!p st.shared.u16 [%1], %3;\n\t}"
+      ::"r"(a1), "r"(a0), "r"(one), "h"((unsigned short)v) : "memory");
+}
+__device__ __forceinline__ void st_split_u32(uint32_t a1, uint32_t a0, uint32_t one, uint32_t v) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p st.shared.u32 [%0], %3;\n\t@!p st.shared.u32 [%1], %3;\n\t}"
+      ::"r"(a1), "r"(a0), "r"(one), "r"(v) : "memory");
+}
+template <typename T>
+__device__ __forceinline__ void st_split(uint32_t a1, uint32_t a0, uint32_t one, uint32_t v) {
+  if (sizeof(T) == 1) st_split_u8(a1, a0, one, v);
+  else if (sizeof(T) == 2) st_split_u16(a1, a0, one, v);
+  else st_split_u32(a1, a0, one, v);
+}
+
 __device__ __forceinline__ void bar_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(int id, int nthreads) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
 // ---------------------------------------------------------------------------
@@ -634,43 +669,6 @@ __device__ __forceinline__ uint64_t extract_bits(const uint32_t* L, int off, int
   return cnt >= 64 ? v : (v & ((1ull << cnt) - 1));
 }
 
-// Copy runs of the tile-local bit string L to the level's global words: run
-// r = local bits [ls[r], ls[r]+len[r]) -> global bits [gs[r], gs[r]+len[r]).
-// Whole destination words are stored; words shared with another run are OR-ed
-// into the pre-zeroed level (the "owner writes whole words" rule of
-// gather_bits, _kernels.py:197-205, relaxed to atomics at run edges).
-__device__ void emit_runs(const uint32_t* L, int R, const int* ls, const int* len, const int64_t* gs, uint64_t* gw,
-                          int* s_wpre) {
-  if (threadIdx.x == 0) {
-    int acc = 0;
-    for (int r = 0; r < R; ++r) {
-      s_wpre[r] = acc;
-      if (len[r]) acc += (int)(((gs[r] + len[r] - 1) >> 6) - (gs[r] >> 6) + 1);
-    }
-    s_wpre[R] = acc;
-  }
-  __syncthreads();
-  const int total = s_wpre[R];
-  for (int f = threadIdx.x; f < total; f += PASS_THREADS) {
-    int r = 0;
-    while (s_wpre[r + 1] <= f) ++r;
-    const int64_t g = gs[r];
-    const int64_t W = (g >> 6) + (f - s_wpre[r]);
-    const int64_t wb = W << 6;
-    const int64_t a0 = g > wb ? g : wb;
-    const int64_t e = g + len[r];
-    const int64_t b0 = e < wb + 64 ? e : wb + 64;
-    const int c = (int)(b0 - a0);
-    const int lo = (int)(a0 - wb);
-    const uint64_t v = extract_bits(L, ls[r] + (int)(a0 - g), c) << lo;
-    if (c == 64)
-      gw[W] = v;
-    else
-      atomicOr(reinterpret_cast<unsigned long long*>(gw + W), (unsigned long long)v);
-  }
-  __syncthreads();
-}
-
 template <typename TIn>
 __device__ __forceinline__ unsigned digit_of(TIn x, int top_shift, int j) {
   // LSD digit d_j = sum_{i<j} bit(top_shift - i) << i
@@ -680,12 +678,19 @@ __device__ __forceinline__ unsigned digit_of(TIn x, int top_shift, int j) {
 }
 
 // One CTA = one tile of T = 512 * E symbols of A_l; CTAs are independent.
+// Symbol p of the tile-local order lives in lane p % 32 of warp p / (32 E)
+// (warp-contiguous 32-symbol chunks), so a ballot gives 32 consecutive bits.
+// Warps 0..15 stage the tile and run the splits; warp 16 derives the tile's
+// placement tables concurrently (named barriers 1: compute warps, 2: tables
+// ready, 3: tile staged).
+constexpr int TAB_WARP_THREADS = 32;
 template <typename TIn, typename TOut, int K, int E>
-__global__ void __launch_bounds__(PASS_THREADS, 2) level_pass_kernel(const PassArgs a) {
+__global__ void __launch_bounds__(PASS_THREADS + TAB_WARP_THREADS, 2) level_pass_kernel(const PassArgs a) {
   using S = PassSmem<TIn, K, E>;
   constexpr int T = S::T;
   constexpr int NC = S::NC;
   constexpr int NW = PASS_THREADS / 32;
+  constexpr int ALLT = PASS_THREADS + TAB_WARP_THREADS;
   constexpr int nd = 1 << K;
   extern __shared__ __align__(16) unsigned char smem[];
   TIn* buf = reinterpret_cast<TIn*>(smem);
@@ -696,12 +701,11 @@ __global__ void __launch_bounds__(PASS_THREADS, 2) level_pass_kernel(const PassA
   __shared__ int s_ls[K + 1][NDIG];
   __shared__ int64_t s_lb[K + 1][NDIG];
   __shared__ int64_t s_gs[K + 1][NDIG];
-  __shared__ int64_t s_off[NDIG];  // output offset by numeric K-bit digit (uniform tiles)
-  __shared__ int64_t s_ft[NDIG];   // first next-pass tile of each output run (numeric digit)
-  __shared__ uint32_t s_ncnt[2 * NDIG][NDIG];  // next-pass digit counts per (run, next tile)
-  __shared__ int s_wpre[NDIG + 1];
+  __shared__ TOut* s_row[NDIG];   // uniform tiles: output row of each numeric digit (dst + offset)
+  __shared__ int s_thr[NDIG];     // local position where that run crosses into the next pass's next tile
+  __shared__ int64_t s_ft[NDIG];  // first next-pass tile of each run
+  __shared__ uint32_t s_ncnt[2 * NDIG * NDIG];  // next-pass digit counts per (run, next tile)
   __shared__ int s_q1;
-  __shared__ int64_t s_q;
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int w = a.width, l0 = a.level;
@@ -710,22 +714,12 @@ __global__ void __launch_bounds__(PASS_THREADS, 2) level_pass_kernel(const PassA
   const int64_t base = tile * T;
   const int cnt = (int)min((int64_t)T, a.n - base);
 
-  // ---- stage the tile (invalid tail slots = all ones so they sort last) ----
-  const TIn* src = reinterpret_cast<const TIn*>(a.src) + base;
-  if (cnt == T && ((((uintptr_t)src) & 15) == 0)) {
-    const uint4* s4 = reinterpret_cast<const uint4*>(src);
-    uint4* d4 = reinterpret_cast<uint4*>(buf);
-    for (int i = tid; i < (int)(T * sizeof(TIn) / 16); i += PASS_THREADS) d4[i] = __ldcs(s4 + i);
-  } else {
-    for (int p = tid; p < T; p += PASS_THREADS) buf[p] = p < cnt ? src[p] : (TIn)~(TIn)0;
-  }
-  if (tid < 2 * NDIG * NDIG) (&s_ncnt[0][0])[tid] = 0;
-  if (wid == 0) {
-    // tile digit counts / prefixes (numeric digit e = lane) -> per LSD digit d
+  if (wid == NW) {
+    // ========================= table warp =========================
     if (lane < nd) {
-      const int d = (int)rev_bits((unsigned)lane, K);
-      s_cnt[K][d] = (int)a.tcnt[(int64_t)lane * a.ntiles + tile];
-      s_lb[K][d] = a.tpre[(int64_t)lane * a.ntiles + tile];
+      const int d = (int)rev_bits((unsigned)lane, K);  // lane = numeric digit
+      s_cnt[K][d] = (int)__ldg(a.tcnt + (int64_t)lane * a.ntiles + tile);
+      s_lb[K][d] = __ldg(a.tpre + (int64_t)lane * a.ntiles + tile);
     }
     __syncwarp();
     // every shorter digit: sums over the digits sharing the low j bits
@@ -754,157 +748,166 @@ __global__ void __launch_bounds__(PASS_THREADS, 2) level_pass_kernel(const PassA
       }
       if (lane < mj) s_ls[j][lane] = incl - c;
     }
-  }
-  __syncthreads();
-  if (wid == 0) {
     bool q1 = true;
     int64_t q = 0;
     if (!wm) {
+      bar_sync(3, ALLT);  // tile staged
       const int sh = w - l0;
       const uint64_t qf = sh >= 32 ? 0 : ((uint64_t)(uint32_t)buf[0] >> sh);
       const uint64_t ql = sh >= 32 ? 0 : ((uint64_t)(uint32_t)buf[cnt - 1] >> sh);
       q1 = qf == ql;
       q = (int64_t)qf;
     }
-    if (lane == 0) {
-      s_q1 = q1;
-      s_q = q;
-    }
+    if (lane == 0) s_q1 = q1;
+    __syncwarp();
     if (q1) {  // placement is a per-digit constant in this tile
       for (int j = 1; j <= K; ++j) {
         if (lane < (1 << j)) {
           const int d = lane;
-          const int64_t tb = wm ? a.wm_base[j * NDIG + d]
-                                : a.corr[a.corr_off[j] + (q << j) + (int64_t)rev_bits((unsigned)d, j)];
+          const int64_t tb = wm ? __ldg(a.wm_base + j * NDIG + d)
+                                : __ldg(a.corr + a.corr_off[j] + (q << j) + (int64_t)rev_bits((unsigned)d, j));
           s_gs[j][d] = tb + s_lb[j][d];
         }
       }
       __syncwarp();
-      if (lane < nd) {
+      if (lane < nd && a.has_out) {
         const int d = (int)rev_bits((unsigned)lane, K);  // lane = numeric digit
-        s_off[lane] = s_gs[K][d] - s_ls[K][d];
-        s_ft[lane] = s_gs[K][d] >> a.ntshift;
+        const int64_t g = s_gs[K][d];
+        s_row[lane] = reinterpret_cast<TOut*>(a.dst) + (g - s_ls[K][d]);
+        const int64_t ntile = (int64_t)1 << a.ntshift;
+        s_thr[lane] = s_ls[K][d] + (int)(ntile - (g & (ntile - 1)));
+        s_ft[lane] = g >> a.ntshift;
       }
     }
+    __threadfence_block();
+    bar_arrive(2, ALLT);
+    return;
   }
-  __syncthreads();
+
+  // ========================== compute warps ==========================
+  // ---- stage the tile (invalid tail slots = all ones so they sort last) ----
+  const TIn* src = reinterpret_cast<const TIn*>(a.src) + base;
+  if (cnt == T && ((((uintptr_t)src) & 15) == 0)) {
+    const uint4* s4 = reinterpret_cast<const uint4*>(src);
+    uint4* d4 = reinterpret_cast<uint4*>(buf);
+#pragma unroll
+    for (int i = tid; i < (int)(T * sizeof(TIn) / 16); i += PASS_THREADS) d4[i] = __ldcs(s4 + i);
+  } else {
+    for (int p = tid; p < T; p += PASS_THREADS) buf[p] = p < cnt ? src[p] : (TIn)~(TIn)0;
+  }
+  if (tid < 2 * NDIG * NDIG) s_ncnt[tid] = 0;
+  bar_sync(1, PASS_THREADS);
+  if (!wm) bar_arrive(3, ALLT);
 
   const unsigned lt = lanemask_lt();
   const int pbase = wid * E * 32;  // this warp's first symbol (warp-contiguous chunks)
-  TIn x[E];
   uint32_t m[E];
 
 #pragma unroll 1
   for (int j = 0; j < K; ++j) {
-    const int sh = w - 1 - l0 - j;
+    const uint32_t bmask = opaque(1u << (w - 1 - l0 - j));
     const TIn* cur = buf + (size_t)j * T;
 #pragma unroll
-    for (int e = 0; e < E; ++e) {
-      x[e] = cur[pbase + e * 32 + lane];
-      m[e] = __ballot_sync(FULL, ((uint32_t)x[e] >> sh) & 1u);
-    }
-    // this level's ballot words: lane e keeps m[e]
-    uint32_t mine = 0;
-#pragma unroll
-    for (int e = 0; e < E; ++e)
-      if (lane == e) mine = m[e];
+    for (int e = 0; e < E; ++e) m[e] = __ballot_sync(FULL, (uint32_t)cur[pbase + e * 32 + lane] & bmask);
     if (j == 0) {
       // level l0 is in global order already: aligned word stores
-      uint32_t* g32 = reinterpret_cast<uint32_t*>(a.words + (int64_t)l0 * a.nwords);
-      const int64_t lim = 2 * a.nwords;
-      if (lane < E) {
-        const int c = wid * E + lane;
-        const int64_t gi = (base >> 5) + c;
-        if (gi < lim) {
-          const int first = c * 32;
+      uint32_t* g32 = reinterpret_cast<uint32_t*>(a.words + (int64_t)l0 * a.nwords) + (base >> 5) + wid * E;
+      if (cnt == T) {
+        if (lane == 0) {
+#pragma unroll
+          for (int q4 = 0; q4 < E / 4; ++q4)
+            reinterpret_cast<uint4*>(g32)[q4] = make_uint4(m[4 * q4], m[4 * q4 + 1], m[4 * q4 + 2], m[4 * q4 + 3]);
+        }
+      } else {
+        uint32_t mine = 0;
+#pragma unroll
+        for (int e = 0; e < E; ++e)
+          if (lane == e) mine = m[e];
+        const int64_t lim = 2 * a.nwords - ((base >> 5) + wid * E);
+        if (lane < E && lane < lim) {
+          const int first = (wid * E + lane) * 32;
           uint32_t v = mine;
           if (first + 32 > cnt) v = first >= cnt ? 0u : (v & ((1u << (cnt - first)) - 1u));
-          g32[gi] = v;
+          g32[lane] = v;
         }
       }
-    } else if (lane < E) {
-      bits[j * (NC + 4) + wid * E + lane] = mine;
+    } else if (lane == 0) {
+      uint4* b4 = reinterpret_cast<uint4*>(bits + j * (NC + 4) + wid * E);
+#pragma unroll
+      for (int q4 = 0; q4 < E / 4; ++q4) b4[q4] = make_uint4(m[4 * q4], m[4 * q4 + 1], m[4 * q4 + 2], m[4 * q4 + 3]);
     }
-    const bool scatter = (j + 1 < K) || a.has_out;
-    if (!scatter) break;
-    // warp-local chunk prefixes in registers, CTA-wide warp prefix via smem
-    uint32_t wtot = 0;
+    if (j + 1 == K && !a.has_out) break;
+    // chunk prefixes inside the warp (warp-uniform) and the CTA-wide warp prefix
+    uint32_t run = 0;
 #pragma unroll
-    for (int e = 0; e < E; ++e) wtot += __popc(m[e]);
-    if (lane == 0) s_wtot[j & 1][wid] = wtot;
-    __syncthreads();
-    uint32_t wpre = 0, tot = 0;
-#pragma unroll
-    for (int q4 = 0; q4 < NW / 4; ++q4) {
-      const uint4 v = reinterpret_cast<const uint4*>(s_wtot[j & 1])[q4];
-      const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        wpre += (q4 * 4 + k) < wid ? vv[k] : 0u;
-        tot += vv[k];
-      }
-    }
-    const int Z = T - (int)tot;
-    uint32_t r = wpre;
+    for (int e = 0; e < E; ++e) run += __popc(m[e]);
+    if (lane == 0) s_wtot[j & 1][wid] = run;
+    bar_sync(1, PASS_THREADS);
+    const uint32_t wv = lane < NW ? s_wtot[j & 1][lane] : 0u;
+    const uint32_t wpre = __reduce_add_sync(FULL, lane < wid ? wv : 0u);
+    const uint32_t tot = __reduce_add_sync(FULL, wv);
+    // ones of chunk e go to U1 + c[e] + rank, zeros to U0 + 32 e - c[e] - rank
+    const int U1 = T - (int)tot + (int)wpre;
+    const int U0 = pbase + lane - (int)wpre;
     if (j + 1 < K) {
-      TIn* nxt = buf + (size_t)(j + 1) * T;
+      const uint32_t nxt = (uint32_t)__cvta_generic_to_shared(buf + (size_t)(j + 1) * T);
+      int ce = 0;  // ones in this warp's earlier chunks
 #pragma unroll
       for (int e = 0; e < E; ++e) {
-        const int p = pbase + e * 32 + lane;
-        const int r1 = (int)r + __popc(m[e] & lt);
-        const int dst = ((m[e] >> lane) & 1u) ? Z + r1 : p - r1;
-        nxt[dst] = x[e];
-        r += __popc(m[e]);
+        const uint32_t xv = (uint32_t)cur[pbase + e * 32 + lane];  // reload: LSU has slack, registers do not
+        const int r = __popc(m[e] & lt);
+        st_split<TIn>(nxt + (uint32_t)(U1 + ce + r) * (uint32_t)sizeof(TIn),
+                      nxt + (uint32_t)(U0 + 32 * e - ce - r) * (uint32_t)sizeof(TIn), xv & bmask, xv);
+        ce += __popc(m[e]);
       }
-      __syncthreads();
+      bar_sync(1, PASS_THREADS);
     } else {
       // last split: straight to HBM, counting the next pass's digits per (run, next tile)
-      TOut* dst = reinterpret_cast<TOut*>(a.dst);
+      bar_sync(2, ALLT);  // placement tables
       const uint32_t keep = wm ? ((w - l0 - K) >= 32 ? FULL : ((1u << (w - l0 - K)) - 1u)) : FULL;
       const int eshift = w - l0 - K;
       const int nshift = w - l0 - K - a.nK;  // next pass digit = bits l0+K .. l0+K+nK-1
       const unsigned nmask = (1u << a.nK) - 1u;
+      int ce = 0;
       if (s_q1) {
 #pragma unroll
         for (int e = 0; e < E; ++e) {
-          const int p = pbase + e * 32 + lane;
-          const int r1 = (int)r + __popc(m[e] & lt);
-          const int pos = ((m[e] >> lane) & 1u) ? Z + r1 : p - r1;
+          const int r = __popc(m[e] & lt);
+          const uint32_t xv = (uint32_t)cur[pbase + e * 32 + lane];
+          const int pos = (xv & bmask) ? U1 + ce + r : U0 + 32 * e - ce - r;
+          ce += __popc(m[e]);
           if (pos < cnt) {
-            const uint32_t xv = (uint32_t)x[e];
             const unsigned dig = (xv >> eshift) & (nd - 1);
-            const int64_t gpos = s_off[dig] + pos;
-            dst[gpos] = (TOut)(xv & keep);
-            const int h = (int)((gpos >> a.ntshift) - s_ft[dig]);
-            atomicAdd(&s_ncnt[2 * dig + h][(xv >> nshift) & nmask], 1u);
+            s_row[dig][pos] = (TOut)(xv & keep);
+            const unsigned h = pos >= s_thr[dig] ? 1u : 0u;
+            atomicAdd(&s_ncnt[(((dig << 1) | h) << a.nK) | ((xv >> nshift) & nmask)], 1u);
           }
-          r += __popc(m[e]);
         }
       } else {
+        TOut* dst = reinterpret_cast<TOut*>(a.dst);
         const int64_t* ctab = a.corr + a.corr_off[K];
 #pragma unroll
         for (int e = 0; e < E; ++e) {
-          const int p = pbase + e * 32 + lane;
-          const int r1 = (int)r + __popc(m[e] & lt);
-          const int pos = ((m[e] >> lane) & 1u) ? Z + r1 : p - r1;
+          const int r = __popc(m[e] & lt);
+          const uint32_t xv = (uint32_t)cur[pbase + e * 32 + lane];
+          const int pos = (xv & bmask) ? U1 + ce + r : U0 + 32 * e - ce - r;
+          ce += __popc(m[e]);
           if (pos < cnt) {
-            const uint32_t xv = (uint32_t)x[e];
             const unsigned d = rev_bits((xv >> eshift) & (nd - 1), K);
             const uint64_t P = eshift >= 32 ? 0 : ((uint64_t)xv >> eshift);
             const int64_t gpos = ctab[P] + s_lb[K][d] + pos - s_ls[K][d];
             dst[gpos] = (TOut)(xv & keep);
             atomicAdd(&a.ncnt[(int64_t)((xv >> nshift) & nmask) * a.nntiles + (gpos >> a.ntshift)], 1u);
           }
-          r += __popc(m[e]);
         }
       }
-      __syncthreads();
+      bar_sync(1, PASS_THREADS);
       if (s_q1) {
-        const int ncount = 2 * nd * (1 << a.nK);
+        const int ncount = 2 * nd << a.nK;
         for (int i = tid; i < ncount; i += PASS_THREADS) {
-          const int slot = i >> a.nK, ne = i & (int)nmask;
-          const uint32_t v = s_ncnt[slot][ne];
+          const uint32_t v = s_ncnt[i];
           if (v) {
+            const int slot = i >> a.nK, ne = i & (int)nmask;
             const int64_t nt = s_ft[slot >> 1] + (slot & 1);
             atomicAdd(&a.ncnt[(int64_t)ne * a.nntiles + nt], v);
           }
@@ -912,19 +915,43 @@ __global__ void __launch_bounds__(PASS_THREADS, 2) level_pass_kernel(const PassA
       }
     }
   }
+  if (!a.has_out) {
+    bar_sync(1, PASS_THREADS);  // every warp's ballot words are stored
+    bar_sync(2, ALLT);          // placement tables
+  }
 
   // ---- emit levels l0+1 .. l0+K-1 ----
-  const bool uniform = s_q1;
+  if (s_q1) {
+    // one warp per (level j, run r): task t = 2^j - 2 + r
+    for (int t = wid; t < nd - 2; t += NW) {
+      const int j = 31 - __clz(t + 2);
+      const int r = t + 2 - (1 << j);
+      const int len = s_cnt[j][r];
+      if (!len) continue;
+      const int64_t g = s_gs[j][r];
+      const int ls = s_ls[j][r];
+      const uint32_t* L = bits + j * (NC + 4);
+      uint64_t* gw = a.words + (int64_t)(l0 + j) * a.nwords;
+      const int64_t W0 = g >> 6, W1 = (g + len - 1) >> 6;
+      for (int64_t W = W0 + lane; W <= W1; W += 32) {
+        const int64_t wb = W << 6;
+        const int64_t a0 = g > wb ? g : wb;
+        const int64_t e0 = g + len;
+        const int64_t b0 = e0 < wb + 64 ? e0 : wb + 64;
+        const int c = (int)(b0 - a0);
+        const uint64_t v = extract_bits(L, ls + (int)(a0 - g), c) << (int)(a0 - wb);
+        if (c == 64)
+          gw[W] = v;
+        else
+          atomicOr(reinterpret_cast<unsigned long long*>(gw + W), (unsigned long long)v);
+      }
+    }
+  } else {
+    // WT tile spanning several nodes: per-symbol placement, runs found by
+    // contiguity of the global position inside each warp chunk
 #pragma unroll 1
-  for (int j = 1; j < K; ++j) {
-    const int mj = 1 << j;
-    uint64_t* gw = a.words + (int64_t)(l0 + j) * a.nwords;
-    const uint32_t* L = bits + j * (NC + 4);
-    if (uniform) {
-      emit_runs(L, mj, s_ls[j], s_cnt[j], s_gs[j], gw, s_wpre);
-    } else {
-      // WT tile spanning several nodes: per-symbol placement, runs found by
-      // contiguity of the global position inside each warp chunk
+    for (int j = 1; j < K; ++j) {
+      uint64_t* gw = a.words + (int64_t)(l0 + j) * a.nwords;
       const TIn* cur = buf + (size_t)j * T;
       const int tshift = w - 1 - l0;
       const int pshift = w - l0 - j;
@@ -967,6 +994,7 @@ __global__ void __launch_bounds__(PASS_THREADS, 2) level_pass_kernel(const PassA
   }
 }
 
+// ---------------------------------------------------------------------------
 // K5: merge (gather_bits)
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) merge_bits_kernel(uint64_t* __restrict__ dst, int64_t wlo, int64_t whi,
@@ -1122,7 +1150,7 @@ cudaError_t launch_pass_t(const PassArgs& a, int64_t ntiles, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  kern<<<(unsigned)ntiles, PASS_THREADS, S::total, s>>>(a);
+  kern<<<(unsigned)ntiles, PASS_THREADS + TAB_WARP_THREADS, S::total, s>>>(a);
   return cudaGetLastError();
 }
 
