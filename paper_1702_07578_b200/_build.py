@@ -30,6 +30,7 @@ NVCC_FLAGS = [
     "-shared", "-Xcompiler", "-fPIC",
     "--expt-relaxed-constexpr",
 ]
+EXTRA_FLAGS = os.environ.get("WVLT_NVCC_EXTRA", "").split()
 
 
 def nvcc_path() -> str:
@@ -50,7 +51,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     if not force and not is_stale():
         return LIB_PATH
     tmp = LIB_PATH.with_suffix(".so.tmp")
-    cmd = [nvcc_path(), *NVCC_FLAGS, f"-I{INCLUDE}", *map(str, SOURCES), "-o", str(tmp), "-lcudart"]
+    cmd = [nvcc_path(), *NVCC_FLAGS, *EXTRA_FLAGS, f"-I{INCLUDE}", *map(str, SOURCES), "-o", str(tmp), "-lcudart"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     log = PKG_DIR / "csrc" / "build.log"
     log.write_text(" ".join(cmd) + "\n\n" + res.stdout + res.stderr)

@@ -127,36 +127,60 @@ __device__ __forceinline__ void bar_arrive(int id, int nthreads) {
 // running totals in registers for the global histogram.
 // ---------------------------------------------------------------------------
 constexpr int HIST_WARPS = 4;
-constexpr int TILE_U8 = PASS_THREADS * 16;  // tile of pass 0 for byte symbols
+#ifndef WVLT_E_SMALL
+#define WVLT_E_SMALL 16
+#endif
+constexpr int E_SMALL = WVLT_E_SMALL;  // symbols per thread per split for 1-2 byte symbols
+constexpr int TILE_U8 = PASS_THREADS * E_SMALL;  // tile of pass 0 for byte symbols
 
 template <int W>
 __global__ void __launch_bounds__(HIST_WARPS * 32) hist_u8_kernel(const uint8_t* __restrict__ text, int64_t n,
-                                                                 int dshift, int nd0,
+                                                                 int dshift_unused, int nd0,
                                                                  unsigned long long* __restrict__ hist,
                                                                  uint32_t* __restrict__ tcnt0, int64_t ntiles,
                                                                  int32_t* __restrict__ status) {
   constexpr int NB = 1 << W;
   constexpr int NPAIR = (NB + 1) / 2;
-  constexpr int WORDS = NPAIR * 32;              // per warp
-  constexpr int PER = (NPAIR + 31) / 32;         // pairs per lane
+  constexpr int WORDS = NPAIR * 32;  // per warp
+  constexpr int K0 = W < KMAX ? W : KMAX;
+  constexpr int DSH = W - K0;        // pass-0 digit = bin >> DSH
+  constexpr int ND = 1 << K0;
+  constexpr int FLUSH_TILES = 128;   // 128 * 256 increments per lane counter < 2^16
   extern __shared__ __align__(16) uint32_t s_cols[];
-  __shared__ uint32_t s_dig[HIST_WARPS][NDIG];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   uint32_t* c32 = s_cols + (size_t)wid * WORDS;
   for (int i = lane; i < WORDS; i += 32) c32[i] = 0;
-  if (lane < NDIG) s_dig[wid][lane] = 0;
   __syncwarp();
   // byte address of this lane's counter for bin v: ((v >> 1) * 32 + lane) * 4 + (v & 1) * 2
   //   = 2 v + 124 (v >> 1) + 4 lane
   unsigned char* cbase = reinterpret_cast<unsigned char*>(c32) + 4 * lane;
-  uint32_t prev[PER][2], tot[PER][2];
+  uint32_t* c32w = c32 + lane;
+  uint32_t prev[ND];  // this lane's column sums per digit at the previous tile (mod 2^16)
 #pragma unroll
-  for (int i = 0; i < PER; ++i) prev[i][0] = prev[i][1] = tot[i][0] = tot[i][1] = 0;
+  for (int d = 0; d < ND; ++d) prev[d] = 0;
   uint32_t bad = 0;
   const uint32_t badmask = ((0xFFu << W) & 0xFFu) * 0x01010101u;
   const bool aligned = (((uintptr_t)text) & 15) == 0;
   const int64_t gw = (int64_t)blockIdx.x * HIST_WARPS + wid;
   const int64_t nwarps = (int64_t)gridDim.x * HIST_WARPS;
+  int since = 0;
+  auto flush = [&]() {
+    // exact bin totals since the last flush: column sums per pair
+    for (int pr = 0; pr < NPAIR; ++pr) {
+      const uint32_t wv = c32[pr * 32 + lane];
+      const uint32_t lo = __reduce_add_sync(FULL, wv & 0xFFFFu);
+      const uint32_t hi = __reduce_add_sync(FULL, wv >> 16);
+      if (lane == 0) {
+        if (lo) atomicAdd(&hist[2 * pr], (unsigned long long)lo);
+        if (hi && 2 * pr + 1 < NB) atomicAdd(&hist[2 * pr + 1], (unsigned long long)hi);
+      }
+    }
+    __syncwarp();
+    for (int i = lane; i < WORDS; i += 32) c32[i] = 0;
+#pragma unroll
+    for (int d = 0; d < ND; ++d) prev[d] = 0;
+    __syncwarp();
+  };
   for (int64_t t = gw; t < ntiles; t += nwarps) {
     const int64_t first = t * TILE_U8;
     const int cnt = (int)min((int64_t)TILE_U8, n - first);
@@ -175,9 +199,10 @@ __global__ void __launch_bounds__(HIST_WARPS * 32) hist_u8_kernel(const uint8_t*
             if (W < 8) bad |= wd[u] & badmask;
 #pragma unroll
             for (int b = 0; b < 4; ++b) {
+              // fire-and-forget shared atomic on the packed counter word: no
+              // load->store dependency chain between consecutive symbols
               const uint32_t v = __byte_perm(wd[u], 0, 0x4440 + b) & (NB - 1);
-              uint16_t* ctr = reinterpret_cast<uint16_t*>(cbase + 2 * v + 124 * (v >> 1));
-              *ctr = (uint16_t)(*ctr + 1);
+              atomicAdd(c32w + (v >> 1) * 32, 1u + (v & 1u) * 0xFFFFu);
             }
           }
         }
@@ -194,43 +219,35 @@ __global__ void __launch_bounds__(HIST_WARPS * 32) hist_u8_kernel(const uint8_t*
       }
     }
     __syncwarp();
-    // column sums of this lane's pairs -> the tile's bin counts
+    // the tile's pass-0 digit counts: each lane sums its own column per digit
+    // (conflict-free), differences to the previous tile, one reduction per digit
+    uint32_t acc[ND];
 #pragma unroll
-    for (int i = 0; i < PER; ++i) {
-      const int pr = lane + 32 * i;
-      if (pr < NPAIR) {
-        const uint4* col = reinterpret_cast<const uint4*>(c32 + pr * 32);
-        uint32_t lo = 0, hi = 0;
+    for (int d = 0; d < ND; ++d) acc[d] = 0;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const uint4 q = col[k];
-          lo += (q.x & 0xFFFFu) + (q.y & 0xFFFFu) + (q.z & 0xFFFFu) + (q.w & 0xFFFFu);
-          hi += (q.x >> 16) + (q.y >> 16) + (q.z >> 16) + (q.w >> 16);
-        }
-        const uint32_t d0 = (lo - prev[i][0]) & 0xFFFFu, d1 = (hi - prev[i][1]) & 0xFFFFu;
-        prev[i][0] = lo;
-        prev[i][1] = hi;
-        tot[i][0] += d0;
-        tot[i][1] += d1;
-        if (d0) atomicAdd(&s_dig[wid][(2 * pr) >> dshift], d0);
-        if (d1 && 2 * pr + 1 < NB) atomicAdd(&s_dig[wid][(2 * pr + 1) >> dshift], d1);
+    for (int pr = 0; pr < NPAIR; ++pr) {
+      const uint32_t wv = c32[pr * 32 + lane];
+      if (DSH >= 1) {
+        acc[(2 * pr) >> DSH] += (wv & 0xFFFFu) + (wv >> 16);
+      } else {
+        acc[2 * pr] += wv & 0xFFFFu;
+        if (2 * pr + 1 < NB) acc[2 * pr + 1] += wv >> 16;
       }
     }
-    __syncwarp();
-    if (lane < nd0) {
-      tcnt0[(int64_t)lane * ntiles + t] = s_dig[wid][lane];
-      s_dig[wid][lane] = 0;
-    }
-    __syncwarp();
-  }
 #pragma unroll
-  for (int i = 0; i < PER; ++i) {
-    const int pr = lane + 32 * i;
-    if (pr < NPAIR) {
-      if (tot[i][0]) atomicAdd(&hist[2 * pr], (unsigned long long)tot[i][0]);
-      if (tot[i][1] && 2 * pr + 1 < NB) atomicAdd(&hist[2 * pr + 1], (unsigned long long)tot[i][1]);
+    for (int d = 0; d < ND; ++d) {
+      const uint32_t delta = (acc[d] - prev[d]) & 0xFFFFu;
+      prev[d] = acc[d];
+      const uint32_t c = __reduce_add_sync(FULL, delta);
+      if (lane == d) tcnt0[(int64_t)d * ntiles + t] = c;
+    }
+    if (++since == FLUSH_TILES) {
+      flush();
+      since = 0;
     }
   }
+  flush();
+  (void)nd0;
   if (bad) atomicOr(status, WVLT_STATUS_RANGE);
 }
 
@@ -677,12 +694,183 @@ __device__ __forceinline__ unsigned digit_of(TIn x, int top_shift, int j) {
   return d;
 }
 
+// Per-tile placement tables, built by the table warp while the compute warps
+// run the splits.
+template <typename TOut, int K>
+struct TileTables {
+  int cnt[K + 1][NDIG];     // group sizes per digit length j (LSD digit)
+  int ls[K + 1][NDIG];      // group starts in the tile-local order of length j
+  int64_t lb[K + 1][NDIG];  // symbols of earlier tiles with the same digit
+  int64_t gs[K + 1][NDIG];  // uniform tiles: global start of each group's run
+  TOut* row[NDIG];          // uniform tiles: output row of each numeric digit (dst + offset)
+  int thr[NDIG];            // local position where that run crosses into the next pass's next tile
+  int64_t ft[NDIG];         // first next-pass tile of each run
+  int q1;                   // tile lies inside one level-l node (always for WM)
+};
+
+template <typename TIn, typename TOut, int K>
+__device__ __forceinline__ void table_warp(const PassArgs& a, TileTables<TOut, K>& tt, const TIn* buf0, int64_t tile,
+                                           int cnt, int lane, int allt) {
+  constexpr int nd = 1 << K;
+  const int w = a.width, l0 = a.level;
+  const bool wm = a.kind == WVLT_KIND_WM;
+  if (lane < nd) {
+    const int d = (int)rev_bits((unsigned)lane, K);  // lane = numeric digit
+    tt.cnt[K][d] = (int)__ldg(a.tcnt + (int64_t)lane * a.ntiles + tile);
+    tt.lb[K][d] = __ldg(a.tpre + (int64_t)lane * a.ntiles + tile);
+  }
+  __syncwarp();
+  // every shorter digit: sums over the digits sharing the low j bits
+  for (int j = 0; j < K; ++j) {
+    if (lane < (1 << j)) {
+      int c = 0;
+      int64_t lb = 0;
+      for (int e = lane; e < nd; e += (1 << j)) {
+        c += tt.cnt[K][e];
+        lb += tt.lb[K][e];
+      }
+      tt.cnt[j][lane] = c;
+      tt.lb[j][lane] = lb;
+    }
+  }
+  __syncwarp();
+  // group starts in the tile-local orders (groups by increasing LSD digit)
+  for (int j = 0; j <= K; ++j) {
+    const int mj = 1 << j;
+    const int c = lane < mj ? tt.cnt[j][lane] : 0;
+    int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += t;
+    }
+    if (lane < mj) tt.ls[j][lane] = incl - c;
+  }
+  bool q1 = true;
+  int64_t q = 0;
+  if (!wm) {
+    bar_sync(3, allt);  // tile staged
+    const int sh = w - l0;
+    const uint64_t qf = sh >= 32 ? 0 : ((uint64_t)(uint32_t)buf0[0] >> sh);
+    const uint64_t ql = sh >= 32 ? 0 : ((uint64_t)(uint32_t)buf0[cnt - 1] >> sh);
+    q1 = qf == ql;
+    q = (int64_t)qf;
+  }
+  if (lane == 0) tt.q1 = q1;
+  __syncwarp();
+  if (q1) {  // placement is a per-digit constant in this tile
+    for (int j = 1; j <= K; ++j) {
+      if (lane < (1 << j)) {
+        const int d = lane;
+        const int64_t tb = wm ? __ldg(a.wm_base + j * NDIG + d)
+                              : __ldg(a.corr + a.corr_off[j] + (q << j) + (int64_t)rev_bits((unsigned)d, j));
+        tt.gs[j][d] = tb + tt.lb[j][d];
+      }
+    }
+    __syncwarp();
+    if (lane < nd && a.has_out) {
+      const int d = (int)rev_bits((unsigned)lane, K);  // lane = numeric digit
+      const int64_t g = tt.gs[K][d];
+      tt.row[lane] = reinterpret_cast<TOut*>(a.dst) + (g - tt.ls[K][d]);
+      const int64_t ntile = (int64_t)1 << a.ntshift;
+      tt.thr[lane] = tt.ls[K][d] + (int)(ntile - (g & (ntile - 1)));
+      tt.ft[lane] = g >> a.ntshift;
+    }
+  }
+  __threadfence_block();
+  bar_arrive(2, allt);
+}
+
+// Levels l0+1 .. l0+K-1 of a uniform tile: one warp per (level j, run r),
+// task t = 2^j - 2 + r; whole words stored, run-edge words OR-ed into the
+// pre-zeroed level (gather_bits' owner rule, _kernels.py:197-205, relaxed to
+// atomics at run edges).
+template <typename TOut, int K, int NC>
+__device__ __forceinline__ void emit_uniform(const PassArgs& a, const TileTables<TOut, K>& tt, const uint32_t* bits,
+                                             int wid, int lane, int nwarps) {
+  constexpr int nd = 1 << K;
+  for (int t = wid; t < nd - 2; t += nwarps) {
+    const int j = 31 - __clz(t + 2);
+    const int r = t + 2 - (1 << j);
+    const int len = tt.cnt[j][r];
+    if (!len) continue;
+    const int64_t g = tt.gs[j][r];
+    const int ls = tt.ls[j][r];
+    const uint32_t* L = bits + j * (NC + 4);
+    uint64_t* gw = a.words + (int64_t)(a.level + j) * a.nwords;
+    const int64_t W0 = g >> 6, W1 = (g + len - 1) >> 6;
+    for (int64_t W = W0 + lane; W <= W1; W += 32) {
+      const int64_t wb = W << 6;
+      const int64_t a0 = g > wb ? g : wb;
+      const int64_t e0 = g + len;
+      const int64_t b0 = e0 < wb + 64 ? e0 : wb + 64;
+      const int c = (int)(b0 - a0);
+      const uint64_t v = extract_bits(L, ls + (int)(a0 - g), c) << (int)(a0 - wb);
+      if (c == 64)
+        gw[W] = v;
+      else
+        atomicOr(reinterpret_cast<unsigned long long*>(gw + W), (unsigned long long)v);
+    }
+  }
+}
+
+// Levels l0+1 .. l0+K-1 of a WT tile spanning several nodes: per-symbol
+// placement (elements of order j are buf + j*T, linear layout), runs found by
+// contiguity of the global position inside each warp chunk.
+template <typename TIn, typename TOut, int K>
+__device__ __forceinline__ void emit_multinode(const PassArgs& a, const TileTables<TOut, K>& tt, const TIn* buf,
+                                               int T, int cnt, int tid, int lane, int nthreads) {
+  const int w = a.width, l0 = a.level;
+#pragma unroll 1
+  for (int j = 1; j < K; ++j) {
+    uint64_t* gw = a.words + (int64_t)(l0 + j) * a.nwords;
+    const TIn* cur = buf + (size_t)j * T;
+    const int tshift = w - 1 - l0;
+    const int pshift = w - l0 - j;
+    const int64_t* ctab = a.corr + a.corr_off[j];
+#pragma unroll 1
+    for (int p0 = (tid >> 5) * 32; p0 < T; p0 += nthreads) {
+      const int p = p0 + lane;
+      const bool valid = p < cnt;
+      const TIn xv = cur[p];
+      int64_t gpos = 0;
+      unsigned bit = 0;
+      if (valid) {
+        const unsigned d = digit_of(xv, tshift, j);
+        const uint64_t P = pshift >= 32 ? 0 : ((uint64_t)(uint32_t)xv >> pshift);
+        gpos = ctab[P] + tt.lb[j][d] + p - tt.ls[j][d];
+        bit = ((uint32_t)xv >> (tshift - j)) & 1u;
+      }
+      const int64_t key = gpos - p;
+      const int64_t pkey = __shfl_up_sync(FULL, key, 1);
+      const bool leader = valid && (lane == 0 || pkey != key);
+      const unsigned Lm = __ballot_sync(FULL, leader);
+      const unsigned Bm = __ballot_sync(FULL, bit);
+      const unsigned Vm = __ballot_sync(FULL, valid);
+      if (leader) {
+        const unsigned rest = Lm & ~((2u << lane) - 1u);
+        const int next = rest ? __ffs(rest) - 1 : __popc(Vm);
+        const int len = next - lane;
+        uint64_t seg = (uint64_t)(Bm >> lane);
+        if (len < 32) seg &= (1ull << len) - 1ull;
+        const int64_t W = gpos >> 6;
+        const int o = (int)(gpos & 63);
+        if (seg) {
+          atomicOr(reinterpret_cast<unsigned long long*>(gw + W), (unsigned long long)(seg << o));
+          if (o + len > 64)
+            atomicOr(reinterpret_cast<unsigned long long*>(gw + W + 1), (unsigned long long)(seg >> (64 - o)));
+        }
+      }
+    }
+  }
+}
+
 // One CTA = one tile of T = 512 * E symbols of A_l; CTAs are independent.
-// Symbol p of the tile-local order lives in lane p % 32 of warp p / (32 E)
-// (warp-contiguous 32-symbol chunks), so a ballot gives 32 consecutive bits.
-// Warps 0..15 stage the tile and run the splits; warp 16 derives the tile's
-// placement tables concurrently (named barriers 1: compute warps, 2: tables
-// ready, 3: tile staged).
+// Generic (striped) variant for 2- and 4-byte symbols: symbol p of the
+// tile-local order lives in lane p % 32 of warp p / (32 E) (warp-contiguous
+// 32-symbol chunks), so a ballot gives 32 consecutive bits.  Warps 0..15 stage
+// the tile and run the splits; warp 16 builds the placement tables
+// concurrently (named barriers 1: compute warps, 2: tables ready, 3: staged).
 constexpr int TAB_WARP_THREADS = 32;
 template <typename TIn, typename TOut, int K, int E>
 __global__ void __launch_bounds__(PASS_THREADS + TAB_WARP_THREADS, 2) level_pass_kernel(const PassArgs a) {
@@ -696,16 +884,9 @@ __global__ void __launch_bounds__(PASS_THREADS + TAB_WARP_THREADS, 2) level_pass
   TIn* buf = reinterpret_cast<TIn*>(smem);
   uint32_t* bits = reinterpret_cast<uint32_t*>(smem + S::buf_bytes);
 
+  __shared__ TileTables<TOut, K> tt;
   __shared__ __align__(16) uint32_t s_wtot[2][NW];
-  __shared__ int s_cnt[K + 1][NDIG];
-  __shared__ int s_ls[K + 1][NDIG];
-  __shared__ int64_t s_lb[K + 1][NDIG];
-  __shared__ int64_t s_gs[K + 1][NDIG];
-  __shared__ TOut* s_row[NDIG];   // uniform tiles: output row of each numeric digit (dst + offset)
-  __shared__ int s_thr[NDIG];     // local position where that run crosses into the next pass's next tile
-  __shared__ int64_t s_ft[NDIG];  // first next-pass tile of each run
   __shared__ uint32_t s_ncnt[2 * NDIG * NDIG];  // next-pass digit counts per (run, next tile)
-  __shared__ int s_q1;
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int w = a.width, l0 = a.level;
@@ -715,76 +896,10 @@ __global__ void __launch_bounds__(PASS_THREADS + TAB_WARP_THREADS, 2) level_pass
   const int cnt = (int)min((int64_t)T, a.n - base);
 
   if (wid == NW) {
-    // ========================= table warp =========================
-    if (lane < nd) {
-      const int d = (int)rev_bits((unsigned)lane, K);  // lane = numeric digit
-      s_cnt[K][d] = (int)__ldg(a.tcnt + (int64_t)lane * a.ntiles + tile);
-      s_lb[K][d] = __ldg(a.tpre + (int64_t)lane * a.ntiles + tile);
-    }
-    __syncwarp();
-    // every shorter digit: sums over the digits sharing the low j bits
-    for (int j = 0; j < K; ++j) {
-      if (lane < (1 << j)) {
-        int c = 0;
-        int64_t lb = 0;
-        for (int e = lane; e < nd; e += (1 << j)) {
-          c += s_cnt[K][e];
-          lb += s_lb[K][e];
-        }
-        s_cnt[j][lane] = c;
-        s_lb[j][lane] = lb;
-      }
-    }
-    __syncwarp();
-    // group starts in the tile-local orders (groups by increasing LSD digit)
-    for (int j = 0; j <= K; ++j) {
-      const int mj = 1 << j;
-      const int c = lane < mj ? s_cnt[j][lane] : 0;
-      int incl = c;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int t = __shfl_up_sync(FULL, incl, o);
-        if (lane >= o) incl += t;
-      }
-      if (lane < mj) s_ls[j][lane] = incl - c;
-    }
-    bool q1 = true;
-    int64_t q = 0;
-    if (!wm) {
-      bar_sync(3, ALLT);  // tile staged
-      const int sh = w - l0;
-      const uint64_t qf = sh >= 32 ? 0 : ((uint64_t)(uint32_t)buf[0] >> sh);
-      const uint64_t ql = sh >= 32 ? 0 : ((uint64_t)(uint32_t)buf[cnt - 1] >> sh);
-      q1 = qf == ql;
-      q = (int64_t)qf;
-    }
-    if (lane == 0) s_q1 = q1;
-    __syncwarp();
-    if (q1) {  // placement is a per-digit constant in this tile
-      for (int j = 1; j <= K; ++j) {
-        if (lane < (1 << j)) {
-          const int d = lane;
-          const int64_t tb = wm ? __ldg(a.wm_base + j * NDIG + d)
-                                : __ldg(a.corr + a.corr_off[j] + (q << j) + (int64_t)rev_bits((unsigned)d, j));
-          s_gs[j][d] = tb + s_lb[j][d];
-        }
-      }
-      __syncwarp();
-      if (lane < nd && a.has_out) {
-        const int d = (int)rev_bits((unsigned)lane, K);  // lane = numeric digit
-        const int64_t g = s_gs[K][d];
-        s_row[lane] = reinterpret_cast<TOut*>(a.dst) + (g - s_ls[K][d]);
-        const int64_t ntile = (int64_t)1 << a.ntshift;
-        s_thr[lane] = s_ls[K][d] + (int)(ntile - (g & (ntile - 1)));
-        s_ft[lane] = g >> a.ntshift;
-      }
-    }
-    __threadfence_block();
-    bar_arrive(2, ALLT);
+    table_warp<TIn, TOut, K>(a, tt, buf, tile, cnt, lane, ALLT);
     return;
   }
 
-  // ========================== compute warps ==========================
   // ---- stage the tile (invalid tail slots = all ones so they sort last) ----
   const TIn* src = reinterpret_cast<const TIn*>(a.src) + base;
   if (cnt == T && ((((uintptr_t)src) & 15) == 0)) {
@@ -837,7 +952,6 @@ __global__ void __launch_bounds__(PASS_THREADS + TAB_WARP_THREADS, 2) level_pass
       for (int q4 = 0; q4 < E / 4; ++q4) b4[q4] = make_uint4(m[4 * q4], m[4 * q4 + 1], m[4 * q4 + 2], m[4 * q4 + 3]);
     }
     if (j + 1 == K && !a.has_out) break;
-    // chunk prefixes inside the warp (warp-uniform) and the CTA-wide warp prefix
     uint32_t run = 0;
 #pragma unroll
     for (int e = 0; e < E; ++e) run += __popc(m[e]);
@@ -846,15 +960,15 @@ __global__ void __launch_bounds__(PASS_THREADS + TAB_WARP_THREADS, 2) level_pass
     const uint32_t wv = lane < NW ? s_wtot[j & 1][lane] : 0u;
     const uint32_t wpre = __reduce_add_sync(FULL, lane < wid ? wv : 0u);
     const uint32_t tot = __reduce_add_sync(FULL, wv);
-    // ones of chunk e go to U1 + c[e] + rank, zeros to U0 + 32 e - c[e] - rank
+    // ones of chunk e go to U1 + ce + rank, zeros to U0 + 32 e - ce - rank
     const int U1 = T - (int)tot + (int)wpre;
     const int U0 = pbase + lane - (int)wpre;
+    int ce = 0;  // ones in this warp's earlier chunks
     if (j + 1 < K) {
       const uint32_t nxt = (uint32_t)__cvta_generic_to_shared(buf + (size_t)(j + 1) * T);
-      int ce = 0;  // ones in this warp's earlier chunks
 #pragma unroll
       for (int e = 0; e < E; ++e) {
-        const uint32_t xv = (uint32_t)cur[pbase + e * 32 + lane];  // reload: LSU has slack, registers do not
+        const uint32_t xv = (uint32_t)cur[pbase + e * 32 + lane];
         const int r = __popc(m[e] & lt);
         st_split<TIn>(nxt + (uint32_t)(U1 + ce + r) * (uint32_t)sizeof(TIn),
                       nxt + (uint32_t)(U0 + 32 * e - ce - r) * (uint32_t)sizeof(TIn), xv & bmask, xv);
@@ -868,48 +982,36 @@ __global__ void __launch_bounds__(PASS_THREADS + TAB_WARP_THREADS, 2) level_pass
       const int eshift = w - l0 - K;
       const int nshift = w - l0 - K - a.nK;  // next pass digit = bits l0+K .. l0+K+nK-1
       const unsigned nmask = (1u << a.nK) - 1u;
-      int ce = 0;
-      if (s_q1) {
+      const bool q1 = tt.q1;
 #pragma unroll
-        for (int e = 0; e < E; ++e) {
-          const int r = __popc(m[e] & lt);
-          const uint32_t xv = (uint32_t)cur[pbase + e * 32 + lane];
-          const int pos = (xv & bmask) ? U1 + ce + r : U0 + 32 * e - ce - r;
-          ce += __popc(m[e]);
-          if (pos < cnt) {
+      for (int e = 0; e < E; ++e) {
+        const int r = __popc(m[e] & lt);
+        const uint32_t xv = (uint32_t)cur[pbase + e * 32 + lane];
+        const int pos = (xv & bmask) ? U1 + ce + r : U0 + 32 * e - ce - r;
+        ce += __popc(m[e]);
+        if (pos < cnt) {
+          if (q1) {
             const unsigned dig = (xv >> eshift) & (nd - 1);
-            s_row[dig][pos] = (TOut)(xv & keep);
-            const unsigned h = pos >= s_thr[dig] ? 1u : 0u;
+            tt.row[dig][pos] = (TOut)(xv & keep);
+            const unsigned h = pos >= tt.thr[dig] ? 1u : 0u;
             atomicAdd(&s_ncnt[(((dig << 1) | h) << a.nK) | ((xv >> nshift) & nmask)], 1u);
-          }
-        }
-      } else {
-        TOut* dst = reinterpret_cast<TOut*>(a.dst);
-        const int64_t* ctab = a.corr + a.corr_off[K];
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-          const int r = __popc(m[e] & lt);
-          const uint32_t xv = (uint32_t)cur[pbase + e * 32 + lane];
-          const int pos = (xv & bmask) ? U1 + ce + r : U0 + 32 * e - ce - r;
-          ce += __popc(m[e]);
-          if (pos < cnt) {
+          } else {
             const unsigned d = rev_bits((xv >> eshift) & (nd - 1), K);
             const uint64_t P = eshift >= 32 ? 0 : ((uint64_t)xv >> eshift);
-            const int64_t gpos = ctab[P] + s_lb[K][d] + pos - s_ls[K][d];
-            dst[gpos] = (TOut)(xv & keep);
+            const int64_t gpos = a.corr[a.corr_off[K] + P] + tt.lb[K][d] + pos - tt.ls[K][d];
+            reinterpret_cast<TOut*>(a.dst)[gpos] = (TOut)(xv & keep);
             atomicAdd(&a.ncnt[(int64_t)((xv >> nshift) & nmask) * a.nntiles + (gpos >> a.ntshift)], 1u);
           }
         }
       }
       bar_sync(1, PASS_THREADS);
-      if (s_q1) {
+      if (q1) {
         const int ncount = 2 * nd << a.nK;
         for (int i = tid; i < ncount; i += PASS_THREADS) {
           const uint32_t v = s_ncnt[i];
           if (v) {
             const int slot = i >> a.nK, ne = i & (int)nmask;
-            const int64_t nt = s_ft[slot >> 1] + (slot & 1);
-            atomicAdd(&a.ncnt[(int64_t)ne * a.nntiles + nt], v);
+            atomicAdd(&a.ncnt[(int64_t)ne * a.nntiles + tt.ft[slot >> 1] + (slot & 1)], v);
           }
         }
       }
@@ -919,79 +1021,172 @@ __global__ void __launch_bounds__(PASS_THREADS + TAB_WARP_THREADS, 2) level_pass
     bar_sync(1, PASS_THREADS);  // every warp's ballot words are stored
     bar_sync(2, ALLT);          // placement tables
   }
+  if (tt.q1)
+    emit_uniform<TOut, K, NC>(a, tt, bits, wid, lane, NW);
+  else
+    emit_multinode<TIn, TOut, K>(a, tt, buf, T, cnt, tid, lane, PASS_THREADS);
+}
 
-  // ---- emit levels l0+1 .. l0+K-1 ----
-  if (s_q1) {
-    // one warp per (level j, run r): task t = 2^j - 2 + r
-    for (int t = wid; t < nd - 2; t += NW) {
-      const int j = 31 - __clz(t + 2);
-      const int r = t + 2 - (1 << j);
-      const int len = s_cnt[j][r];
-      if (!len) continue;
-      const int64_t g = s_gs[j][r];
-      const int ls = s_ls[j][r];
-      const uint32_t* L = bits + j * (NC + 4);
-      uint64_t* gw = a.words + (int64_t)(l0 + j) * a.nwords;
-      const int64_t W0 = g >> 6, W1 = (g + len - 1) >> 6;
-      for (int64_t W = W0 + lane; W <= W1; W += 32) {
-        const int64_t wb = W << 6;
-        const int64_t a0 = g > wb ? g : wb;
-        const int64_t e0 = g + len;
-        const int64_t b0 = e0 < wb + 64 ? e0 : wb + 64;
-        const int c = (int)(b0 - a0);
-        const uint64_t v = extract_bits(L, ls + (int)(a0 - g), c) << (int)(a0 - wb);
-        if (c == 64)
-          gw[W] = v;
-        else
-          atomicOr(reinterpret_cast<unsigned long long*>(gw + W), (unsigned long long)v);
-      }
-    }
+// Byte variant (all passes of byte alphabets): SIMD within a register.  Thread
+// t owns the 16 consecutive symbols [16 t, 16 t + 16) of the tile-local order
+// (one 128-bit shared load); bits and in-thread ranks are computed four
+// symbols per instruction (byte-lane multiply prefix sums), the CTA prefix by
+// one warp-shuffle scan, and every symbol is stored once per split with a
+// predicated zeros/ones store pair.
+template <int K>
+__global__ void __launch_bounds__(PASS_THREADS + TAB_WARP_THREADS, 2) level_pass_u8_kernel(const PassArgs a) {
+  using S = PassSmem<uint8_t, K, 16>;
+  constexpr int T = S::T;
+  constexpr int NC = S::NC;
+  constexpr int NW = PASS_THREADS / 32;
+  constexpr int ALLT = PASS_THREADS + TAB_WARP_THREADS;
+  constexpr int nd = 1 << K;
+  constexpr uint32_t B1 = 0x01010101u;
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint8_t* buf = smem;
+  uint32_t* bits = reinterpret_cast<uint32_t*>(smem + S::buf_bytes);
+
+  __shared__ TileTables<uint8_t, K> tt;
+  __shared__ __align__(16) uint32_t s_wtot[2][NW];
+  __shared__ uint32_t s_ncnt[2 * NDIG * NDIG];
+
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int w = a.width, l0 = a.level;
+  const bool wm = a.kind == WVLT_KIND_WM;
+  const int64_t tile = blockIdx.x;
+  const int64_t base = tile * T;
+  const int cnt = (int)min((int64_t)T, a.n - base);
+
+  if (wid == NW) {
+    table_warp<uint8_t, uint8_t, K>(a, tt, buf, tile, cnt, lane, ALLT);
+    return;
+  }
+
+  // ---- stage the tile (invalid tail slots = all ones so they sort last) ----
+  const uint8_t* src = reinterpret_cast<const uint8_t*>(a.src) + base;
+  if (cnt == T && ((((uintptr_t)src) & 15) == 0)) {
+    reinterpret_cast<uint4*>(buf)[tid] = __ldcs(reinterpret_cast<const uint4*>(src) + tid);
   } else {
-    // WT tile spanning several nodes: per-symbol placement, runs found by
-    // contiguity of the global position inside each warp chunk
+    for (int p = tid; p < T; p += PASS_THREADS) buf[p] = p < cnt ? src[p] : (uint8_t)0xFF;
+  }
+  if (tid < 2 * NDIG * NDIG) s_ncnt[tid] = 0;
+  bar_sync(1, PASS_THREADS);
+  if (!wm) bar_arrive(3, ALLT);
+
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(buf);
+  uint16_t* bits16 = reinterpret_cast<uint16_t*>(bits);
+
 #pragma unroll 1
-    for (int j = 1; j < K; ++j) {
-      uint64_t* gw = a.words + (int64_t)(l0 + j) * a.nwords;
-      const TIn* cur = buf + (size_t)j * T;
-      const int tshift = w - 1 - l0;
-      const int pshift = w - l0 - j;
-      const int64_t* ctab = a.corr + a.corr_off[j];
-#pragma unroll 1
-      for (int e = 0; e < E; ++e) {
-        const int p = pbase + e * 32 + lane;
-        const bool valid = p < cnt;
-        const TIn xv = cur[p];
-        int64_t gpos = 0;
-        unsigned bit = 0;
-        if (valid) {
-          const unsigned d = digit_of(xv, tshift, j);
-          const uint64_t P = pshift >= 32 ? 0 : ((uint64_t)(uint32_t)xv >> pshift);
-          gpos = ctab[P] + s_lb[j][d] + p - s_ls[j][d];
-          bit = ((uint32_t)xv >> (tshift - j)) & 1u;
+  for (int j = 0; j < K; ++j) {
+    const int sh = w - 1 - l0 - j;
+    const uint4 q = reinterpret_cast<const uint4*>(buf + (size_t)j * T)[tid];
+    const uint32_t x[4] = {q.x, q.y, q.z, q.w};
+    uint32_t b[4], p[4];
+    uint32_t ones = 0;  // running in-thread ones count
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      b[k] = (x[k] >> sh) & B1;
+      p[k] = (b[k] + ones) * B1;  // inclusive ones count through each byte
+      ones = p[k] >> 24;
+    }
+    // this thread's 16 level bits (symbol 4k + i -> bit 4k + i)
+    uint32_t m16 = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) m16 |= ((b[k] * 0x01020408u) >> 24) << (4 * k);
+    if (j == 0) {
+      // level l0 is in global order already: lane pairs form aligned words
+      const uint32_t word = m16 | (__shfl_down_sync(FULL, m16, 1) << 16);
+      const int64_t gi = (base >> 5) + (tid >> 1);
+      if (!(lane & 1) && gi < 2 * a.nwords) {
+        uint32_t v = word;
+        const int first = (tid >> 1) * 32;
+        if (first + 32 > cnt) v = first >= cnt ? 0u : (v & ((1u << (cnt - first)) - 1u));
+        reinterpret_cast<uint32_t*>(a.words + (int64_t)l0 * a.nwords)[gi] = v;
+      }
+    } else {
+      bits16[j * 2 * (NC + 4) + tid] = (uint16_t)m16;
+    }
+    if (j + 1 == K && !a.has_out) break;
+    // CTA-wide exclusive scan of the per-thread ones counts
+    uint32_t incl = ones;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += t;
+    }
+    if (lane == 31) s_wtot[j & 1][wid] = incl;
+    bar_sync(1, PASS_THREADS);
+    const uint32_t wv = lane < NW ? s_wtot[j & 1][lane] : 0u;
+    const uint32_t wpre = __reduce_add_sync(FULL, lane < wid ? wv : 0u);
+    const uint32_t tot = __reduce_add_sync(FULL, wv);
+    const int opre = (int)(wpre + incl - ones);  // ones before this thread
+    // ones: OB + (inclusive rank); zeros: ZB + symbol index - (inclusive ones)
+    const int OB = T - (int)tot + opre - 1;
+    const int ZB = 16 * tid - opre;
+    if (j + 1 < K) {
+      const uint32_t nxt = sbase + (uint32_t)(j + 1) * T;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int r = (int)__byte_perm(p[k], 0, 0x4440 + i);
+          st_split_u8(nxt + (uint32_t)(OB + r), nxt + (uint32_t)(ZB + 4 * k + i - r), b[k] & (0xFFu << (8 * i)),
+                      x[k] >> (8 * i));
         }
-        const int64_t key = gpos - p;
-        const int64_t pkey = __shfl_up_sync(FULL, key, 1);
-        const bool leader = valid && (lane == 0 || pkey != key);
-        const unsigned Lm = __ballot_sync(FULL, leader);
-        const unsigned Bm = __ballot_sync(FULL, bit);
-        const unsigned Vm = __ballot_sync(FULL, valid);
-        if (leader) {
-          const unsigned rest = Lm & ~((2u << lane) - 1u);
-          const int next = rest ? __ffs(rest) - 1 : __popc(Vm);
-          const int len = next - lane;
-          uint64_t seg = (uint64_t)(Bm >> lane);
-          if (len < 32) seg &= (1ull << len) - 1ull;
-          const int64_t W = gpos >> 6;
-          const int o = (int)(gpos & 63);
-          if (seg) {
-            atomicOr(reinterpret_cast<unsigned long long*>(gw + W), (unsigned long long)(seg << o));
-            if (o + len > 64)
-              atomicOr(reinterpret_cast<unsigned long long*>(gw + W + 1), (unsigned long long)(seg >> (64 - o)));
+      }
+      bar_sync(1, PASS_THREADS);
+    } else {
+      // last split: straight to HBM, counting the next pass's digits per (run, next tile)
+      bar_sync(2, ALLT);  // placement tables
+      const uint32_t keep = wm ? ((w - l0 - K) >= 32 ? FULL : ((1u << (w - l0 - K)) - 1u)) : FULL;
+      const int eshift = w - l0 - K;
+      const int nshift = w - l0 - K - a.nK;
+      const unsigned nmask = (1u << a.nK) - 1u;
+      const bool q1 = tt.q1;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int r = (int)__byte_perm(p[k], 0, 0x4440 + i);
+          const uint32_t xv = __byte_perm(x[k], 0, 0x4440 + i);
+          const int pos = (b[k] & (0xFFu << (8 * i))) ? OB + r : ZB + 4 * k + i - r;
+          if (pos < cnt) {
+            if (q1) {
+              const unsigned dig = (xv >> eshift) & (nd - 1);
+              tt.row[dig][pos] = (uint8_t)(xv & keep);
+              const unsigned h = pos >= tt.thr[dig] ? 1u : 0u;
+              atomicAdd(&s_ncnt[(((dig << 1) | h) << a.nK) | ((xv >> nshift) & nmask)], 1u);
+            } else {
+              const unsigned d = rev_bits((xv >> eshift) & (nd - 1), K);
+              const uint64_t P = (uint64_t)xv >> eshift;
+              const int64_t gpos = a.corr[a.corr_off[K] + P] + tt.lb[K][d] + pos - tt.ls[K][d];
+              reinterpret_cast<uint8_t*>(a.dst)[gpos] = (uint8_t)(xv & keep);
+              atomicAdd(&a.ncnt[(int64_t)((xv >> nshift) & nmask) * a.nntiles + (gpos >> a.ntshift)], 1u);
+            }
+          }
+        }
+      }
+      bar_sync(1, PASS_THREADS);
+      if (q1) {
+        const int ncount = 2 * nd << a.nK;
+        for (int i = tid; i < ncount; i += PASS_THREADS) {
+          const uint32_t v = s_ncnt[i];
+          if (v) {
+            const int slot = i >> a.nK, ne = i & (int)nmask;
+            atomicAdd(&a.ncnt[(int64_t)ne * a.nntiles + tt.ft[slot >> 1] + (slot & 1)], v);
           }
         }
       }
     }
   }
+  if (!a.has_out) {
+    bar_sync(1, PASS_THREADS);
+    bar_sync(2, ALLT);
+  }
+  if (tt.q1)
+    emit_uniform<uint8_t, K, NC>(a, tt, bits, wid, lane, NW);
+  else
+    emit_multinode<uint8_t, uint8_t, K>(a, tt, buf, T, cnt, tid, lane, PASS_THREADS);
 }
 
 // ---------------------------------------------------------------------------
@@ -1054,7 +1249,7 @@ int bytes_for_bits(int bits) { return bits <= 8 ? 1 : (bits <= 16 ? 2 : 4); }
 
 inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
-int tile_for(int in_bytes) { return in_bytes == 4 ? PASS_THREADS * 8 : PASS_THREADS * 16; }
+int tile_for(int in_bytes) { return in_bytes == 4 ? PASS_THREADS * 8 : (in_bytes == 1 ? PASS_THREADS * 16 : PASS_THREADS * E_SMALL); }
 int log2i(int v) {
   int r = 0;
   while ((1 << r) < v) ++r;
@@ -1141,7 +1336,7 @@ bool make_plan(int64_t n, int sym_bytes, int64_t sigma, int kind, Plan* P) {
 
 template <typename TIn, typename TOut, int K>
 cudaError_t launch_pass_t(const PassArgs& a, int64_t ntiles, cudaStream_t s) {
-  constexpr int E = sizeof(TIn) == 4 ? 8 : 16;
+  constexpr int E = sizeof(TIn) == 4 ? 8 : E_SMALL;
   using S = PassSmem<TIn, K, E>;
   auto kern = level_pass_kernel<TIn, TOut, K, E>;
   static bool attr_set = false;
@@ -1164,9 +1359,30 @@ cudaError_t launch_pass_k(int K, const PassArgs& a, int64_t ntiles, cudaStream_t
   }
 }
 
+template <int K>
+cudaError_t launch_pass_u8(const PassArgs& a, int64_t ntiles, cudaStream_t s) {
+  using S = PassSmem<uint8_t, K, 16>;
+  auto kern = level_pass_u8_kernel<K>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::total);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  kern<<<(unsigned)ntiles, PASS_THREADS + TAB_WARP_THREADS, S::total, s>>>(a);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_pass(int in_bytes, int out_bytes, int K, const PassArgs& a, int64_t ntiles, cudaStream_t s) {
   const int ob = out_bytes ? out_bytes : in_bytes;
-  if (in_bytes == 1) return launch_pass_k<uint8_t, uint8_t>(K, a, ntiles, s);
+  if (in_bytes == 1) {
+    switch (K) {
+      case 1: return launch_pass_u8<1>(a, ntiles, s);
+      case 2: return launch_pass_u8<2>(a, ntiles, s);
+      case 3: return launch_pass_u8<3>(a, ntiles, s);
+      default: return launch_pass_u8<4>(a, ntiles, s);
+    }
+  }
   if (in_bytes == 2) {
     if (ob == 1) return launch_pass_k<uint16_t, uint8_t>(K, a, ntiles, s);
     return launch_pass_k<uint16_t, uint16_t>(K, a, ntiles, s);
