@@ -1028,15 +1028,18 @@ __global__ void __launch_bounds__(PASS_THREADS + TAB_WARP_THREADS, 2) level_pass
 }
 
 // Byte variant (all passes of byte alphabets): SIMD within a register.  Thread
-// t owns the 16 consecutive symbols [16 t, 16 t + 16) of the tile-local order
-// (one 128-bit shared load); bits and in-thread ranks are computed four
-// symbols per instruction (byte-lane multiply prefix sums), the CTA prefix by
-// one warp-shuffle scan, and every symbol is stored once per split with a
-// predicated zeros/ones store pair.
+// t owns the two 8-symbol runs [8t, 8t+8) and [T/2 + 8t, T/2 + 8t + 8) of the
+// tile-local order (two 64-bit shared loads): bits and in-thread ranks are
+// computed four symbols per instruction (byte-lane multiply prefix sums), the
+// CTA prefix of both halves by one packed warp-shuffle scan, and every symbol
+// is stored once per split with a predicated zeros/ones store pair.  With 8
+// symbols per half the 32 lanes' destinations of one store stream span about
+// 128 bytes, so each store is a single conflict-free wavefront.
 template <int K>
 __global__ void __launch_bounds__(PASS_THREADS + TAB_WARP_THREADS, 2) level_pass_u8_kernel(const PassArgs a) {
   using S = PassSmem<uint8_t, K, 16>;
   constexpr int T = S::T;
+  constexpr int H = T / 2;
   constexpr int NC = S::NC;
   constexpr int NW = PASS_THREADS / 32;
   constexpr int ALLT = PASS_THREADS + TAB_WARP_THREADS;
@@ -1074,41 +1077,43 @@ __global__ void __launch_bounds__(PASS_THREADS + TAB_WARP_THREADS, 2) level_pass
   if (!wm) bar_arrive(3, ALLT);
 
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(buf);
-  uint16_t* bits16 = reinterpret_cast<uint16_t*>(bits);
+  uint8_t* bits8 = reinterpret_cast<uint8_t*>(bits);
 
 #pragma unroll 1
   for (int j = 0; j < K; ++j) {
     const int sh = w - 1 - l0 - j;
-    const uint4 q = reinterpret_cast<const uint4*>(buf + (size_t)j * T)[tid];
-    const uint32_t x[4] = {q.x, q.y, q.z, q.w};
+    const uint8_t* cur = buf + (size_t)j * T;
+    const uint2 q0 = reinterpret_cast<const uint2*>(cur)[tid];
+    const uint2 q1 = reinterpret_cast<const uint2*>(cur + H)[tid];
+    const uint32_t x[4] = {q0.x, q0.y, q1.x, q1.y};
     uint32_t b[4], p[4];
-    uint32_t ones = 0;  // running in-thread ones count
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      b[k] = (x[k] >> sh) & B1;
-      p[k] = (b[k] + ones) * B1;  // inclusive ones count through each byte
-      ones = p[k] >> 24;
-    }
-    // this thread's 16 level bits (symbol 4k + i -> bit 4k + i)
-    uint32_t m16 = 0;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) m16 |= ((b[k] * 0x01020408u) >> 24) << (4 * k);
+    for (int k = 0; k < 4; ++k) b[k] = (x[k] >> sh) & B1;
+    // inclusive ones count through each byte, per half
+    p[0] = b[0] * B1;
+    p[1] = (b[1] + (p[0] >> 24)) * B1;
+    p[2] = b[2] * B1;
+    p[3] = (b[3] + (p[2] >> 24)) * B1;
+    const uint32_t ones0 = p[1] >> 24, ones1 = p[3] >> 24;
+    // this thread's level bits: byte t (first half) and byte T/16 + t (second half)
+    const uint32_t m0 = ((b[0] * 0x01020408u) >> 24) | (((b[1] * 0x01020408u) >> 24) << 4);
+    const uint32_t m1 = ((b[2] * 0x01020408u) >> 24) | (((b[3] * 0x01020408u) >> 24) << 4);
     if (j == 0) {
-      // level l0 is in global order already: lane pairs form aligned words
-      const uint32_t word = m16 | (__shfl_down_sync(FULL, m16, 1) << 16);
-      const int64_t gi = (base >> 5) + (tid >> 1);
-      if (!(lane & 1) && gi < 2 * a.nwords) {
-        uint32_t v = word;
-        const int first = (tid >> 1) * 32;
-        if (first + 32 > cnt) v = first >= cnt ? 0u : (v & ((1u << (cnt - first)) - 1u));
-        reinterpret_cast<uint32_t*>(a.words + (int64_t)l0 * a.nwords)[gi] = v;
-      }
+      // level l0 is in global order already: byte stores (32 lanes = 32 consecutive bytes)
+      uint8_t* g8 = reinterpret_cast<uint8_t*>(a.words + (int64_t)l0 * a.nwords) + (base >> 3);
+      const int64_t lim = 8 * a.nwords - (base >> 3);
+      const int f0 = 8 * tid, f1 = H + 8 * tid;
+      if (tid < lim) g8[tid] = (uint8_t)(f0 + 8 <= cnt ? m0 : (f0 >= cnt ? 0u : (m0 & ((1u << (cnt - f0)) - 1u))));
+      if (H / 8 + tid < lim)
+        g8[H / 8 + tid] = (uint8_t)(f1 + 8 <= cnt ? m1 : (f1 >= cnt ? 0u : (m1 & ((1u << (cnt - f1)) - 1u))));
     } else {
-      bits16[j * 2 * (NC + 4) + tid] = (uint16_t)m16;
+      bits8[j * 4 * (NC + 4) + tid] = (uint8_t)m0;
+      bits8[j * 4 * (NC + 4) + H / 8 + tid] = (uint8_t)m1;
     }
     if (j + 1 == K && !a.has_out) break;
-    // CTA-wide exclusive scan of the per-thread ones counts
-    uint32_t incl = ones;
+    // CTA-wide exclusive scans of both halves' ones counts (packed 16|16)
+    const uint32_t pk = ones0 | (ones1 << 16);
+    uint32_t incl = pk;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const uint32_t t = __shfl_up_sync(FULL, incl, o);
@@ -1119,10 +1124,14 @@ __global__ void __launch_bounds__(PASS_THREADS + TAB_WARP_THREADS, 2) level_pass
     const uint32_t wv = lane < NW ? s_wtot[j & 1][lane] : 0u;
     const uint32_t wpre = __reduce_add_sync(FULL, lane < wid ? wv : 0u);
     const uint32_t tot = __reduce_add_sync(FULL, wv);
-    const int opre = (int)(wpre + incl - ones);  // ones before this thread
-    // ones: OB + (inclusive rank); zeros: ZB + symbol index - (inclusive ones)
-    const int OB = T - (int)tot + opre - 1;
-    const int ZB = 16 * tid - opre;
+    const uint32_t ex = wpre + incl - pk;
+    const int tot0 = (int)(tot & 0xFFFFu), tot1 = (int)(tot >> 16);
+    const int Z = T - tot0 - tot1;
+    const int opre0 = (int)(ex & 0xFFFFu);
+    const int opre1 = tot0 + (int)(ex >> 16);
+    // ones: OBh + (inclusive rank); zeros: ZBh + symbol index - (inclusive ones)
+    const int OB[2] = {Z + opre0 - 1, Z + opre1 - 1};
+    const int ZB[2] = {8 * tid - opre0, H + 8 * tid - opre1};
     if (j + 1 < K) {
       const uint32_t nxt = sbase + (uint32_t)(j + 1) * T;
 #pragma unroll
@@ -1130,8 +1139,8 @@ __global__ void __launch_bounds__(PASS_THREADS + TAB_WARP_THREADS, 2) level_pass
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const int r = (int)__byte_perm(p[k], 0, 0x4440 + i);
-          st_split_u8(nxt + (uint32_t)(OB + r), nxt + (uint32_t)(ZB + 4 * k + i - r), b[k] & (0xFFu << (8 * i)),
-                      x[k] >> (8 * i));
+          st_split_u8(nxt + (uint32_t)(OB[k >> 1] + r), nxt + (uint32_t)(ZB[k >> 1] + 4 * (k & 1) + i - r),
+                      b[k] & (0xFFu << (8 * i)), x[k] >> (8 * i));
         }
       }
       bar_sync(1, PASS_THREADS);
@@ -1149,7 +1158,7 @@ __global__ void __launch_bounds__(PASS_THREADS + TAB_WARP_THREADS, 2) level_pass
         for (int i = 0; i < 4; ++i) {
           const int r = (int)__byte_perm(p[k], 0, 0x4440 + i);
           const uint32_t xv = __byte_perm(x[k], 0, 0x4440 + i);
-          const int pos = (b[k] & (0xFFu << (8 * i))) ? OB + r : ZB + 4 * k + i - r;
+          const int pos = (b[k] & (0xFFu << (8 * i))) ? OB[k >> 1] + r : ZB[k >> 1] + 4 * (k & 1) + i - r;
           if (pos < cnt) {
             if (q1) {
               const unsigned dig = (xv >> eshift) & (nd - 1);
