@@ -50,6 +50,7 @@ class DeviceBuild:
     zeros: object        # torch.int64 [width]
     hist: object         # torch.int64 [2^width]
     borders: object      # torch.int64 [2^width - 2] or None
+    status: object = None  # torch.int32 [1]: WVLT_STATUS_RANGE bit set on a bad symbol
 
     def to_host(self):
         """(level_words uint64 ndarray, zeros list, hist ndarray) after a device->host copy."""
@@ -131,7 +132,7 @@ class DeviceBuilder:
         _lib.check(rc)
         if check and int(status.item()) & _lib.STATUS_RANGE:
             raise ValueError(f"symbols must lie in [0, {sigma})")
-        return DeviceBuild(kind, n, sigma, w, lw, zeros, hist, bd)
+        return DeviceBuild(kind, n, sigma, w, lw, zeros, hist, bd, status)
 
     def build_host(self, arr: np.ndarray, sigma: int, kind: str, *, out_words: np.ndarray | None = None,
                    stream=None):
@@ -166,12 +167,18 @@ class DeviceBuilder:
         return out_words, [int(z) for z in zeros[:w]], hist
 
     def merge_bits(self, dst_words, word_lo: int, word_hi: int, n_bits: int, bounds, src_starts, src_words,
-                   stream=None) -> None:
-        """gather_bits (_kernels.py:196-232) on device tensors (int64 views of uint64 words)."""
+                   stream=None, dst_offset_words: int = 0) -> None:
+        """gather_bits (_kernels.py:196-232) on device tensors (int64 views of uint64 words).
+
+        Destination word ``wd`` of [word_lo, word_hi) is written at
+        ``dst_words[wd - dst_offset_words]`` (so a buffer holding just the owned
+        range can be passed with ``dst_offset_words = word_lo``).
+        """
         torch = _torch()
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
         ntasks = int(bounds.numel()) - 1
-        rc = self.lib.wvlt_merge_bits(dst_words.data_ptr(), int(word_lo), int(word_hi), int(n_bits),
+        rc = self.lib.wvlt_merge_bits(dst_words.data_ptr() - 8 * int(dst_offset_words), int(word_lo), int(word_hi),
+                                      int(n_bits),
                                       bounds.data_ptr() if ntasks > 0 else None,
                                       src_starts.data_ptr() if ntasks > 0 else None, max(ntasks, 0),
                                       src_words.data_ptr() if src_words.numel() else None, s.cuda_stream)

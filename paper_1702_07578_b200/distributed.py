@@ -1,0 +1,274 @@
+"""Multi-GPU construction: the text is sharded by position across ranks.
+
+The reference's domain decomposition (construct.build_domain_decomposed,
+construct.py:437-513) builds one partial structure per text slice and then
+merges every level by moving whole intervals (_merge_plan, construct.py:516-543;
+gather_bits, _kernels.py:196-232).  Here the slices are the ranks of a
+torch.distributed process group (one process per GPU, NCCL over NVLink):
+
+1. every rank builds the complete local WT/WM of its shard on its GPU
+   (no communication);
+2. one all_gather of the per-rank symbol histograms (2^w int64 each) gives
+   every rank the merge plan of every level: prefix groups in interval order
+   (numeric for WT, bit-reversed for WM, construct.py:498), ranks in text order
+   inside each group -- the interleaved (prefix, core) order of
+   levelstats.interleaved_starts (levelstats.py:76-94) with cores -> ranks;
+3. one all_to_all_single moves, for every level, the bit segments each rank
+   needs to the rank owning the destination words (word ranges split like
+   construct._word_ranges, construct.py:214-217, so every rank owns 1/R of
+   every level);
+4. every rank shift-merges its word range of every level (wvlt_merge_bits).
+
+The result is bit-identical to the single-GPU build (the reference guarantees
+the same for any slice count, test_construct.py:43-51).  The host-side plan
+and exchange logic is backend-agnostic so the CPU tests can run it on the
+gloo backend with the oracle standing in for the device kernels.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .bitperm import bit_reversal_permutation, code_width
+
+
+@dataclass
+class ShardedResult:
+    """This rank's share of a sharded build."""
+
+    n: int                  # global text length
+    sigma: int
+    kind: str
+    width: int
+    word_lo: int            # owned global word range [word_lo, word_hi) of every level
+    word_hi: int
+    level_words: object     # tensor int64 [width, word_hi - word_lo] (uint64 bit patterns)
+    zeros: list             # global per-level zero counts
+    hist: np.ndarray        # global symbol histogram (2^width)
+
+
+def word_ranges(total_words: int, world: int) -> list[tuple[int, int]]:
+    """construct._word_ranges (construct.py:214-217)."""
+    cuts = [(total_words * c) // world for c in range(world + 1)]
+    return [(cuts[c], cuts[c + 1]) for c in range(world)]
+
+
+def fold_to(hist: np.ndarray, width: int, ell: int) -> np.ndarray:
+    """Counts of the ell-bit prefixes (fold_pairs applied width-ell times, _kernels.py:45-49)."""
+    h = np.asarray(hist, dtype=np.int64).reshape(-1)
+    if ell == width:
+        return h.copy()
+    return h.reshape(1 << ell, 1 << (width - ell)).sum(axis=1)
+
+
+def zeros_from_hist(hist: np.ndarray, width: int) -> list[int]:
+    """Z[l] = sum of even (l+1)-prefix counts (construct.py:238-239, structures.py:28-35)."""
+    return [int(fold_to(hist, width, ell + 1)[0::2].sum()) for ell in range(width)]
+
+
+def level_plan(hists: np.ndarray, kind: str, width: int, ell: int):
+    """Merge plan of level ell (construct._merge_plan, construct.py:516-543).
+
+    hists: (R, 2^width) per-rank histograms.  Returns pieces in destination
+    order: (rank, local_start, length, global_start), empty pieces dropped.
+    """
+    R = hists.shape[0]
+    if ell == 0:
+        lens = np.array([int(h.sum()) for h in hists], dtype=np.int64)
+        ranks = np.arange(R, dtype=np.int64)
+        local = np.zeros(R, dtype=np.int64)
+    else:
+        counts = np.stack([fold_to(h, width, ell) for h in hists])  # (R, 2^ell), numeric prefix
+        order = bit_reversal_permutation(ell) if (kind == "wm" and ell >= 2) else np.arange(1 << ell)
+        ordered = counts[:, order]
+        local_starts = np.cumsum(ordered, axis=1) - ordered  # (R, groups) in interval order
+        lens = ordered.T.reshape(-1)                          # group-major, rank-minor
+        ranks = np.tile(np.arange(R, dtype=np.int64), 1 << ell)
+        local = local_starts.T.reshape(-1)
+    keep = lens > 0
+    lens, ranks, local = lens[keep], ranks[keep], local[keep]
+    gstart = np.cumsum(lens) - lens
+    return ranks, local, lens, gstart
+
+
+def exchange_plan(hists: np.ndarray, kind: str, width: int, n: int, local_ns, world: int):
+    """Per level: which local bit range every source rank sends to every owner,
+    and the owner's merge tasks.  Identical on every rank."""
+    total_words = (n + 63) >> 6
+    ranges = word_ranges(total_words, world)
+    levels = []
+    for ell in range(width):
+        ranks, local, lens, gstart = level_plan(hists, kind, width, ell)
+        per_dest = []
+        for d, (w0, w1) in enumerate(ranges):
+            b0, b1 = 64 * w0, min(64 * w1, n)
+            if b1 <= b0:
+                per_dest.append(None)
+                continue
+            # pieces intersecting [b0, b1)
+            k0 = int(np.searchsorted(gstart + lens, b0, side="right"))
+            k1 = int(np.searchsorted(gstart, b1, side="left"))
+            sel = slice(k0, k1)
+            pr, pl, pn, pg = ranks[sel], local[sel], lens[sel], gstart[sel]
+            # local bit range needed from each source rank (contiguous: the local
+            # level is the concatenation of the rank's pieces in interval order)
+            lo = np.maximum(pl + np.maximum(b0 - pg, 0), 0)
+            hi = pl + np.minimum(pg + pn, b1) - pg
+            src_rng = []
+            for r in range(world):
+                m = pr == r
+                if m.any():
+                    src_rng.append((int(lo[m].min()) >> 6, (int(hi[m].max()) + 63) >> 6))
+                else:
+                    src_rng.append((0, 0))
+            per_dest.append(dict(words=(w0, w1), ranks=pr, local=pl, lens=pn, gstart=pg, src=src_rng))
+        levels.append(per_dest)
+    return ranges, levels
+
+
+def build_sharded(local_text, sigma: int, kind: str = "wm", group=None, *, ops=None, gather: bool = False):
+    """Sharded build over the ranks of ``group`` (default: the world group).
+
+    Every rank passes its own contiguous shard of the text (rank order = text
+    order).  Returns this rank's ShardedResult; with ``gather`` rank 0 also gets
+    the full level words (attribute ``full_words``).  ``ops`` supplies the local
+    build and the merge; the default uses this rank's CUDA device.
+    """
+    import torch
+    import torch.distributed as dist
+
+    if kind not in ("wt", "wm"):
+        raise ValueError(f"unknown structure kind {kind!r}")
+    sigma = int(sigma)
+    if sigma < 1:
+        raise ValueError("alphabet size must be at least 1")
+    ops = ops or CudaOps()
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    dev = ops.device
+    width = code_width(sigma)
+
+    n_local = int(local_text.numel() if hasattr(local_text, "numel") else np.asarray(local_text).size)
+    ns = torch.zeros(world, dtype=torch.int64, device=dev)
+    mine = torch.tensor([n_local], dtype=torch.int64, device=dev)
+    dist.all_gather_into_tensor(ns, mine, group=group)
+    local_ns = [int(v) for v in ns.cpu().tolist()]
+    n = sum(local_ns)
+
+    # 1. local build (no communication)
+    words, hist, bad = ops.local_build(local_text, sigma, kind)
+    flag = torch.tensor([1 if bad else 0], dtype=torch.int64, device=dev)
+    dist.all_reduce(flag, group=group)
+    if int(flag.item()):
+        raise ValueError(f"symbols must lie in [0, {sigma})")
+    # 2. histograms -> plan
+    allh = torch.empty((world, 1 << width), dtype=torch.int64, device=dev)
+    dist.all_gather_into_tensor(allh, hist.reshape(1, -1).contiguous(), group=group)
+    hists = allh.cpu().numpy()
+    ghist = hists.sum(axis=0)
+    zeros = zeros_from_hist(ghist, width) if width else []
+    total_words = (n + 63) >> 6
+    ranges, plans = exchange_plan(hists, kind, width, n, local_ns, world)
+    w0, w1 = ranges[rank]
+    owned = torch.zeros((width, max(w1 - w0, 0)), dtype=torch.int64, device=dev)
+    if width == 0 or n == 0:
+        return ShardedResult(n, sigma, kind, width, w0, w1, owned, zeros, ghist)
+
+    # 3. one all_to_all for every level: the send buffer is grouped by
+    #    destination (levels in order inside), so the receive buffer is grouped
+    #    by source rank with levels in order inside
+    send_parts, send_sizes = [], [0] * world
+    recv_sizes = [0] * world
+    for d in range(world):
+        for ell in range(width):
+            pd = plans[ell][d]
+            if pd is None:
+                continue
+            a, b = pd["src"][rank]
+            if b > a:
+                send_parts.append(words[ell, a:b])
+                send_sizes[d] += b - a
+    for ell in range(width):
+        pd = plans[ell][rank]
+        if pd is not None:
+            for r in range(world):
+                a, b = pd["src"][r]
+                recv_sizes[r] += max(b - a, 0)
+    send = torch.cat(send_parts) if send_parts else torch.zeros(0, dtype=torch.int64, device=dev)
+    recv = torch.empty(sum(recv_sizes), dtype=torch.int64, device=dev)
+    dist.all_to_all_single(recv, send, recv_sizes, send_sizes, group=group)
+
+    # receive-buffer offsets: segments arrive grouped by source rank, level-major inside
+    seg_base = np.cumsum([0] + recv_sizes[:-1])
+    cursor = list(seg_base)
+    # 4. shift-merge every owned level range
+    for ell in range(width):
+        pd = plans[ell][rank]
+        if pd is None:
+            continue
+        off = np.zeros(world, dtype=np.int64)  # word offset of (ell, r) segment in recv
+        for r in range(world):
+            a, b = pd["src"][r]
+            off[r] = cursor[r] - a  # so that local word x of rank r is recv[off[r] + x]
+            cursor[r] += max(b - a, 0)
+        pr = pd["ranks"]
+        src_starts = 64 * off[pr] + pd["local"]
+        bounds = np.concatenate([pd["gstart"], [pd["gstart"][-1] + pd["lens"][-1]]]).astype(np.int64)
+        ops.merge(owned[ell], w0, w1, n, bounds, src_starts.astype(np.int64), recv)
+    res = ShardedResult(n, sigma, kind, width, w0, w1, owned, zeros, ghist)
+    if gather:
+        res.full_words = _gather_levels(owned, ranges, width, total_words, rank, world, group, dev)
+    return res
+
+
+def _gather_levels(owned, ranges, width, total_words, rank, world, group, dev):
+    """Assemble the full levels on rank 0 (owned ranges padded to equal size for gather)."""
+    import torch
+    import torch.distributed as dist
+
+    sizes = [(b - a) * width for a, b in ranges]
+    mx = max(sizes) if sizes else 0
+    flat = torch.zeros(mx, dtype=torch.int64, device=dev)
+    flat[: sizes[rank]] = owned.reshape(-1)
+    if rank == 0:
+        parts = [torch.empty(mx, dtype=torch.int64, device=dev) for _ in range(world)]
+        dist.gather(flat, parts, dst=0, group=group)
+        full = torch.empty((width, total_words), dtype=torch.int64, device=dev)
+        for (a, b), p, sz in zip(ranges, parts, sizes):
+            full[:, a:b] = p[:sz].reshape(width, b - a)
+        return full
+    dist.gather(flat, None, dst=0, group=group)
+    return None
+
+
+class CudaOps:
+    """Local build + merge on this rank's CUDA device (hand-written kernels)."""
+
+    def __init__(self, device=None):
+        import torch
+
+        from .device import DeviceBuilder
+
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        self.builder = DeviceBuilder(self.device)
+
+    def local_build(self, text, sigma: int, kind: str):
+        import torch
+
+        if not isinstance(text, torch.Tensor):
+            from .construct import _device_text
+
+            text = torch.from_numpy(_device_text(np.ascontiguousarray(np.asarray(text)), sigma))
+        text = text.to(self.device)
+        res = self.builder.build(text, sigma, kind, check=False)
+        bad = bool(int(res.status.item()) & 1) if res.status is not None else False
+        return res.level_words, res.hist, bad
+
+    def merge(self, dst_row, word_lo: int, word_hi: int, n_bits: int, bounds, src_starts, src):
+        import torch
+
+        b = torch.from_numpy(bounds).to(self.device)
+        s = torch.from_numpy(src_starts).to(self.device)
+        self.builder.merge_bits(dst_row, word_lo, word_hi, n_bits, b, s, src, dst_offset_words=word_lo)

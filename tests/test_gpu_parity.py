@@ -164,3 +164,26 @@ def test_config_c1_vs_oracle():
     text = rng.integers(0, 256, 1 << 20, dtype=np.uint8)
     for kind in ("wt", "wm"):
         assert wv.dump_structure(wv.build_structure(text, 256, kind)) == ref_dump(text, 256, kind)
+
+
+def test_sharded_build_world1_nccl_matches_single_build(rng):
+    """The multi-GPU path (CUDA local build + wvlt_merge_bits + NCCL collectives) at world size 1."""
+    import os
+
+    import torch.distributed as dist
+
+    from paper_1702_07578_b200.distributed import build_sharded
+
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29733")
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        for sigma, kind in ((256, "wm"), (256, "wt"), (70000, "wm"), (5, "wt")):
+            text = random_text(rng, 123_457, sigma)
+            res = build_sharded(torch.from_numpy(text).cuda(), sigma, kind, gather=True)
+            words, zeros, _ = oracle.build(text, sigma, kind, "pc")
+            assert np.array_equal(res.full_words.cpu().numpy().view(np.uint64), words), (sigma, kind)
+            if kind == "wm":
+                assert list(res.zeros) == zeros
+    finally:
+        dist.destroy_process_group()
