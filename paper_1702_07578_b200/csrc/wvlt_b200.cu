@@ -251,45 +251,50 @@ __global__ void __launch_bounds__(HIST_WARPS * 32) hist_u8_kernel(const uint8_t*
   if (bad) atomicOr(status, WVLT_STATUS_RANGE);
 }
 
-// Generic histogram for wide symbols / wide alphabets: shared-memory bins when
-// 2^w fits, else warp-aggregated global atomics (Zipf heavy hitters collapse
-// to one atomic per warp via __match_any_sync).
-template <typename TIn, bool SMEM>
-__global__ void __launch_bounds__(256) hist_generic_kernel(const TIn* __restrict__ text, int64_t n, int w,
-                                                           unsigned long long* __restrict__ hist,
-                                                           int32_t* __restrict__ status) {
-  extern __shared__ unsigned s_bins[];
-  const int64_t nb = 1ll << w;
-  if (SMEM) {
-    for (int64_t i = threadIdx.x; i < nb; i += blockDim.x) s_bins[i] = 0;
-    __syncthreads();
-  }
+// Generic histogram for wide symbols / wide alphabets.  Bins [0, 2^min(w,16))
+// live in shared memory as 16-bit counters packed two per word (128 KB at
+// most); an increment that wraps a counter is detected from the atomic's
+// returned old value and carried into the global histogram exactly (low half:
+// the carry that leaked into the high half is taken back).  Bins at or above
+// 2^16 (code widths 17..24) go to global atomics.
+constexpr int HISTG_THREADS = 1024;
+template <typename TIn>
+__global__ void __launch_bounds__(HISTG_THREADS) hist_generic_kernel(const TIn* __restrict__ text, int64_t n, int w,
+                                                                    unsigned long long* __restrict__ hist,
+                                                                    int32_t* __restrict__ status) {
+  extern __shared__ uint32_t s_pairs[];
+  const int sw = w < 16 ? w : 16;          // shared-memory window: bins [0, 2^sw)
+  const int npairs = ((1 << sw) + 1) >> 1;
+  for (int i = threadIdx.x; i < npairs; i += blockDim.x) s_pairs[i] = 0;
+  __syncthreads();
   unsigned bad = 0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  const int64_t start = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t nround = (n + stride - 1) / stride;
-  for (int64_t r = 0; r < nround; ++r) {  // warp-uniform trip count for __match_any_sync
-    const int64_t i = start + r * stride;
-    const bool valid = i < n;
-    uint32_t v = valid ? (uint32_t)__ldcs(text + i) : 0u;
-    const bool ok = valid && (w >= 32 || (v >> w) == 0);
-    if (valid && !ok) bad = 1;
-    if (SMEM) {
-      if (ok) atomicAdd(&s_bins[v], 1u);
-    } else {
-      const unsigned act = __ballot_sync(FULL, ok);
-      if (ok) {
-        const unsigned peers = __match_any_sync(act, v);
-        if ((threadIdx.x & 31) == (unsigned)(__ffs(peers) - 1) && hist)
-          atomicAdd(&hist[v], (unsigned long long)__popc(peers));
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint32_t v = (uint32_t)__ldcs(text + i);
+    if (w < 32 && (v >> w)) {
+      bad = 1;
+      continue;
+    }
+    if ((v >> sw) == 0) {
+      const uint32_t hi = v & 1u;
+      const uint32_t old = atomicAdd(&s_pairs[v >> 1], hi ? 0x10000u : 1u);
+      const uint32_t half = hi ? (old >> 16) : (old & 0xFFFFu);
+      if (half == 0xFFFFu) {  // wrapped: carry 2^16 to the global bin
+        if (!hi) atomicSub(&s_pairs[v >> 1], 0x10000u);  // the carry leaked into the high half
+        if (hist) atomicAdd(&hist[v], 65536ull);
       }
+    } else if (hist) {
+      atomicAdd(&hist[v], 1ull);
     }
   }
   if (bad) atomicOr(status, WVLT_STATUS_RANGE);
-  if (SMEM && hist) {
-    __syncthreads();
-    for (int64_t i = threadIdx.x; i < nb; i += blockDim.x)
-      if (s_bins[i]) atomicAdd(&hist[i], (unsigned long long)s_bins[i]);
+  __syncthreads();
+  if (hist) {
+    for (int i = threadIdx.x; i < npairs; i += blockDim.x) {
+      const uint32_t c = s_pairs[i];
+      if (c & 0xFFFFu) atomicAdd(&hist[2 * i], (unsigned long long)(c & 0xFFFFu));
+      if ((c >> 16) && 2 * i + 1 < (1 << sw)) atomicAdd(&hist[2 * i + 1], (unsigned long long)(c >> 16));
+    }
   }
 }
 
@@ -1415,19 +1420,19 @@ int sm_count() {
 // Generic full histogram (wide symbols / alphabets) or the range check alone (hist == null).
 cudaError_t launch_hist_generic(const void* text, int sym_bytes, int64_t n, int w, unsigned long long* hist,
                                 int32_t* status, cudaStream_t s) {
-  const int blocks = sm_count() * 4;
-  const bool smem = w <= 14;
-  const size_t sb = smem ? ((size_t)4 << w) : 0;
-  if (smem && sb > 48 * 1024) {
-    cudaError_t e;
-    if (sym_bytes == 1) e = cudaFuncSetAttribute(hist_generic_kernel<uint8_t, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
-    else if (sym_bytes == 2) e = cudaFuncSetAttribute(hist_generic_kernel<uint16_t, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
-    else e = cudaFuncSetAttribute(hist_generic_kernel<uint32_t, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
-    if (e != cudaSuccess) return e;
-  }
-#define WVLT_HG(T)                                                                                   \
-  (smem ? (hist_generic_kernel<T, true><<<blocks, 256, sb, s>>>((const T*)text, n, w, hist, status)) \
-        : (hist_generic_kernel<T, false><<<blocks, 256, 0, s>>>((const T*)text, n, w, hist, status)))
+  const int sw = w < 16 ? w : 16;
+  const size_t sb = (size_t)((((1 << sw) + 1) >> 1)) * 4;
+  const int per_sm = sb > 100 * 1024 ? 1 : 2;
+  const int blocks = sm_count() * per_sm;
+#define WVLT_HG(T)                                                                                          \
+  do {                                                                                                      \
+    static bool set = false;                                                                                \
+    if (!set) {                                                                                             \
+      cudaFuncSetAttribute(hist_generic_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 1024); \
+      set = true;                                                                                           \
+    }                                                                                                       \
+    hist_generic_kernel<T><<<blocks, HISTG_THREADS, sb, s>>>((const T*)text, n, w, hist, status);          \
+  } while (0)
   if (sym_bytes == 1) WVLT_HG(uint8_t);
   else if (sym_bytes == 2) WVLT_HG(uint16_t);
   else WVLT_HG(uint32_t);
