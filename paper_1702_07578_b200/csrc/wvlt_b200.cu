@@ -1033,13 +1033,15 @@ __global__ void __launch_bounds__(PASS_THREADS + TAB_WARP_THREADS, 2) level_pass
 }
 
 // Byte variant (all passes of byte alphabets): SIMD within a register.  Thread
-// t owns the two 8-symbol runs [8t, 8t+8) and [T/2 + 8t, T/2 + 8t + 8) of the
-// tile-local order (two 64-bit shared loads): bits and in-thread ranks are
-// computed four symbols per instruction (byte-lane multiply prefix sums), the
-// CTA prefix of both halves by one packed warp-shuffle scan, and every symbol
-// is stored once per split with a predicated zeros/ones store pair.  With 8
-// symbols per half the 32 lanes' destinations of one store stream span about
-// 128 bytes, so each store is a single conflict-free wavefront.
+// t owns the two 8-symbol halves [8t, 8t+8) and [T/2 + 8t, T/2 + 8t + 8) of
+// the tile-local order (two 64-bit shared loads).  A split sorts each half in
+// registers by the split bit with two byte permutes (PRMT selectors from a
+// 256-entry shared table indexed by the half's 8-bit mask), so the half's
+// zeros and ones become two contiguous byte runs; the CTA prefix of both
+// halves comes from one packed warp-shuffle scan, and byte k of a sorted half
+// is stored once, to the zeros run when k < (number of zeros), else to the
+// ones run -- no per-symbol rank extraction.  The last split of a pass with
+// output scatters symbol by symbol to HBM.
 template <int K>
 __global__ void __launch_bounds__(PASS_THREADS + TAB_WARP_THREADS, 2) level_pass_u8_kernel(const PassArgs a) {
   using S = PassSmem<uint8_t, K, 16>;
@@ -1057,6 +1059,7 @@ __global__ void __launch_bounds__(PASS_THREADS + TAB_WARP_THREADS, 2) level_pass
   __shared__ TileTables<uint8_t, K> tt;
   __shared__ __align__(16) uint32_t s_wtot[2][NW];
   __shared__ uint32_t s_ncnt[2 * NDIG * NDIG];
+  __shared__ uint32_t s_lut[256];  // PRMT selectors: zeros of the 8-bit mask first, then ones
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int w = a.width, l0 = a.level;
@@ -1078,6 +1081,14 @@ __global__ void __launch_bounds__(PASS_THREADS + TAB_WARP_THREADS, 2) level_pass
     for (int p = tid; p < T; p += PASS_THREADS) buf[p] = p < cnt ? src[p] : (uint8_t)0xFF;
   }
   if (tid < 2 * NDIG * NDIG) s_ncnt[tid] = 0;
+  if (tid < 256) {
+    uint32_t sel = 0;
+    int o = 0;
+    for (int bit = 0; bit < 2; ++bit)
+      for (int i = 0; i < 8; ++i)
+        if (((tid >> i) & 1) == bit) sel |= (uint32_t)i << (4 * o++);
+    s_lut[tid] = sel;
+  }
   bar_sync(1, PASS_THREADS);
   if (!wm) bar_arrive(3, ALLT);
 
@@ -1091,18 +1102,13 @@ __global__ void __launch_bounds__(PASS_THREADS + TAB_WARP_THREADS, 2) level_pass
     const uint2 q0 = reinterpret_cast<const uint2*>(cur)[tid];
     const uint2 q1 = reinterpret_cast<const uint2*>(cur + H)[tid];
     const uint32_t x[4] = {q0.x, q0.y, q1.x, q1.y};
-    uint32_t b[4], p[4];
+    uint32_t b[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) b[k] = (x[k] >> sh) & B1;
-    // inclusive ones count through each byte, per half
-    p[0] = b[0] * B1;
-    p[1] = (b[1] + (p[0] >> 24)) * B1;
-    p[2] = b[2] * B1;
-    p[3] = (b[3] + (p[2] >> 24)) * B1;
-    const uint32_t ones0 = p[1] >> 24, ones1 = p[3] >> 24;
     // this thread's level bits: byte t (first half) and byte T/16 + t (second half)
     const uint32_t m0 = ((b[0] * 0x01020408u) >> 24) | (((b[1] * 0x01020408u) >> 24) << 4);
     const uint32_t m1 = ((b[2] * 0x01020408u) >> 24) | (((b[3] * 0x01020408u) >> 24) << 4);
+    const uint32_t ones0 = __popc(m0), ones1 = __popc(m1);
     if (j == 0) {
       // level l0 is in global order already: byte stores (32 lanes = 32 consecutive bytes)
       uint8_t* g8 = reinterpret_cast<uint8_t*>(a.words + (int64_t)l0 * a.nwords) + (base >> 3);
@@ -1139,13 +1145,20 @@ __global__ void __launch_bounds__(PASS_THREADS + TAB_WARP_THREADS, 2) level_pass
     const int ZB[2] = {8 * tid - opre0, H + 8 * tid - opre1};
     if (j + 1 < K) {
       const uint32_t nxt = sbase + (uint32_t)(j + 1) * T;
+      // each half sorted in registers (zeros first): byte k goes to the zeros
+      // run (k < nz) or to the ones run, one store per symbol
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
+      for (int hh = 0; hh < 2; ++hh) {
+        const uint32_t sel = s_lut[hh ? m1 : m0];
+        const uint32_t sv[2] = {__byte_perm(x[2 * hh], x[2 * hh + 1], sel & 0xFFFFu),
+                                __byte_perm(x[2 * hh], x[2 * hh + 1], sel >> 16)};
+        const int nz = 8 - (int)(hh ? ones1 : ones0);
+        const uint32_t za = nxt + (uint32_t)ZB[hh];
+        const uint32_t oa = nxt + (uint32_t)(OB[hh] + 1 - nz);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int r = (int)__byte_perm(p[k], 0, 0x4440 + i);
-          st_split_u8(nxt + (uint32_t)(OB[k >> 1] + r), nxt + (uint32_t)(ZB[k >> 1] + 4 * (k & 1) + i - r),
-                      b[k] & (0xFFu << (8 * i)), x[k] >> (8 * i));
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t addr = (kk < nz ? za : oa) + kk;
+          asm volatile("st.shared.u8 [%0], %1;" ::"r"(addr), "r"(sv[kk >> 2] >> (8 * (kk & 3))) : "memory");
         }
       }
       bar_sync(1, PASS_THREADS);
@@ -1157,6 +1170,11 @@ __global__ void __launch_bounds__(PASS_THREADS + TAB_WARP_THREADS, 2) level_pass
       const int nshift = w - l0 - K - a.nK;
       const unsigned nmask = (1u << a.nK) - 1u;
       const bool q1 = tt.q1;
+      uint32_t p[4];  // inclusive ones count through each byte, per half
+      p[0] = b[0] * B1;
+      p[1] = (b[1] + (p[0] >> 24)) * B1;
+      p[2] = b[2] * B1;
+      p[3] = (b[3] + (p[2] >> 24)) * B1;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
 #pragma unroll
