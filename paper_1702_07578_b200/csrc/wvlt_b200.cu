@@ -48,6 +48,12 @@ namespace {
 constexpr int KMAX = 4;             // levels fused per pass
 constexpr int NDIG = 1 << KMAX;     // digit bins per pass
 constexpr int PASS_THREADS = 512;
+#ifndef U8_CTAS_PER_SM
+#define U8_CTAS_PER_SM 3
+#endif
+#ifndef U8_THREADS
+#define U8_THREADS 512  // compute threads of the byte pass kernel (tile = 16 per thread)
+#endif
 constexpr int MAXP = 32;            // passes per build (width <= 24 => <= 6 at K = 4)
 constexpr unsigned FULL = 0xffffffffu;
 
@@ -109,6 +115,24 @@ __device__ __forceinline__ void st_split(uint32_t a1, uint32_t a0, uint32_t one,
   else st_split_u32(a1, a0, one, v);
 }
 
+// PRMT selectors that stably sort 8 bytes by an 8-bit mask (zeros first, then
+// ones), two nibble selectors per byte pair packed 8 x 4 bits; built at compile
+// time and copied into shared memory by each byte pass CTA.
+struct SortLut {
+  uint32_t sel[256];
+  constexpr SortLut() : sel() {
+    for (int m = 0; m < 256; ++m) {
+      uint32_t v = 0;
+      int o = 0;
+      for (int bit = 0; bit < 2; ++bit)
+        for (int i = 0; i < 8; ++i)
+          if (((m >> i) & 1) == bit) v |= (uint32_t)i << (4 * o++);
+      sel[m] = v;
+    }
+  }
+};
+__device__ constexpr SortLut g_sort_lut{};
+
 __device__ __forceinline__ void bar_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
@@ -131,7 +155,7 @@ constexpr int HIST_WARPS = 4;
 #define WVLT_E_SMALL 16
 #endif
 constexpr int E_SMALL = WVLT_E_SMALL;  // symbols per thread per split for 1-2 byte symbols
-constexpr int TILE_U8 = PASS_THREADS * E_SMALL;  // tile of pass 0 for byte symbols
+constexpr int TILE_U8 = U8_THREADS * 16;  // tile of every pass that reads byte symbols
 
 template <int W>
 __global__ void __launch_bounds__(HIST_WARPS * 32) hist_u8_kernel(const uint8_t* __restrict__ text, int64_t n,
@@ -673,9 +697,9 @@ struct PassArgs {
   int64_t corr_off[KMAX + 1];
 };
 
-template <typename TIn, int K, int E>
+template <typename TIn, int K, int E, int NT = PASS_THREADS>
 struct PassSmem {
-  static constexpr int T = PASS_THREADS * E;
+  static constexpr int T = NT * E;
   static constexpr int NC = T / 32;
   // order buffers A_l .. A_{l+K-1} in the tile-local digit orders d_0 .. d_{K-1}
   static constexpr size_t buf_bytes = (size_t)K * T * sizeof(TIn);
@@ -710,6 +734,7 @@ struct TileTables {
   TOut* row[NDIG];          // uniform tiles: output row of each numeric digit (dst + offset)
   int thr[NDIG];            // local position where that run crosses into the next pass's next tile
   int64_t ft[NDIG];         // first next-pass tile of each run
+  int ipre[NDIG + 1];       // byte copy-out: 16-byte destination chunks before each group (tile order)
   int q1;                   // tile lies inside one level-l node (always for WM)
 };
 
@@ -780,6 +805,26 @@ __device__ __forceinline__ void table_warp(const PassArgs& a, TileTables<TOut, K
       const int64_t ntile = (int64_t)1 << a.ntshift;
       tt.thr[lane] = tt.ls[K][d] + (int)(ntile - (g & (ntile - 1)));
       tt.ft[lane] = g >> a.ntshift;
+    }
+    if (sizeof(TOut) == 1 && a.has_out) {
+      // 16-byte-aligned destination chunks per group, prefix in tile order
+      __syncwarp();
+      int c = 0;
+      if (lane < nd) {
+        const int n = tt.cnt[K][lane];
+        if (n) {
+          const uintptr_t lo = (uintptr_t)(tt.row[rev_bits((unsigned)lane, K)] + tt.ls[K][lane]);
+          c = (int)(((lo + n - 1) >> 4) - (lo >> 4) + 1);
+        }
+      }
+      int incl = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += t;
+      }
+      if (lane < nd) tt.ipre[lane] = incl - c;
+      if (lane == nd - 1) tt.ipre[nd] = incl;
     }
   }
   __threadfence_block();
@@ -1032,6 +1077,63 @@ __global__ void __launch_bounds__(PASS_THREADS + TAB_WARP_THREADS, 2) level_pass
     emit_multinode<TIn, TOut, K>(a, tt, buf, T, cnt, tid, lane, PASS_THREADS);
 }
 
+// Copy-out of a uniform byte tile sorted into `fin` (groups in tile order):
+// work items are the 16-byte-aligned destination chunks of every group's run
+// (TileTables::ipre); a full chunk is read from shared memory at any byte
+// offset (five words, four PRMT) and written with one 16-byte store, edge
+// chunks byte by byte.  Each symbol also counts its next-pass digit per
+// (run, next tile) in s_ncnt.
+template <int K>
+__device__ __forceinline__ void copy_out_u8(const PassArgs& a, const TileTables<uint8_t, K>& tt, const uint8_t* fin,
+                                            uint32_t* s_ncnt, int tid) {
+  constexpr int nd = 1 << K;
+  const int nK = a.nK;
+  const int nshift = a.width - a.level - K - nK;
+  const uint32_t nmask = (1u << nK) - 1u;
+  const uint32_t nrep = nmask * 0x01010101u;
+  const uint32_t keep = a.kind == WVLT_KIND_WM ? ((1u << (a.width - a.level - K)) - 1u) : 0xFFu;
+  const uint32_t krep = keep * 0x01010101u;
+  const int nitems = tt.ipre[nd];
+  const uint32_t* fw = reinterpret_cast<const uint32_t*>(fin);
+  for (int it = tid; it < nitems; it += U8_THREADS) {
+    int d = 0;
+#pragma unroll
+    for (int s = nd / 2; s >= 1; s >>= 1)
+      if (tt.ipre[d + s] <= it) d += s;
+    const int num = (int)rev_bits((unsigned)d, K);
+    uint8_t* row = tt.row[num];
+    const int s0 = tt.ls[K][d], e0 = s0 + tt.cnt[K][d];
+    const uintptr_t D = (((uintptr_t)(row + s0) >> 4) + (uintptr_t)(it - tt.ipre[d])) << 4;
+    const int p = (int)(D - (uintptr_t)row);  // tile-local position of the chunk's first byte
+    const int thr = tt.thr[num];
+    const uint32_t cb = (uint32_t)(num << 1) << nK;
+    if (p >= s0 && p + 16 <= e0 && (p >= thr || p + 16 <= thr)) {
+      const uint32_t* q = fw + (p >> 2);
+      const uint32_t sel = 0x3210u + 0x1111u * (uint32_t)(p & 3);
+      const uint32_t w0 = q[0], w1 = q[1], w2 = q[2], w3 = q[3], w4 = q[4];
+      uint32_t v[4] = {__byte_perm(w0, w1, sel), __byte_perm(w1, w2, sel), __byte_perm(w2, w3, sel),
+                       __byte_perm(w3, w4, sel)};
+      uint32_t* cnt = s_ncnt + (cb | (p >= thr ? (1u << nK) : 0u));
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t m = (v[k] >> nshift) & nrep;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) atomicAdd(cnt + __byte_perm(m, 0, 0x4440 + i), 1u);
+        v[k] &= krep;
+      }
+      asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(D), "r"(v[0]), "r"(v[1]), "r"(v[2]),
+                   "r"(v[3]) : "memory");
+    } else {
+      const int lo = p > s0 ? p : s0, hi = p + 16 < e0 ? p + 16 : e0;
+      for (int i = lo; i < hi; ++i) {
+        const uint32_t x = fin[i];
+        row[i] = (uint8_t)(x & keep);
+        atomicAdd(s_ncnt + (cb | (i >= thr ? (1u << nK) : 0u) | ((x >> nshift) & nmask)), 1u);
+      }
+    }
+  }
+}
+
 // Byte variant (all passes of byte alphabets): SIMD within a register.  Thread
 // t owns the two 8-symbol halves [8t, 8t+8) and [T/2 + 8t, T/2 + 8t + 8) of
 // the tile-local order (two 64-bit shared loads).  A split sorts each half in
@@ -1043,13 +1145,13 @@ __global__ void __launch_bounds__(PASS_THREADS + TAB_WARP_THREADS, 2) level_pass
 // ones run -- no per-symbol rank extraction.  The last split of a pass with
 // output scatters symbol by symbol to HBM.
 template <int K>
-__global__ void __launch_bounds__(PASS_THREADS + TAB_WARP_THREADS, 2) level_pass_u8_kernel(const PassArgs a) {
-  using S = PassSmem<uint8_t, K, 16>;
+__global__ void __launch_bounds__(U8_THREADS + TAB_WARP_THREADS, U8_CTAS_PER_SM) level_pass_u8_kernel(const PassArgs a) {
+  using S = PassSmem<uint8_t, K, 16, U8_THREADS>;
   constexpr int T = S::T;
   constexpr int H = T / 2;
   constexpr int NC = S::NC;
-  constexpr int NW = PASS_THREADS / 32;
-  constexpr int ALLT = PASS_THREADS + TAB_WARP_THREADS;
+  constexpr int NW = U8_THREADS / 32;
+  constexpr int ALLT = U8_THREADS + TAB_WARP_THREADS;
   constexpr int nd = 1 << K;
   constexpr uint32_t B1 = 0x01010101u;
   extern __shared__ __align__(16) unsigned char smem[];
@@ -1078,18 +1180,11 @@ __global__ void __launch_bounds__(PASS_THREADS + TAB_WARP_THREADS, 2) level_pass
   if (cnt == T && ((((uintptr_t)src) & 15) == 0)) {
     reinterpret_cast<uint4*>(buf)[tid] = __ldcs(reinterpret_cast<const uint4*>(src) + tid);
   } else {
-    for (int p = tid; p < T; p += PASS_THREADS) buf[p] = p < cnt ? src[p] : (uint8_t)0xFF;
+    for (int p = tid; p < T; p += U8_THREADS) buf[p] = p < cnt ? src[p] : (uint8_t)0xFF;
   }
-  if (tid < 2 * NDIG * NDIG) s_ncnt[tid] = 0;
-  if (tid < 256) {
-    uint32_t sel = 0;
-    int o = 0;
-    for (int bit = 0; bit < 2; ++bit)
-      for (int i = 0; i < 8; ++i)
-        if (((tid >> i) & 1) == bit) sel |= (uint32_t)i << (4 * o++);
-    s_lut[tid] = sel;
-  }
-  bar_sync(1, PASS_THREADS);
+  for (int i = tid; i < 2 * NDIG * NDIG; i += U8_THREADS) s_ncnt[i] = 0;
+  for (int i = tid; i < 256; i += U8_THREADS) s_lut[i] = g_sort_lut.sel[i];
+  bar_sync(1, U8_THREADS);
   if (!wm) bar_arrive(3, ALLT);
 
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(buf);
@@ -1131,7 +1226,7 @@ __global__ void __launch_bounds__(PASS_THREADS + TAB_WARP_THREADS, 2) level_pass
       if (lane >= o) incl += t;
     }
     if (lane == 31) s_wtot[j & 1][wid] = incl;
-    bar_sync(1, PASS_THREADS);
+    bar_sync(1, U8_THREADS);
     const uint32_t wv = lane < NW ? s_wtot[j & 1][lane] : 0u;
     const uint32_t wpre = __reduce_add_sync(FULL, lane < wid ? wv : 0u);
     const uint32_t tot = __reduce_add_sync(FULL, wv);
@@ -1143,8 +1238,16 @@ __global__ void __launch_bounds__(PASS_THREADS + TAB_WARP_THREADS, 2) level_pass
     // ones: OBh + (inclusive rank); zeros: ZBh + symbol index - (inclusive ones)
     const int OB[2] = {Z + opre0 - 1, Z + opre1 - 1};
     const int ZB[2] = {8 * tid - opre0, H + 8 * tid - opre1};
-    if (j + 1 < K) {
-      const uint32_t nxt = sbase + (uint32_t)(j + 1) * T;
+    const bool last = j + 1 == K;
+    bool in_smem = !last;
+    if (last) {
+      bar_sync(2, ALLT);  // placement tables
+      in_smem = tt.q1;
+    }
+    if (in_smem) {
+      // the last split of a uniform tile goes to buffer 0 (free once the
+      // table warp is done) and is then copied out run by run
+      const uint32_t nxt = sbase + (last ? 0u : (uint32_t)(j + 1) * T);
       // each half sorted in registers (zeros first): byte k goes to the zeros
       // run (k < nz) or to the ones run, one store per symbol
 #pragma unroll
@@ -1153,23 +1256,34 @@ __global__ void __launch_bounds__(PASS_THREADS + TAB_WARP_THREADS, 2) level_pass
         const uint32_t sv[2] = {__byte_perm(x[2 * hh], x[2 * hh + 1], sel & 0xFFFFu),
                                 __byte_perm(x[2 * hh], x[2 * hh + 1], sel >> 16)};
         const int nz = 8 - (int)(hh ? ones1 : ones0);
-        const uint32_t za = nxt + (uint32_t)ZB[hh];
-        const uint32_t oa = nxt + (uint32_t)(OB[hh] + 1 - nz);
+        const uint32_t za = opaque(nxt + (uint32_t)ZB[hh]);
+        const uint32_t oa = opaque(nxt + (uint32_t)(OB[hh] + 1 - nz));
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           const uint32_t addr = (kk < nz ? za : oa) + kk;
           asm volatile("st.shared.u8 [%0], %1;" ::"r"(addr), "r"(sv[kk >> 2] >> (8 * (kk & 3))) : "memory");
         }
       }
-      bar_sync(1, PASS_THREADS);
+      bar_sync(1, U8_THREADS);
+      if (last) {
+        copy_out_u8<K>(a, tt, buf, s_ncnt, tid);
+        bar_sync(1, U8_THREADS);
+        const int ncount = 2 * nd << a.nK;
+        const unsigned nmask = (1u << a.nK) - 1u;
+        for (int i = tid; i < ncount; i += U8_THREADS) {
+          const uint32_t v = s_ncnt[i];
+          if (v) {
+            const int slot = i >> a.nK, ne = i & (int)nmask;
+            atomicAdd(&a.ncnt[(int64_t)ne * a.nntiles + tt.ft[slot >> 1] + (slot & 1)], v);
+          }
+        }
+      }
     } else {
-      // last split: straight to HBM, counting the next pass's digits per (run, next tile)
-      bar_sync(2, ALLT);  // placement tables
+      // last split of a tile spanning several nodes (WT): symbol by symbol to HBM
       const uint32_t keep = wm ? ((w - l0 - K) >= 32 ? FULL : ((1u << (w - l0 - K)) - 1u)) : FULL;
       const int eshift = w - l0 - K;
       const int nshift = w - l0 - K - a.nK;
       const unsigned nmask = (1u << a.nK) - 1u;
-      const bool q1 = tt.q1;
       uint32_t p[4];  // inclusive ones count through each byte, per half
       p[0] = b[0] * B1;
       p[1] = (b[1] + (p[0] >> 24)) * B1;
@@ -1183,42 +1297,25 @@ __global__ void __launch_bounds__(PASS_THREADS + TAB_WARP_THREADS, 2) level_pass
           const uint32_t xv = __byte_perm(x[k], 0, 0x4440 + i);
           const int pos = (b[k] & (0xFFu << (8 * i))) ? OB[k >> 1] + r : ZB[k >> 1] + 4 * (k & 1) + i - r;
           if (pos < cnt) {
-            if (q1) {
-              const unsigned dig = (xv >> eshift) & (nd - 1);
-              tt.row[dig][pos] = (uint8_t)(xv & keep);
-              const unsigned h = pos >= tt.thr[dig] ? 1u : 0u;
-              atomicAdd(&s_ncnt[(((dig << 1) | h) << a.nK) | ((xv >> nshift) & nmask)], 1u);
-            } else {
-              const unsigned d = rev_bits((xv >> eshift) & (nd - 1), K);
-              const uint64_t P = (uint64_t)xv >> eshift;
-              const int64_t gpos = a.corr[a.corr_off[K] + P] + tt.lb[K][d] + pos - tt.ls[K][d];
-              reinterpret_cast<uint8_t*>(a.dst)[gpos] = (uint8_t)(xv & keep);
-              atomicAdd(&a.ncnt[(int64_t)((xv >> nshift) & nmask) * a.nntiles + (gpos >> a.ntshift)], 1u);
-            }
+            const unsigned d = rev_bits((xv >> eshift) & (nd - 1), K);
+            const uint64_t P = (uint64_t)xv >> eshift;
+            const int64_t gpos = a.corr[a.corr_off[K] + P] + tt.lb[K][d] + pos - tt.ls[K][d];
+            reinterpret_cast<uint8_t*>(a.dst)[gpos] = (uint8_t)(xv & keep);
+            atomicAdd(&a.ncnt[(int64_t)((xv >> nshift) & nmask) * a.nntiles + (gpos >> a.ntshift)], 1u);
           }
         }
       }
-      bar_sync(1, PASS_THREADS);
-      if (q1) {
-        const int ncount = 2 * nd << a.nK;
-        for (int i = tid; i < ncount; i += PASS_THREADS) {
-          const uint32_t v = s_ncnt[i];
-          if (v) {
-            const int slot = i >> a.nK, ne = i & (int)nmask;
-            atomicAdd(&a.ncnt[(int64_t)ne * a.nntiles + tt.ft[slot >> 1] + (slot & 1)], v);
-          }
-        }
-      }
+      bar_sync(1, U8_THREADS);
     }
   }
   if (!a.has_out) {
-    bar_sync(1, PASS_THREADS);
+    bar_sync(1, U8_THREADS);
     bar_sync(2, ALLT);
   }
   if (tt.q1)
     emit_uniform<uint8_t, K, NC>(a, tt, bits, wid, lane, NW);
   else
-    emit_multinode<uint8_t, uint8_t, K>(a, tt, buf, T, cnt, tid, lane, PASS_THREADS);
+    emit_multinode<uint8_t, uint8_t, K>(a, tt, buf, T, cnt, tid, lane, U8_THREADS);
 }
 
 // ---------------------------------------------------------------------------
@@ -1281,7 +1378,7 @@ int bytes_for_bits(int bits) { return bits <= 8 ? 1 : (bits <= 16 ? 2 : 4); }
 
 inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
-int tile_for(int in_bytes) { return in_bytes == 4 ? PASS_THREADS * 8 : (in_bytes == 1 ? PASS_THREADS * 16 : PASS_THREADS * E_SMALL); }
+int tile_for(int in_bytes) { return in_bytes == 4 ? PASS_THREADS * 8 : (in_bytes == 1 ? TILE_U8 : PASS_THREADS * E_SMALL); }
 int log2i(int v) {
   int r = 0;
   while ((1 << r) < v) ++r;
@@ -1393,7 +1490,7 @@ cudaError_t launch_pass_k(int K, const PassArgs& a, int64_t ntiles, cudaStream_t
 
 template <int K>
 cudaError_t launch_pass_u8(const PassArgs& a, int64_t ntiles, cudaStream_t s) {
-  using S = PassSmem<uint8_t, K, 16>;
+  using S = PassSmem<uint8_t, K, 16, U8_THREADS>;
   auto kern = level_pass_u8_kernel<K>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -1401,7 +1498,7 @@ cudaError_t launch_pass_u8(const PassArgs& a, int64_t ntiles, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  kern<<<(unsigned)ntiles, PASS_THREADS + TAB_WARP_THREADS, S::total, s>>>(a);
+  kern<<<(unsigned)ntiles, U8_THREADS + TAB_WARP_THREADS, S::total, s>>>(a);
   return cudaGetLastError();
 }
 
