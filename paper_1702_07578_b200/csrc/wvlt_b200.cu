@@ -38,6 +38,8 @@
 // P = q 2^j + e.  Both tables come from the histogram alone (K2).
 
 #include <cuda_runtime.h>
+
+#include <algorithm>
 #include <stdint.h>
 #include <string.h>
 
@@ -132,6 +134,45 @@ struct SortLut {
   }
 };
 __device__ constexpr SortLut g_sort_lut{};
+
+// Byte permute with the selector used as is (nibbles <= 7, so no masking).
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t d;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
+  return d;
+}
+// v >> (32 - k) through the multiplier (keeps the shift off the integer ALU pipe)
+template <int SH>
+__device__ __forceinline__ uint32_t shr_mul(uint32_t v) {
+  if (SH == 0) return v;
+#ifndef U8_SHR_MUL
+  return v >> SH;
+#endif
+  uint32_t d;
+  asm("mul.hi.u32 %0, %1, %2;" : "=r"(d) : "r"(v), "n"(1u << (32 - SH)));
+  return d;
+}
+
+// mbarrier + bulk async copy (global -> shared), completion by transaction bytes
+__device__ __forceinline__ void mbar_init(uint32_t mbar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(mbar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t mbar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(mbar)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tLAB_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra LAB_WAIT;\n\t}" ::"r"(mbar),
+      "r"(parity)
+      : "memory");
+}
 
 __device__ __forceinline__ void bar_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
@@ -1145,177 +1186,218 @@ __device__ __forceinline__ void copy_out_u8(const PassArgs& a, const TileTables<
 // ones run -- no per-symbol rank extraction.  The last split of a pass with
 // output scatters symbol by symbol to HBM.
 template <int K>
+struct U8Smem {
+  static constexpr int T = U8_THREADS * 16;
+  // two staging buffers (tile i in stage i % 2, the next tile prefetched into
+  // the other) + the orders of levels l+1 .. l+K-1
+  // + one buffer for the last split (so stage buffers only ever receive bulk copies)
+  static constexpr size_t buf_bytes = (size_t)(K + 2) * T;
+  static constexpr size_t bits_bytes = PassSmem<uint8_t, K, 16, U8_THREADS>::bits_bytes;
+  static constexpr size_t total = buf_bytes + bits_bytes;
+};
+
+template <int K>
 __global__ void __launch_bounds__(U8_THREADS + TAB_WARP_THREADS, U8_CTAS_PER_SM) level_pass_u8_kernel(const PassArgs a) {
-  using S = PassSmem<uint8_t, K, 16, U8_THREADS>;
+  using S = U8Smem<K>;
   constexpr int T = S::T;
   constexpr int H = T / 2;
-  constexpr int NC = S::NC;
+  constexpr int NC = T / 32;
   constexpr int NW = U8_THREADS / 32;
   constexpr int ALLT = U8_THREADS + TAB_WARP_THREADS;
   constexpr int nd = 1 << K;
   constexpr uint32_t B1 = 0x01010101u;
-  extern __shared__ __align__(16) unsigned char smem[];
-  uint8_t* buf = smem;
+  extern __shared__ __align__(128) unsigned char smem[];
   uint32_t* bits = reinterpret_cast<uint32_t*>(smem + S::buf_bytes);
 
   __shared__ TileTables<uint8_t, K> tt;
   __shared__ __align__(16) uint32_t s_wtot[2][NW];
   __shared__ uint32_t s_ncnt[2 * NDIG * NDIG];
   __shared__ uint32_t s_lut[256];  // PRMT selectors: zeros of the 8-bit mask first, then ones
+  __shared__ __align__(8) uint64_t s_mbar[2];
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int w = a.width, l0 = a.level;
   const bool wm = a.kind == WVLT_KIND_WM;
-  const int64_t tile = blockIdx.x;
-  const int64_t base = tile * T;
-  const int cnt = (int)min((int64_t)T, a.n - base);
+  const int64_t G = gridDim.x;
+  const uint8_t* text = reinterpret_cast<const uint8_t*>(a.src);
+  const bool bulk_ok = (((uintptr_t)text) & 15) == 0;  // full tiles are then 16-byte aligned
 
-  if (wid == NW) {
-    table_warp<uint8_t, uint8_t, K>(a, tt, buf, tile, cnt, lane, ALLT);
+  if (wid == NW) {  // table warp: one tile after the other, in step with the compute warps
+    int i = 0;
+    for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += G, ++i) {
+      if (i) bar_sync(4, ALLT);  // previous tile's tables consumed
+      const int cnt = (int)min((int64_t)T, a.n - tile * T);
+      table_warp<uint8_t, uint8_t, K>(a, tt, smem + (i & 1) * T, tile, cnt, lane, ALLT);
+    }
     return;
   }
 
-  // ---- stage the tile (invalid tail slots = all ones so they sort last) ----
-  const uint8_t* src = reinterpret_cast<const uint8_t*>(a.src) + base;
-  if (cnt == T && ((((uintptr_t)src) & 15) == 0)) {
-    reinterpret_cast<uint4*>(buf)[tid] = __ldcs(reinterpret_cast<const uint4*>(src) + tid);
-  } else {
-    for (int p = tid; p < T; p += U8_THREADS) buf[p] = p < cnt ? src[p] : (uint8_t)0xFF;
-  }
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
+  const uint32_t mbar0 = (uint32_t)__cvta_generic_to_shared(&s_mbar[0]);
+  uint8_t* bits8 = reinterpret_cast<uint8_t*>(bits);
   for (int i = tid; i < 2 * NDIG * NDIG; i += U8_THREADS) s_ncnt[i] = 0;
   for (int i = tid; i < 256; i += U8_THREADS) s_lut[i] = g_sort_lut.sel[i];
+  if (tid == 0) {
+    mbar_init(mbar0, 1);
+    mbar_init(mbar0 + 8, 1);
+    fence_mbar_init();
+    if (bulk_ok && (int64_t)blockIdx.x * T + T <= a.n)
+      bulk_load(sbase, text + (int64_t)blockIdx.x * T, T, mbar0);
+  }
   bar_sync(1, U8_THREADS);
-  if (!wm) bar_arrive(3, ALLT);
 
-  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(buf);
-  uint8_t* bits8 = reinterpret_cast<uint8_t*>(bits);
+  int i = 0;
+#pragma unroll 1
+  for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += G, ++i) {
+    const int st = i & 1;
+    const int64_t base = tile * T;
+    const int cnt = (int)min((int64_t)T, a.n - base);
+    uint8_t* stage = smem + st * T;
+    // prefetch the next tile into the other stage buffer (its previous tile is done)
+    if (tid == 0 && bulk_ok && tile + G < a.ntiles && (tile + G) * T + T <= a.n)
+      bulk_load(sbase + (st ^ 1) * T, text + (tile + G) * T, T, mbar0 + 8 * (st ^ 1));
+    // ---- this tile (invalid tail slots = all ones so they sort last) ----
+    if (bulk_ok && cnt == T) {
+      mbar_wait(mbar0 + 8 * st, (uint32_t)(i >> 1) & 1u);
+    } else {
+      for (int p = tid; p < T; p += U8_THREADS) stage[p] = p < cnt ? text[base + p] : (uint8_t)0xFF;
+      bar_sync(1, U8_THREADS);
+    }
+    if (!wm) bar_arrive(3, ALLT);
 
 #pragma unroll 1
-  for (int j = 0; j < K; ++j) {
-    const int sh = w - 1 - l0 - j;
-    const uint8_t* cur = buf + (size_t)j * T;
-    const uint2 q0 = reinterpret_cast<const uint2*>(cur)[tid];
-    const uint2 q1 = reinterpret_cast<const uint2*>(cur + H)[tid];
-    const uint32_t x[4] = {q0.x, q0.y, q1.x, q1.y};
-    uint32_t b[4];
+    for (int j = 0; j < K; ++j) {
+      const int sh = w - 1 - l0 - j;
+      const uint8_t* cur = j ? smem + (size_t)(j + 1) * T : stage;
+      const uint2 q0 = reinterpret_cast<const uint2*>(cur)[tid];
+      const uint2 q1 = reinterpret_cast<const uint2*>(cur + H)[tid];
+      const uint32_t x[4] = {q0.x, q0.y, q1.x, q1.y};
+      uint32_t b[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) b[k] = (x[k] >> sh) & B1;
-    // this thread's level bits: byte t (first half) and byte T/16 + t (second half)
-    const uint32_t m0 = ((b[0] * 0x01020408u) >> 24) | (((b[1] * 0x01020408u) >> 24) << 4);
-    const uint32_t m1 = ((b[2] * 0x01020408u) >> 24) | (((b[3] * 0x01020408u) >> 24) << 4);
-    const uint32_t ones0 = __popc(m0), ones1 = __popc(m1);
-    if (j == 0) {
-      // level l0 is in global order already: byte stores (32 lanes = 32 consecutive bytes)
-      uint8_t* g8 = reinterpret_cast<uint8_t*>(a.words + (int64_t)l0 * a.nwords) + (base >> 3);
-      const int64_t lim = 8 * a.nwords - (base >> 3);
-      const int f0 = 8 * tid, f1 = H + 8 * tid;
-      if (tid < lim) g8[tid] = (uint8_t)(f0 + 8 <= cnt ? m0 : (f0 >= cnt ? 0u : (m0 & ((1u << (cnt - f0)) - 1u))));
-      if (H / 8 + tid < lim)
-        g8[H / 8 + tid] = (uint8_t)(f1 + 8 <= cnt ? m1 : (f1 >= cnt ? 0u : (m1 & ((1u << (cnt - f1)) - 1u))));
-    } else {
-      bits8[j * 4 * (NC + 4) + tid] = (uint8_t)m0;
-      bits8[j * 4 * (NC + 4) + H / 8 + tid] = (uint8_t)m1;
-    }
-    if (j + 1 == K && !a.has_out) break;
-    // CTA-wide exclusive scans of both halves' ones counts (packed 16|16)
-    const uint32_t pk = ones0 | (ones1 << 16);
-    uint32_t incl = pk;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t t = __shfl_up_sync(FULL, incl, o);
-      if (lane >= o) incl += t;
-    }
-    if (lane == 31) s_wtot[j & 1][wid] = incl;
-    bar_sync(1, U8_THREADS);
-    const uint32_t wv = lane < NW ? s_wtot[j & 1][lane] : 0u;
-    const uint32_t wpre = __reduce_add_sync(FULL, lane < wid ? wv : 0u);
-    const uint32_t tot = __reduce_add_sync(FULL, wv);
-    const uint32_t ex = wpre + incl - pk;
-    const int tot0 = (int)(tot & 0xFFFFu), tot1 = (int)(tot >> 16);
-    const int Z = T - tot0 - tot1;
-    const int opre0 = (int)(ex & 0xFFFFu);
-    const int opre1 = tot0 + (int)(ex >> 16);
-    // ones: OBh + (inclusive rank); zeros: ZBh + symbol index - (inclusive ones)
-    const int OB[2] = {Z + opre0 - 1, Z + opre1 - 1};
-    const int ZB[2] = {8 * tid - opre0, H + 8 * tid - opre1};
-    const bool last = j + 1 == K;
-    bool in_smem = !last;
-    if (last) {
-      bar_sync(2, ALLT);  // placement tables
-      in_smem = tt.q1;
-    }
-    if (in_smem) {
-      // the last split of a uniform tile goes to buffer 0 (free once the
-      // table warp is done) and is then copied out run by run
-      const uint32_t nxt = sbase + (last ? 0u : (uint32_t)(j + 1) * T);
-      // each half sorted in registers (zeros first): byte k goes to the zeros
-      // run (k < nz) or to the ones run, one store per symbol
-#pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
-        const uint32_t sel = s_lut[hh ? m1 : m0];
-        const uint32_t sv[2] = {__byte_perm(x[2 * hh], x[2 * hh + 1], sel & 0xFFFFu),
-                                __byte_perm(x[2 * hh], x[2 * hh + 1], sel >> 16)};
-        const int nz = 8 - (int)(hh ? ones1 : ones0);
-        const uint32_t za = opaque(nxt + (uint32_t)ZB[hh]);
-        const uint32_t oa = opaque(nxt + (uint32_t)(OB[hh] + 1 - nz));
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          const uint32_t addr = (kk < nz ? za : oa) + kk;
-          asm volatile("st.shared.u8 [%0], %1;" ::"r"(addr), "r"(sv[kk >> 2] >> (8 * (kk & 3))) : "memory");
-        }
+      for (int k = 0; k < 4; ++k) b[k] = (x[k] >> sh) & B1;
+      // this thread's level bits: byte t (first half) and byte T/16 + t (second half)
+      const uint32_t m0 = ((b[0] * 0x01020408u) >> 24) | (((b[1] * 0x01020408u) >> 24) << 4);
+      const uint32_t m1 = ((b[2] * 0x01020408u) >> 24) | (((b[3] * 0x01020408u) >> 24) << 4);
+      const uint32_t ones0 = __popc(m0), ones1 = __popc(m1);
+      if (j == 0) {
+        // level l0 is in global order already: byte stores (32 lanes = 32 consecutive bytes)
+        uint8_t* g8 = reinterpret_cast<uint8_t*>(a.words + (int64_t)l0 * a.nwords) + (base >> 3);
+        const int64_t lim = 8 * a.nwords - (base >> 3);
+        const int f0 = 8 * tid, f1 = H + 8 * tid;
+        if (tid < lim) g8[tid] = (uint8_t)(f0 + 8 <= cnt ? m0 : (f0 >= cnt ? 0u : (m0 & ((1u << (cnt - f0)) - 1u))));
+        if (H / 8 + tid < lim)
+          g8[H / 8 + tid] = (uint8_t)(f1 + 8 <= cnt ? m1 : (f1 >= cnt ? 0u : (m1 & ((1u << (cnt - f1)) - 1u))));
+      } else {
+        bits8[j * 4 * (NC + 4) + tid] = (uint8_t)m0;
+        bits8[j * 4 * (NC + 4) + H / 8 + tid] = (uint8_t)m1;
       }
+      if (j + 1 == K && !a.has_out) break;
+      // CTA-wide exclusive scans of both halves' ones counts (packed 16|16)
+      const uint32_t pk = ones0 | (ones1 << 16);
+      uint32_t incl = pk;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += t;
+      }
+      if (lane == 31) s_wtot[j & 1][wid] = incl;
       bar_sync(1, U8_THREADS);
+      const uint32_t wv = lane < NW ? s_wtot[j & 1][lane] : 0u;
+      const uint32_t wpre = __reduce_add_sync(FULL, lane < wid ? wv : 0u);
+      const uint32_t tot = __reduce_add_sync(FULL, wv);
+      const uint32_t ex = wpre + incl - pk;
+      const int tot0 = (int)(tot & 0xFFFFu), tot1 = (int)(tot >> 16);
+      const int Z = T - tot0 - tot1;
+      const int opre0 = (int)(ex & 0xFFFFu);
+      const int opre1 = tot0 + (int)(ex >> 16);
+      // ones: OBh + (inclusive rank); zeros: ZBh + symbol index - (inclusive ones)
+      const int OB[2] = {Z + opre0 - 1, Z + opre1 - 1};
+      const int ZB[2] = {8 * tid - opre0, H + 8 * tid - opre1};
+      const bool last = j + 1 == K;
+      bool in_smem = !last;
       if (last) {
-        copy_out_u8<K>(a, tt, buf, s_ncnt, tid);
+        bar_sync(2, ALLT);  // placement tables
+        in_smem = tt.q1;
+      }
+      if (in_smem) {
+        // the last split of a uniform tile goes to buffer K + 1 and is copied
+        // out run by run
+        const uint32_t nxt = sbase + (uint32_t)(j + 2) * T;
+        // each half sorted in registers (zeros first): byte k goes to the zeros
+        // run (k < nz) or to the ones run, one store per symbol
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          const uint32_t sel = s_lut[hh ? m1 : m0];  // prmt reads selector bits 0-15
+          const uint32_t sv[2] = {prmt(x[2 * hh], x[2 * hh + 1], sel), prmt(x[2 * hh], x[2 * hh + 1], sel >> 16)};
+          const int nz = 8 - (int)(hh ? ones1 : ones0);
+          const uint32_t za = opaque(nxt + (uint32_t)ZB[hh]);
+          const uint32_t oa = opaque(nxt + (uint32_t)(OB[hh] + 1 - nz));
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            const uint32_t addr = (kk < nz ? za : oa) + kk;
+            const uint32_t v = sv[kk >> 2];
+            const uint32_t vb = (kk & 3) == 0 ? v : (kk & 3) == 1 ? shr_mul<8>(v) : (kk & 3) == 2 ? shr_mul<16>(v) : shr_mul<24>(v);
+            asm volatile("st.shared.u8 [%0], %1;" ::"r"(addr), "r"(vb) : "memory");
+          }
+        }
         bar_sync(1, U8_THREADS);
-        const int ncount = 2 * nd << a.nK;
+        if (last) {
+          copy_out_u8<K>(a, tt, smem + (size_t)(K + 1) * T, s_ncnt, tid);
+          bar_sync(1, U8_THREADS);
+          const int ncount = 2 * nd << a.nK;
+          const unsigned nmask = (1u << a.nK) - 1u;
+          for (int q = tid; q < ncount; q += U8_THREADS) {
+            const uint32_t v = s_ncnt[q];
+            if (v) {
+              s_ncnt[q] = 0;
+              const int slot = q >> a.nK, ne = q & (int)nmask;
+              atomicAdd(&a.ncnt[(int64_t)ne * a.nntiles + tt.ft[slot >> 1] + (slot & 1)], v);
+            }
+          }
+        }
+      } else {
+        // last split of a tile spanning several nodes (WT): symbol by symbol to HBM
+        const uint32_t keep = wm ? ((w - l0 - K) >= 32 ? FULL : ((1u << (w - l0 - K)) - 1u)) : FULL;
+        const int eshift = w - l0 - K;
+        const int nshift = w - l0 - K - a.nK;
         const unsigned nmask = (1u << a.nK) - 1u;
-        for (int i = tid; i < ncount; i += U8_THREADS) {
-          const uint32_t v = s_ncnt[i];
-          if (v) {
-            const int slot = i >> a.nK, ne = i & (int)nmask;
-            atomicAdd(&a.ncnt[(int64_t)ne * a.nntiles + tt.ft[slot >> 1] + (slot & 1)], v);
+        uint32_t p[4];  // inclusive ones count through each byte, per half
+        p[0] = b[0] * B1;
+        p[1] = (b[1] + (p[0] >> 24)) * B1;
+        p[2] = b[2] * B1;
+        p[3] = (b[3] + (p[2] >> 24)) * B1;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int r = (int)__byte_perm(p[k], 0, 0x4440 + e);
+            const uint32_t xv = __byte_perm(x[k], 0, 0x4440 + e);
+            const int pos = (b[k] & (0xFFu << (8 * e))) ? OB[k >> 1] + r : ZB[k >> 1] + 4 * (k & 1) + e - r;
+            if (pos < cnt) {
+              const unsigned d = rev_bits((xv >> eshift) & (nd - 1), K);
+              const uint64_t P = (uint64_t)xv >> eshift;
+              const int64_t gpos = a.corr[a.corr_off[K] + P] + tt.lb[K][d] + pos - tt.ls[K][d];
+              reinterpret_cast<uint8_t*>(a.dst)[gpos] = (uint8_t)(xv & keep);
+              atomicAdd(&a.ncnt[(int64_t)((xv >> nshift) & nmask) * a.nntiles + (gpos >> a.ntshift)], 1u);
+            }
           }
         }
+        bar_sync(1, U8_THREADS);
       }
-    } else {
-      // last split of a tile spanning several nodes (WT): symbol by symbol to HBM
-      const uint32_t keep = wm ? ((w - l0 - K) >= 32 ? FULL : ((1u << (w - l0 - K)) - 1u)) : FULL;
-      const int eshift = w - l0 - K;
-      const int nshift = w - l0 - K - a.nK;
-      const unsigned nmask = (1u << a.nK) - 1u;
-      uint32_t p[4];  // inclusive ones count through each byte, per half
-      p[0] = b[0] * B1;
-      p[1] = (b[1] + (p[0] >> 24)) * B1;
-      p[2] = b[2] * B1;
-      p[3] = (b[3] + (p[2] >> 24)) * B1;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int r = (int)__byte_perm(p[k], 0, 0x4440 + i);
-          const uint32_t xv = __byte_perm(x[k], 0, 0x4440 + i);
-          const int pos = (b[k] & (0xFFu << (8 * i))) ? OB[k >> 1] + r : ZB[k >> 1] + 4 * (k & 1) + i - r;
-          if (pos < cnt) {
-            const unsigned d = rev_bits((xv >> eshift) & (nd - 1), K);
-            const uint64_t P = (uint64_t)xv >> eshift;
-            const int64_t gpos = a.corr[a.corr_off[K] + P] + tt.lb[K][d] + pos - tt.ls[K][d];
-            reinterpret_cast<uint8_t*>(a.dst)[gpos] = (uint8_t)(xv & keep);
-            atomicAdd(&a.ncnt[(int64_t)((xv >> nshift) & nmask) * a.nntiles + (gpos >> a.ntshift)], 1u);
-          }
-        }
-      }
-      bar_sync(1, U8_THREADS);
     }
-  }
-  if (!a.has_out) {
+    if (!a.has_out) {
+      bar_sync(1, U8_THREADS);
+      bar_sync(2, ALLT);
+    }
+    if (tt.q1)
+      emit_uniform<uint8_t, K, NC>(a, tt, bits, wid, lane, NW);
+    else
+      emit_multinode<uint8_t, uint8_t, K>(a, tt, smem + T, T, cnt, tid, lane, U8_THREADS);
+    // stage buffers are only read here (no generic writes except for the
+    // final partial tile, after which no bulk copy targets them)
     bar_sync(1, U8_THREADS);
-    bar_sync(2, ALLT);
+    if (tile + G < a.ntiles) bar_arrive(4, ALLT);
   }
-  if (tt.q1)
-    emit_uniform<uint8_t, K, NC>(a, tt, bits, wid, lane, NW);
-  else
-    emit_multinode<uint8_t, uint8_t, K>(a, tt, buf, T, cnt, tid, lane, U8_THREADS);
 }
 
 // ---------------------------------------------------------------------------
@@ -1488,17 +1570,26 @@ cudaError_t launch_pass_k(int K, const PassArgs& a, int64_t ntiles, cudaStream_t
   }
 }
 
+int sm_count();
+
 template <int K>
 cudaError_t launch_pass_u8(const PassArgs& a, int64_t ntiles, cudaStream_t s) {
-  using S = PassSmem<uint8_t, K, 16, U8_THREADS>;
+  using S = U8Smem<K>;
   auto kern = level_pass_u8_kernel<K>;
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::total);
     if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
+    if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  kern<<<(unsigned)ntiles, U8_THREADS + TAB_WARP_THREADS, S::total, s>>>(a);
+  // persistent CTAs: U8_CTAS_PER_SM per SM, tiles strided by the grid
+#ifndef U8_GRID_PER_SM
+#define U8_GRID_PER_SM 0  // 0: one CTA per tile (measured faster than persistent CTAs)
+#endif
+  const int64_t grid = U8_GRID_PER_SM ? std::min<int64_t>(ntiles, (int64_t)sm_count() * U8_GRID_PER_SM) : ntiles;
+  kern<<<(unsigned)grid, U8_THREADS + TAB_WARP_THREADS, S::total, s>>>(a);
   return cudaGetLastError();
 }
 

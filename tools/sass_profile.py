@@ -1,6 +1,6 @@
 """Condense an ncu source page (SASS view) into addr/instr/samples/executed columns.
 
-usage: python tools/sass_profile.py report.ncu-rep [kernel-substring] > out.txt
+usage: python tools/sass_profile.py report.ncu-rep [profiled-kernel-index] > out.txt
 """
 import csv
 import io
@@ -9,11 +9,17 @@ import sys
 
 rep = sys.argv[1]
 cmd = ["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"]
-if len(sys.argv) > 2:
-    cmd += ["-k", sys.argv[2]]
 txt = subprocess.run(cmd, capture_output=True, text=True).stdout
 lines = txt.splitlines()
-rows = list(csv.reader(io.StringIO("\n".join(l for l in lines if not l.startswith('"Kernel Name"')))))
+which = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+blocks, cur = [], None
+for l in lines:
+    if l.startswith('"Kernel Name"'):
+        cur = []
+        blocks.append(cur)
+    elif cur is not None:
+        cur.append(l)
+rows = list(csv.reader(io.StringIO("\n".join(blocks[which]))))
 hdr = rows[0]
 ia = hdr.index("Address"); isrc = hdr.index("Source"); ism = hdr.index("Warp Stall Sampling (All Samples)")
 iex = hdr.index("Instructions Executed"); iwf = hdr.index("L1 Wavefronts Shared"); iwi = hdr.index("L1 Wavefronts Shared Ideal")
