@@ -848,15 +848,15 @@ __device__ __forceinline__ void table_warp(const PassArgs& a, TileTables<TOut, K
       tt.ft[lane] = g >> a.ntshift;
     }
     if (sizeof(TOut) == 1 && a.has_out) {
-      // 16-byte-aligned destination chunks per group, prefix in tile order
+      // whole 16-byte-aligned destination chunks inside each group's run,
+      // prefix in tile order (the partial edge chunks are handled separately)
       __syncwarp();
       int c = 0;
       if (lane < nd) {
         const int n = tt.cnt[K][lane];
-        if (n) {
-          const uintptr_t lo = (uintptr_t)(tt.row[rev_bits((unsigned)lane, K)] + tt.ls[K][lane]);
-          c = (int)(((lo + n - 1) >> 4) - (lo >> 4) + 1);
-        }
+        const uintptr_t lo = (uintptr_t)(tt.row[rev_bits((unsigned)lane, K)] + tt.ls[K][lane]);
+        const intptr_t f = (intptr_t)((lo + n) >> 4) - (intptr_t)((lo + 15) >> 4);
+        c = f > 0 ? (int)f : 0;
       }
       int incl = c;
 #pragma unroll
@@ -1118,16 +1118,18 @@ __global__ void __launch_bounds__(PASS_THREADS + TAB_WARP_THREADS, 2) level_pass
     emit_multinode<TIn, TOut, K>(a, tt, buf, T, cnt, tid, lane, PASS_THREADS);
 }
 
-// Copy-out of a uniform byte tile sorted into `fin` (groups in tile order):
-// work items are the 16-byte-aligned destination chunks of every group's run
-// (TileTables::ipre); a full chunk is read from shared memory at any byte
-// offset (five words, four PRMT) and written with one 16-byte store, edge
-// chunks byte by byte.  Each symbol also counts its next-pass digit per
-// (run, next tile) in s_ncnt.
+// Copy-out of a uniform byte tile sorted into `fin` (groups in tile order).
+// Work items are the whole 16-byte-aligned destination chunks inside every
+// group's run (TileTables::ipre): a chunk is read from shared memory at any
+// byte offset (five words, four PRMT) and written with one 16-byte store.  The
+// partial chunks at both ends of a run (< 16 bytes each) go byte by byte, one
+// warp per group.  Every symbol also counts its next-pass digit per (run, next
+// tile) in s_ncnt.
 template <int K>
 __device__ __forceinline__ void copy_out_u8(const PassArgs& a, const TileTables<uint8_t, K>& tt, const uint8_t* fin,
                                             uint32_t* s_ncnt, int tid) {
   constexpr int nd = 1 << K;
+  static_assert(nd <= U8_THREADS / 32, "one warp per group for the run edges");
   const int nK = a.nK;
   const int nshift = a.width - a.level - K - nK;
   const uint32_t nmask = (1u << nK) - 1u;
@@ -1143,35 +1145,56 @@ __device__ __forceinline__ void copy_out_u8(const PassArgs& a, const TileTables<
       if (tt.ipre[d + s] <= it) d += s;
     const int num = (int)rev_bits((unsigned)d, K);
     uint8_t* row = tt.row[num];
-    const int s0 = tt.ls[K][d], e0 = s0 + tt.cnt[K][d];
-    const uintptr_t D = (((uintptr_t)(row + s0) >> 4) + (uintptr_t)(it - tt.ipre[d])) << 4;
+    const uintptr_t D = ((((uintptr_t)(row + tt.ls[K][d]) + 15) >> 4) + (uintptr_t)(it - tt.ipre[d])) << 4;
     const int p = (int)(D - (uintptr_t)row);  // tile-local position of the chunk's first byte
     const int thr = tt.thr[num];
     const uint32_t cb = (uint32_t)(num << 1) << nK;
-    if (p >= s0 && p + 16 <= e0 && (p >= thr || p + 16 <= thr)) {
-      const uint32_t* q = fw + (p >> 2);
-      const uint32_t sel = 0x3210u + 0x1111u * (uint32_t)(p & 3);
-      const uint32_t w0 = q[0], w1 = q[1], w2 = q[2], w3 = q[3], w4 = q[4];
-      uint32_t v[4] = {__byte_perm(w0, w1, sel), __byte_perm(w1, w2, sel), __byte_perm(w2, w3, sel),
-                       __byte_perm(w3, w4, sel)};
+    const uint32_t* q = fw + (p >> 2);
+    const uint32_t sel = 0x3210u + 0x1111u * (uint32_t)(p & 3);
+    const uint32_t w0 = q[0], w1 = q[1], w2 = q[2], w3 = q[3], w4 = q[4];
+    uint32_t v[4] = {prmt(w0, w1, sel), prmt(w1, w2, sel), prmt(w2, w3, sel), prmt(w3, w4, sel)};
+    if (p >= thr || p + 16 <= thr) {
       uint32_t* cnt = s_ncnt + (cb | (p >= thr ? (1u << nK) : 0u));
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const uint32_t m = (v[k] >> nshift) & nrep;
 #pragma unroll
         for (int i = 0; i < 4; ++i) atomicAdd(cnt + __byte_perm(m, 0, 0x4440 + i), 1u);
-        v[k] &= krep;
       }
-      asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(D), "r"(v[0]), "r"(v[1]), "r"(v[2]),
-                   "r"(v[3]) : "memory");
-    } else {
-      const int lo = p > s0 ? p : s0, hi = p + 16 < e0 ? p + 16 : e0;
-      for (int i = lo; i < hi; ++i) {
-        const uint32_t x = fin[i];
-        row[i] = (uint8_t)(x & keep);
-        atomicAdd(s_ncnt + (cb | (i >= thr ? (1u << nK) : 0u) | ((x >> nshift) & nmask)), 1u);
+    } else {  // the chunk where the run crosses into the next pass's next tile
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t m = (v[k] >> nshift) & nrep;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          atomicAdd(s_ncnt + (cb | (p + 4 * k + i >= thr ? (1u << nK) : 0u) | __byte_perm(m, 0, 0x4440 + i)), 1u);
       }
     }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] &= krep;
+    asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(D), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3])
+                 : "memory");
+  }
+  // run edges: warp d, lanes 0-15 the head bytes, lanes 16-31 the tail bytes
+  const int wid = tid >> 5, lane = tid & 31;
+  if (wid < nd) {
+    const int d = wid;
+    const int n = tt.cnt[K][d];
+    const int num = (int)rev_bits((unsigned)d, K);
+    uint8_t* row = tt.row[num];
+    const int s0 = tt.ls[K][d], e0 = s0 + n;
+    const uintptr_t lo = (uintptr_t)(row + s0), hi = lo + n;
+    const uintptr_t hend = ((lo + 15) & ~(uintptr_t)15) < hi ? ((lo + 15) & ~(uintptr_t)15) : hi;
+    const uintptr_t tbeg = (hi & ~(uintptr_t)15) > hend ? (hi & ~(uintptr_t)15) : hend;
+    const int hlen = (int)(hend - lo), tlen = (int)(hi - tbeg);
+    const int pos = lane < 16 ? s0 + lane : (int)(tbeg - (uintptr_t)row) + (lane - 16);
+    if ((lane < 16 && lane < hlen) || (lane >= 16 && lane - 16 < tlen)) {
+      const uint32_t x = fin[pos];
+      row[pos] = (uint8_t)(x & keep);
+      const uint32_t cb = (uint32_t)(num << 1) << nK;
+      atomicAdd(s_ncnt + (cb | (pos >= tt.thr[num] ? (1u << nK) : 0u) | ((x >> nshift) & nmask)), 1u);
+    }
+    (void)e0;
   }
 }
 
