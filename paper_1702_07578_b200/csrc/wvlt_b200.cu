@@ -192,6 +192,7 @@ __device__ __forceinline__ void bar_arrive(int id, int nthreads) {
 // running totals in registers for the global histogram.
 // ---------------------------------------------------------------------------
 constexpr int HIST_WARPS = 4;
+
 #ifndef WVLT_E_SMALL
 #define WVLT_E_SMALL 16
 #endif
@@ -205,22 +206,20 @@ __global__ void __launch_bounds__(HIST_WARPS * 32) hist_u8_kernel(const uint8_t*
                                                                  uint32_t* __restrict__ tcnt0, int64_t ntiles,
                                                                  int32_t* __restrict__ status) {
   constexpr int NB = 1 << W;
-  constexpr int NPAIR = (NB + 1) / 2;
-  constexpr int WORDS = NPAIR * 32;  // per warp
+  constexpr int HALF = NB / 2;        // counter word p holds bins p (low 16 bits) and p + HALF (high)
+  constexpr int WORDS = HALF * 32;    // per warp
   constexpr int K0 = W < KMAX ? W : KMAX;
-  constexpr int DSH = W - K0;        // pass-0 digit = bin >> DSH
+  constexpr int DSH = W - K0;         // pass-0 digit = bin >> DSH; word p: digits p >> DSH, + ND / 2
   constexpr int ND = 1 << K0;
-  constexpr int FLUSH_TILES = 128;   // 128 * 256 increments per lane counter < 2^16
+  constexpr int FLUSH_TILES = 128;    // a lane adds 256 per tile: < 2^16 between flushes, so
+                                      // low-half sums never carry into the high half
   extern __shared__ __align__(16) uint32_t s_cols[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   uint32_t* c32 = s_cols + (size_t)wid * WORDS;
   for (int i = lane; i < WORDS; i += 32) c32[i] = 0;
   __syncwarp();
-  // byte address of this lane's counter for bin v: ((v >> 1) * 32 + lane) * 4 + (v & 1) * 2
-  //   = 2 v + 124 (v >> 1) + 4 lane
-  unsigned char* cbase = reinterpret_cast<unsigned char*>(c32) + 4 * lane;
-  uint32_t* c32w = c32 + lane;
-  uint32_t prev[ND];  // this lane's column sums per digit at the previous tile (mod 2^16)
+  uint32_t* c32w = c32 + lane;        // counter word p of this lane: c32w[32 p]
+  uint32_t prev[ND];  // this lane's column sums per digit at the previous tile
 #pragma unroll
   for (int d = 0; d < ND; ++d) prev[d] = 0;
   uint32_t bad = 0;
@@ -230,14 +229,14 @@ __global__ void __launch_bounds__(HIST_WARPS * 32) hist_u8_kernel(const uint8_t*
   const int64_t nwarps = (int64_t)gridDim.x * HIST_WARPS;
   int since = 0;
   auto flush = [&]() {
-    // exact bin totals since the last flush: column sums per pair
-    for (int pr = 0; pr < NPAIR; ++pr) {
-      const uint32_t wv = c32[pr * 32 + lane];
+    // exact bin totals since the last flush: column sums per word
+    for (int p = 0; p < HALF; ++p) {
+      const uint32_t wv = c32[p * 32 + lane];
       const uint32_t lo = __reduce_add_sync(FULL, wv & 0xFFFFu);
       const uint32_t hi = __reduce_add_sync(FULL, wv >> 16);
       if (lane == 0) {
-        if (lo) atomicAdd(&hist[2 * pr], (unsigned long long)lo);
-        if (hi && 2 * pr + 1 < NB) atomicAdd(&hist[2 * pr + 1], (unsigned long long)hi);
+        if (lo) atomicAdd(&hist[p], (unsigned long long)lo);
+        if (hi) atomicAdd(&hist[p + HALF], (unsigned long long)hi);
       }
     }
     __syncwarp();
@@ -251,23 +250,29 @@ __global__ void __launch_bounds__(HIST_WARPS * 32) hist_u8_kernel(const uint8_t*
     const int cnt = (int)min((int64_t)TILE_U8, n - first);
     if (cnt == TILE_U8 && aligned) {
       const uint4* v4 = reinterpret_cast<const uint4*>(text + first);
-#pragma unroll 2
-      for (int k0 = 0; k0 < TILE_U8 / 16 / 32; k0 += 4) {
-        uint4 q[4];
+#ifndef HIST_BATCH
+#define HIST_BATCH 8
+#endif
+#pragma unroll 1
+      for (int k0 = 0; k0 < TILE_U8 / 16 / 32; k0 += HIST_BATCH) {
+        uint4 q[HIST_BATCH];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) q[k] = __ldcs(v4 + (k0 + k) * 32 + lane);
+        for (int k = 0; k < HIST_BATCH; ++k) q[k] = __ldcs(v4 + (k0 + k) * 32 + lane);
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < HIST_BATCH; ++k) {
           const uint32_t wd[4] = {q[k].x, q[k].y, q[k].z, q[k].w};
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             if (W < 8) bad |= wd[u] & badmask;
+            // per byte: counter word from the low W-1 bits, increment 1 or
+            // 1 << 16 from bit W-1 (two PRMT, one LEA, one IMAD)
+            const uint32_t lo = wd[u] & ((uint32_t)(HALF - 1) * 0x01010101u);
+            const uint32_t hb = (wd[u] >> (W - 1)) & 0x01010101u;
 #pragma unroll
             for (int b = 0; b < 4; ++b) {
               // fire-and-forget shared atomic on the packed counter word: no
               // load->store dependency chain between consecutive symbols
-              const uint32_t v = __byte_perm(wd[u], 0, 0x4440 + b) & (NB - 1);
-              atomicAdd(c32w + (v >> 1) * 32, 1u + (v & 1u) * 0xFFFFu);
+              atomicAdd(c32w + prmt(lo, 0, 0x4440 + b) * 32, prmt(hb, 0, 0x4440 + b) * 0xFFFFu + 1u);
             }
           }
         }
@@ -275,34 +280,26 @@ __global__ void __launch_bounds__(HIST_WARPS * 32) hist_u8_kernel(const uint8_t*
     } else {
       for (int i = lane; i < cnt; i += 32) {
         const uint32_t v = text[first + i];
-        if (v >> W) {
+        if (v >> W)
           bad = 1;
-        } else {
-          uint16_t* ctr = reinterpret_cast<uint16_t*>(cbase + 2 * v + 124 * (v >> 1));
-          *ctr = (uint16_t)(*ctr + 1);
-        }
+        else
+          c32w[(v & (HALF - 1)) * 32] += (v >> (W - 1)) ? 0x10000u : 1u;
       }
     }
     __syncwarp();
-    // the tile's pass-0 digit counts: each lane sums its own column per digit
-    // (conflict-free), differences to the previous tile, one reduction per digit
-    uint32_t acc[ND];
+    // the tile's pass-0 digit counts: each lane sums its own column (packed:
+    // digit q low, digit q + ND/2 high; conflict-free), differences to the
+    // previous tile, one reduction per digit
+    uint32_t acc[ND / 2];
 #pragma unroll
-    for (int d = 0; d < ND; ++d) acc[d] = 0;
+    for (int q = 0; q < ND / 2; ++q) acc[q] = 0;
 #pragma unroll
-    for (int pr = 0; pr < NPAIR; ++pr) {
-      const uint32_t wv = c32[pr * 32 + lane];
-      if (DSH >= 1) {
-        acc[(2 * pr) >> DSH] += (wv & 0xFFFFu) + (wv >> 16);
-      } else {
-        acc[2 * pr] += wv & 0xFFFFu;
-        if (2 * pr + 1 < NB) acc[2 * pr + 1] += wv >> 16;
-      }
-    }
+    for (int p = 0; p < HALF; ++p) acc[p >> DSH] += c32[p * 32 + lane];
 #pragma unroll
     for (int d = 0; d < ND; ++d) {
-      const uint32_t delta = (acc[d] - prev[d]) & 0xFFFFu;
-      prev[d] = acc[d];
+      const uint32_t cur = d < ND / 2 ? (acc[d] & 0xFFFFu) : (acc[d - ND / 2] >> 16);
+      const uint32_t delta = cur - prev[d];
+      prev[d] = cur;
       const uint32_t c = __reduce_add_sync(FULL, delta);
       if (lane == d) tcnt0[(int64_t)d * ntiles + t] = c;
     }
@@ -1675,8 +1672,8 @@ cudaError_t launch_hist_build(const void* text, int sym_bytes, int64_t n, int w,
   const bool fast = sym_bytes == 1 && w >= 1 && w <= 8 && tile0 == TILE_U8 && (((uintptr_t)text) & 15) == 0;
   if (fast) {
     const uint8_t* t = (const uint8_t*)text;
-    const size_t sb = (size_t)HIST_WARPS * ((((size_t)1 << w) + 1) / 2) * 32 * 4;
-    const int hb = sm_count() * 3;
+    const size_t sb = (size_t)HIST_WARPS * ((size_t)1 << (w - 1)) * 32 * 4;
+    const int hb = sm_count() * (int)std::min<size_t>(8, (size_t)(220 * 1024) / (sb + 1024));
     const int dshift = w - K0;
     const int nd0 = 1 << K0;
 #define WVLT_H8(WW)                                                                                         \
