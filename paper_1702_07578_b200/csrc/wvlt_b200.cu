@@ -1285,7 +1285,7 @@ __global__ void __launch_bounds__(U8_THREADS + TAB_WARP_THREADS, U8_CTAS_PER_SM)
     }
     if (!wm) bar_arrive(3, ALLT);
 
-#pragma unroll 1
+#pragma unroll  // constant j: buffer and scan addresses fold (32 registers at 3 CTAs/SM)
     for (int j = 0; j < K; ++j) {
       const int sh = w - 1 - l0 - j;
       const uint8_t* cur = j ? smem + (size_t)(j + 1) * T : stage;
@@ -1296,8 +1296,13 @@ __global__ void __launch_bounds__(U8_THREADS + TAB_WARP_THREADS, U8_CTAS_PER_SM)
 #pragma unroll
       for (int k = 0; k < 4; ++k) b[k] = (x[k] >> sh) & B1;
       // this thread's level bits: byte t (first half) and byte T/16 + t (second half)
+#ifdef U8_NEW_M
+      const uint32_t m0 = ((b[1] * 16u + b[0]) * 0x01020408u) >> 24;
+      const uint32_t m1 = ((b[3] * 16u + b[2]) * 0x01020408u) >> 24;
+#else
       const uint32_t m0 = ((b[0] * 0x01020408u) >> 24) | (((b[1] * 0x01020408u) >> 24) << 4);
       const uint32_t m1 = ((b[2] * 0x01020408u) >> 24) | (((b[3] * 0x01020408u) >> 24) << 4);
+#endif
       const uint32_t ones0 = __popc(m0), ones1 = __popc(m1);
       if (j == 0) {
         // level l0 is in global order already: byte stores (32 lanes = 32 consecutive bytes)
@@ -1354,10 +1359,18 @@ __global__ void __launch_bounds__(U8_THREADS + TAB_WARP_THREADS, U8_CTAS_PER_SM)
           const uint32_t oa = opaque(nxt + (uint32_t)(OB[hh] + 1 - nz));
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) {
-            const uint32_t addr = (kk < nz ? za : oa) + kk;
             const uint32_t v = sv[kk >> 2];
             const uint32_t vb = (kk & 3) == 0 ? v : (kk & 3) == 1 ? shr_mul<8>(v) : (kk & 3) == 2 ? shr_mul<16>(v) : shr_mul<24>(v);
+#ifdef U8_DUAL_ST
+            // two predicated stores (zeros run / ones run): no address select on the ALU pipe
+            asm volatile(
+                "{\n\t.reg .pred p;\n\tsetp.lt.u32 p, %2, %3;\n\t@p st.shared.u8 [%0], %4;\n\t"
+                "@!p st.shared.u8 [%1], %4;\n\t}" ::"r"(za + kk), "r"(oa + kk), "r"(kk), "r"(nz), "r"(vb)
+                : "memory");
+#else
+            const uint32_t addr = (kk < nz ? za : oa) + kk;
             asm volatile("st.shared.u8 [%0], %1;" ::"r"(addr), "r"(vb) : "memory");
+#endif
           }
         }
         bar_sync(1, U8_THREADS);
