@@ -56,6 +56,14 @@ constexpr int PASS_THREADS = 512;
 #ifndef U8_THREADS
 #define U8_THREADS 512  // compute threads of the byte pass kernel (tile = 16 per thread)
 #endif
+#ifndef U8_FINAL_BUF
+// 1: the last split goes to its own buffer (required with persistent CTAs: stage
+// buffers then only ever receive bulk copies); 0: back into the stage buffer
+#define U8_FINAL_BUF 1
+#endif
+#ifndef U8_TABLE_WARP
+#define U8_TABLE_WARP 1  // 1: a 17th warp builds the tile tables concurrently; 0: the last compute warp does
+#endif
 constexpr int MAXP = 32;            // passes per build (width <= 24 => <= 6 at K = 4)
 constexpr unsigned FULL = 0xffffffffu;
 
@@ -817,7 +825,7 @@ __device__ __forceinline__ void table_warp(const PassArgs& a, TileTables<TOut, K
   bool q1 = true;
   int64_t q = 0;
   if (!wm) {
-    bar_sync(3, allt);  // tile staged
+    if (allt > 0) bar_sync(3, allt);  // tile staged (inline callers have staged it)
     const int sh = w - l0;
     const uint64_t qf = sh >= 32 ? 0 : ((uint64_t)(uint32_t)buf0[0] >> sh);
     const uint64_t ql = sh >= 32 ? 0 : ((uint64_t)(uint32_t)buf0[cnt - 1] >> sh);
@@ -865,8 +873,10 @@ __device__ __forceinline__ void table_warp(const PassArgs& a, TileTables<TOut, K
       if (lane == nd - 1) tt.ipre[nd] = incl;
     }
   }
-  __threadfence_block();
-  bar_arrive(2, allt);
+  if (allt > 0) {
+    __threadfence_block();
+    bar_arrive(2, allt);
+  }
 }
 
 // Levels l0+1 .. l0+K-1 of a uniform tile: one warp per (level j, run r),
@@ -1211,19 +1221,21 @@ struct U8Smem {
   // two staging buffers (tile i in stage i % 2, the next tile prefetched into
   // the other) + the orders of levels l+1 .. l+K-1
   // + one buffer for the last split (so stage buffers only ever receive bulk copies)
-  static constexpr size_t buf_bytes = (size_t)(K + 2) * T;
+  static constexpr size_t buf_bytes = (size_t)(K + 1 + U8_FINAL_BUF) * T;
   static constexpr size_t bits_bytes = PassSmem<uint8_t, K, 16, U8_THREADS>::bits_bytes;
   static constexpr size_t total = buf_bytes + bits_bytes;
 };
 
+constexpr int U8_TABW = U8_TABLE_WARP ? TAB_WARP_THREADS : 0;
+
 template <int K>
-__global__ void __launch_bounds__(U8_THREADS + TAB_WARP_THREADS, U8_CTAS_PER_SM) level_pass_u8_kernel(const PassArgs a) {
+__global__ void __launch_bounds__(U8_THREADS + U8_TABW, U8_CTAS_PER_SM) level_pass_u8_kernel(const PassArgs a) {
   using S = U8Smem<K>;
   constexpr int T = S::T;
   constexpr int H = T / 2;
   constexpr int NC = T / 32;
   constexpr int NW = U8_THREADS / 32;
-  constexpr int ALLT = U8_THREADS + TAB_WARP_THREADS;
+  constexpr int ALLT = U8_THREADS + U8_TABW;
   constexpr int nd = 1 << K;
   constexpr uint32_t B1 = 0x01010101u;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -1242,7 +1254,7 @@ __global__ void __launch_bounds__(U8_THREADS + TAB_WARP_THREADS, U8_CTAS_PER_SM)
   const uint8_t* text = reinterpret_cast<const uint8_t*>(a.src);
   const bool bulk_ok = (((uintptr_t)text) & 15) == 0;  // full tiles are then 16-byte aligned
 
-  if (wid == NW) {  // table warp: one tile after the other, in step with the compute warps
+  if (U8_TABLE_WARP && wid == NW) {  // table warp: one tile after the other, in step with the compute warps
     int i = 0;
     for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += G, ++i) {
       if (i) bar_sync(4, ALLT);  // previous tile's tables consumed
@@ -1283,7 +1295,12 @@ __global__ void __launch_bounds__(U8_THREADS + TAB_WARP_THREADS, U8_CTAS_PER_SM)
       for (int p = tid; p < T; p += U8_THREADS) stage[p] = p < cnt ? text[base + p] : (uint8_t)0xFF;
       bar_sync(1, U8_THREADS);
     }
-    if (!wm) bar_arrive(3, ALLT);
+    if (U8_TABLE_WARP) {
+      if (!wm) bar_arrive(3, ALLT);
+    } else if (wid == NW - 1) {
+      // tables by the last compute warp (visible to all after the next CTA barrier)
+      table_warp<uint8_t, uint8_t, K>(a, tt, stage, tile, cnt, lane, 0);
+    }
 
 #pragma unroll  // constant j: buffer and scan addresses fold (32 registers at 3 CTAs/SM)
     for (int j = 0; j < K; ++j) {
@@ -1341,13 +1358,13 @@ __global__ void __launch_bounds__(U8_THREADS + TAB_WARP_THREADS, U8_CTAS_PER_SM)
       const bool last = j + 1 == K;
       bool in_smem = !last;
       if (last) {
-        bar_sync(2, ALLT);  // placement tables
+        if (U8_TABLE_WARP) bar_sync(2, ALLT);  // placement tables
         in_smem = tt.q1;
       }
       if (in_smem) {
         // the last split of a uniform tile goes to buffer K + 1 and is copied
         // out run by run
-        const uint32_t nxt = sbase + (uint32_t)(j + 2) * T;
+        const uint32_t nxt = sbase + (uint32_t)(last && !U8_FINAL_BUF ? st : j + 2) * T;
         // each half sorted in registers (zeros first): byte k goes to the zeros
         // run (k < nz) or to the ones run, one store per symbol
 #pragma unroll
@@ -1375,7 +1392,7 @@ __global__ void __launch_bounds__(U8_THREADS + TAB_WARP_THREADS, U8_CTAS_PER_SM)
         }
         bar_sync(1, U8_THREADS);
         if (last) {
-          copy_out_u8<K>(a, tt, smem + (size_t)(K + 1) * T, s_ncnt, tid);
+          copy_out_u8<K>(a, tt, U8_FINAL_BUF ? smem + (size_t)(K + 1) * T : stage, s_ncnt, tid);
           bar_sync(1, U8_THREADS);
           const int ncount = 2 * nd << a.nK;
           const unsigned nmask = (1u << a.nK) - 1u;
@@ -1420,7 +1437,7 @@ __global__ void __launch_bounds__(U8_THREADS + TAB_WARP_THREADS, U8_CTAS_PER_SM)
     }
     if (!a.has_out) {
       bar_sync(1, U8_THREADS);
-      bar_sync(2, ALLT);
+      if (U8_TABLE_WARP) bar_sync(2, ALLT);
     }
     if (tt.q1)
       emit_uniform<uint8_t, K, NC>(a, tt, bits, wid, lane, NW);
@@ -1429,7 +1446,7 @@ __global__ void __launch_bounds__(U8_THREADS + TAB_WARP_THREADS, U8_CTAS_PER_SM)
     // stage buffers are only read here (no generic writes except for the
     // final partial tile, after which no bulk copy targets them)
     bar_sync(1, U8_THREADS);
-    if (tile + G < a.ntiles) bar_arrive(4, ALLT);
+    if (U8_TABLE_WARP && tile + G < a.ntiles) bar_arrive(4, ALLT);
   }
 }
 
@@ -1622,7 +1639,7 @@ cudaError_t launch_pass_u8(const PassArgs& a, int64_t ntiles, cudaStream_t s) {
 #define U8_GRID_PER_SM 0  // 0: one CTA per tile (measured faster than persistent CTAs)
 #endif
   const int64_t grid = U8_GRID_PER_SM ? std::min<int64_t>(ntiles, (int64_t)sm_count() * U8_GRID_PER_SM) : ntiles;
-  kern<<<(unsigned)grid, U8_THREADS + TAB_WARP_THREADS, S::total, s>>>(a);
+  kern<<<(unsigned)grid, U8_THREADS + U8_TABW, S::total, s>>>(a);
   return cudaGetLastError();
 }
 
