@@ -89,6 +89,9 @@ int wvlt_histogram(const void* text, int sym_bytes, int64_t n, int64_t sigma, in
  *   status       device int32 or NULL; set to 0 then WVLT_STATUS_RANGE on a bad symbol
  * When status reports a bad symbol the level words are unspecified (the caller
  * raises, like construct._validated, construct.py:183-187).
+ * A WM build with hist == NULL and borders == NULL computes no histogram at all:
+ * its per-level tables and zero counts come from the tile digit counts of each
+ * pass (the output is identical).
  */
 int wvlt_build_device(const void* text, int sym_bytes, int64_t n, int64_t sigma, int kind,
                       uint64_t* level_words, int64_t* zeros, int64_t* hist, int64_t* borders,
@@ -100,7 +103,7 @@ int wvlt_build_device(const void* text, int sym_bytes, int64_t n, int64_t sigma,
  * `stream`.  Device buffers are caller-provided (dev_text: n*sym_bytes bytes,
  * dev_level_words: width*ceil(n/64)*8 bytes, dev_small: (2^width + width + 1)*8 bytes).
  * Host buffers should be page-locked for full copy bandwidth.  host_zeros and
- * host_hist may be NULL.  Returns WVLT_E_RANGE when a symbol is out of range.
+ * host_hist may be NULL (host_hist == NULL selects the histogram-free WM build).  Returns WVLT_E_RANGE when a symbol is out of range.
  * This is the call a reference-side binding (ctypes / cgo / JNI) would make
  * in place of construct.build_structure (construct.py:150-164).
  */

@@ -202,7 +202,8 @@ def _build(text, sigma: int, kind: str, threads: int = 1):
 
     dev_arr = _device_text(arr, sigma)
     _note_device_build(n, dev_arr.dtype.itemsize, sigma, kind)
-    words, zeros, hist = default_builder().build_host(dev_arr, sigma, kind)
+    # the WT build computes the histogram anyway (its placement tables need it)
+    words, zeros, hist = default_builder().build_host(dev_arr, sigma, kind, histogram=kind == "wt")
     st = wrap(kind, n, sigma, words, zeros)
     st.histogram = hist
     return st

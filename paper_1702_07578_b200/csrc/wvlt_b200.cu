@@ -403,6 +403,117 @@ __global__ void __launch_bounds__(256) digits_kernel(const void* __restrict__ te
   }
 }
 
+// K1 of a lean WM build (no histogram requested): pass-0 tile digit counts and
+// the range check only -- the WM placement tables need nothing finer than each
+// pass's digit totals, which the tile scans provide.  One warp per tile,
+// lane-private 32-bit counter columns (fire-and-forget atomics, no overflow).
+template <typename TIn>
+__global__ void __launch_bounds__(256) digits_fast_kernel(const TIn* __restrict__ text, int64_t n, int tile, int dshift,
+                                                          int nd0, int64_t ntiles, uint32_t vmax_ok,
+                                                          uint32_t* __restrict__ tcnt0, int32_t* __restrict__ status) {
+  constexpr int PER = 16 / sizeof(TIn);  // symbols per 16-byte load
+  __shared__ uint32_t s_c[8][NDIG * 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint32_t* c = s_c[wid];
+  for (int i = lane; i < NDIG * 32; i += 32) c[i] = 0;
+  __syncwarp();
+  uint32_t* cl = c + lane;
+  const uint32_t dmask = (uint32_t)nd0 - 1u;
+  uint32_t prev[NDIG];
+#pragma unroll
+  for (int d = 0; d < NDIG; ++d) prev[d] = 0;
+  uint32_t vmax = 0;
+  const bool aligned = (((uintptr_t)text) & 15) == 0;
+  const int64_t gw = (int64_t)blockIdx.x * 8 + wid;
+  const int64_t nwarps = (int64_t)gridDim.x * 8;
+  for (int64_t t = gw; t < ntiles; t += nwarps) {
+    const int64_t first = t * tile;
+    const int cnt = (int)min((int64_t)tile, n - first);
+    if (cnt == tile && aligned) {
+      const uint4* v4 = reinterpret_cast<const uint4*>(text + first);
+      const int nq = tile / PER;
+#pragma unroll 4
+      for (int k = lane; k < nq; k += 32) {
+        const uint4 q = __ldcs(v4 + k);
+        const uint32_t wd[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (sizeof(TIn) == 1) {
+            vmax = __vmaxu4(vmax, wd[u]);
+            const uint32_t dg = (wd[u] >> dshift) & (dmask * 0x01010101u);
+#pragma unroll
+            for (int b = 0; b < 4; ++b) atomicAdd(cl + prmt(dg, 0, 0x4440 + b) * 32, 1u);
+          } else if (sizeof(TIn) == 2) {
+            vmax = __vmaxu2(vmax, wd[u]);
+            atomicAdd(cl + (((wd[u] & 0xFFFFu) >> dshift) & dmask) * 32, 1u);
+            atomicAdd(cl + ((wd[u] >> (16 + dshift)) & dmask) * 32, 1u);
+          } else {
+            vmax = max(vmax, wd[u]);
+            atomicAdd(cl + ((dshift >= 32 ? 0u : (wd[u] >> dshift)) & dmask) * 32, 1u);
+          }
+        }
+      }
+    } else {
+      for (int i = lane; i < cnt; i += 32) {
+        const uint32_t v = (uint32_t)text[first + i];
+        vmax = max(vmax, v);
+        atomicAdd(cl + ((dshift >= 32 ? 0u : (v >> dshift)) & dmask) * 32, 1u);
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int d = 0; d < NDIG; ++d) {
+      if (d < nd0) {
+        const uint32_t cur = cl[d * 32];
+        const uint32_t tot = __reduce_add_sync(FULL, cur - prev[d]);
+        prev[d] = cur;
+        if (lane == d) tcnt0[(int64_t)d * ntiles + t] = tot;
+      }
+    }
+  }
+  // SIMD maxima hold per-lane maxima of byte / halfword lanes: fold them
+  if (sizeof(TIn) == 1) vmax = max(max(vmax & 0xFFu, (vmax >> 8) & 0xFFu), max((vmax >> 16) & 0xFFu, vmax >> 24));
+  if (sizeof(TIn) == 2) vmax = max(vmax & 0xFFFFu, vmax >> 16);
+  if (vmax > vmax_ok) atomicOr(status, WVLT_STATUS_RANGE);
+}
+
+// Per-pass WM tables from the pass's digit totals (lean builds): the G table
+// of every level of the pass (as tables_kernel step 5) and its zero counts.
+__global__ void wm_pass_tables_kernel(const uint32_t* __restrict__ tcnt, const int64_t* __restrict__ tpre,
+                                      int64_t ntiles, int K, int l0, int64_t* __restrict__ wm_base,
+                                      int64_t* __restrict__ zeros) {
+  __shared__ int64_t s_tot[NDIG];  // by LSD digit d = rev(numeric e)
+  const int lane = threadIdx.x;
+  const int nd = 1 << K;
+  if (lane < nd) {
+    const int64_t i = (int64_t)lane * ntiles + ntiles - 1;
+    s_tot[rev_bits((unsigned)lane, K)] = tpre[i] + (int64_t)tcnt[i];
+  }
+  __syncwarp();
+  if (lane == 0) {
+    for (int j = 1; j <= K; ++j) {
+      const int mj = 1 << j;
+      int64_t run = 0;
+      for (int d = 0; d < mj; ++d) {
+        int64_t cj = 0;
+        for (int e = d; e < nd; e += mj) cj += s_tot[e];
+        wm_base[j * NDIG + d] = run;
+        run += cj;
+      }
+    }
+    if (zeros) {
+      // level l0 + j: symbols whose (j+1)-th digit bit from the top is 0, i.e.
+      // LSD digit d with bit j clear
+      for (int j = 0; j < K; ++j) {
+        int64_t z = 0;
+        for (int d = 0; d < nd; ++d)
+          if (!((d >> j) & 1)) z += s_tot[d];
+        zeros[l0 + j] = z;
+      }
+    }
+  }
+}
+
 // Widen symbols stored narrower than the code width (e.g. uint8 storage with
 // sigma > 256) so the all-ones tail sentinel of the pass kernel covers every
 // code bit.
@@ -555,8 +666,10 @@ __global__ void __launch_bounds__(TAB_THREADS) tables_kernel(const TablesArgs a)
     s = block_sum_i64(s, s_red);
     if (tid == 0 && a.zeros_out) a.zeros_out[l] = s;
   }
-  // 4. node borders: WT in numeric prefix order, WM in bit-reversed order
+  // 4. node borders: WT in numeric prefix order (also the WT placement tables'
+  // input), WM in bit-reversed order (only when requested)
   for (int k = 0; k <= w; ++k) {
+    if (P.kind == WVLT_KIND_WM && !a.borders_out) break;
     const int64_t* c = a.chain + chain_off(k);
     int64_t* ws = a.wtstart + chain_off(k);
     block_scan_excl(
@@ -583,21 +696,10 @@ __global__ void __launch_bounds__(TAB_THREADS) tables_kernel(const TablesArgs a)
       const int64_t* c = a.chain + chain_off(l + K);
       const int64_t tot = 1ll << (l + K);
       const int nd = 1 << K;
-      int64_t acc[NDIG];
-#pragma unroll
-      for (int d = 0; d < NDIG; ++d) acc[d] = 0;
-      for (int64_t i = tid; i < tot; i += blockDim.x) {
-        const unsigned e = (unsigned)(i & (nd - 1));  // numeric digit (MSB first)
-        const unsigned d = rev_bits(e, K);
-#pragma unroll
-        for (int dd = 0; dd < NDIG; ++dd)
-          if (dd == (int)d) acc[dd] += c[i];
-      }
-#pragma unroll
-      for (int d = 0; d < NDIG; ++d) {
-        const int64_t s = warp_sum(acc[d]);
-        if ((tid & 31) == 0 && s) atomicAdd(&s_dig[d], (unsigned long long)s);
-      }
+      // blockDim.x is a multiple of nd: thread tid only ever sees numeric digit tid % nd
+      int64_t acc = 0;
+      for (int64_t i = tid; i < tot; i += blockDim.x) acc += c[i];
+      if (acc) atomicAdd(&s_dig[rev_bits((unsigned)(tid & (nd - 1)), K)], (unsigned long long)acc);
       __syncthreads();
       if (tid == 0) {
         int64_t* g = a.wm_base + (int64_t)p * (KMAX + 1) * NDIG;
@@ -1735,6 +1837,24 @@ cudaError_t launch_hist_build(const void* text, int sym_bytes, int64_t n, int w,
   return cudaGetLastError();
 }
 
+// K1 of a lean WM build: pass-0 tile digit counts + range check.
+cudaError_t launch_digits_fast(const void* text, int sym_bytes, int64_t n, int w, int64_t sigma, int K0, int tile0,
+                               int64_t ntiles0, uint32_t* tcnt0, int32_t* status, cudaStream_t s) {
+  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((ntiles0 + 7) / 8, (int64_t)sm_count() * 8));
+  const uint32_t vmax_ok = (uint32_t)std::min<int64_t>(sigma - 1, 0xFFFFFFFFll);
+  const int dshift = w - K0;
+  if (sym_bytes == 1)
+    digits_fast_kernel<uint8_t><<<blocks, 256, 0, s>>>((const uint8_t*)text, n, tile0, dshift, 1 << K0, ntiles0,
+                                                         vmax_ok, tcnt0, status);
+  else if (sym_bytes == 2)
+    digits_fast_kernel<uint16_t><<<blocks, 256, 0, s>>>((const uint16_t*)text, n, tile0, dshift, 1 << K0, ntiles0,
+                                                          vmax_ok, tcnt0, status);
+  else
+    digits_fast_kernel<uint32_t><<<blocks, 256, 0, s>>>((const uint32_t*)text, n, tile0, dshift, 1 << K0, ntiles0,
+                                                          vmax_ok, tcnt0, status);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_scan(const uint32_t* cnt, int K, int64_t ntiles, int64_t* bsum, int64_t* pre, cudaStream_t s) {
   const int64_t nblk = (ntiles + SCAN_TILE - 1) / SCAN_TILE;
   dim3 g((unsigned)nblk, 1u << K);
@@ -1886,9 +2006,14 @@ int wvlt_build_device(const void* text, int sym_bytes, int64_t n, int64_t sigma,
   if (e != cudaSuccess) return (int)e;
   e = cudaMemsetAsync(ws + P.off_tcnt[0], 0, P.tcnt_bytes, s);
   if (e != cudaSuccess) return (int)e;
+  // lean WM build: no histogram / borders requested -> no K1 histogram and no
+  // K2 tables; each pass's tables come from its own tile-count scan
+  const bool lean = kind == WVLT_KIND_WM && !hist && !borders;
   unsigned long long* hw = (unsigned long long*)(chain + chain_off(w));
-  e = cudaMemsetAsync(hw, 0, ((size_t)1 << w) * 8, s);
-  if (e != cudaSuccess) return (int)e;
+  if (!lean) {
+    e = cudaMemsetAsync(hw, 0, ((size_t)1 << w) * 8, s);
+    if (e != cudaSuccess) return (int)e;
+  }
   if (!status) {
     e = cudaMemsetAsync(st_flag, 0, 4, s);
     if (e != cudaSuccess) return (int)e;
@@ -1905,8 +2030,13 @@ int wvlt_build_device(const void* text, int sym_bytes, int64_t n, int64_t sigma,
     src0 = wide;
   }
   prof_mark(s, WVLT_STAGE_MEMSET);
-  e = launch_hist_build(src0, P.in_bytes[0], n, w, P.K[0], P.tile[0], P.ntiles[0], hw,
-                        (uint32_t*)(ws + P.off_tcnt[0]), st_flag, s);
+  if (lean) {
+    e = launch_digits_fast(src0, P.in_bytes[0], n, w, sigma, P.K[0], P.tile[0], P.ntiles[0],
+                           (uint32_t*)(ws + P.off_tcnt[0]), st_flag, s);
+  } else {
+    e = launch_hist_build(src0, P.in_bytes[0], n, w, P.K[0], P.tile[0], P.ntiles[0], hw,
+                          (uint32_t*)(ws + P.off_tcnt[0]), st_flag, s);
+  }
   if (e != cudaSuccess) return (int)e;
   prof_mark(s, WVLT_STAGE_HIST);
 
@@ -1924,9 +2054,11 @@ int wvlt_build_device(const void* text, int sym_bytes, int64_t n, int64_t sigma,
   ta.hist_out = hist;
   ta.borders_out = (w >= 2) ? borders : nullptr;
   ta.status = st_flag;
-  tables_kernel<<<1, TAB_THREADS, 0, s>>>(ta);
-  e = cudaGetLastError();
-  if (e != cudaSuccess) return (int)e;
+  if (!lean) {
+    tables_kernel<<<1, TAB_THREADS, 0, s>>>(ta);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return (int)e;
+  }
   prof_mark(s, WVLT_STAGE_TABLES);
 
   const void* cur = src0;
@@ -1935,6 +2067,12 @@ int wvlt_build_device(const void* text, int sym_bytes, int64_t n, int64_t sigma,
     int64_t* tpre = (int64_t*)(ws + P.off_tpre[p]);
     e = launch_scan(tcnt, P.K[p], P.ntiles[p], bsum, tpre, s);
     if (e != cudaSuccess) return (int)e;
+    if (lean) {
+      wm_pass_tables_kernel<<<1, 32, 0, s>>>(tcnt, tpre, P.ntiles[p], P.K[p], P.lvl[p],
+                                             wm_base + (int64_t)p * (KMAX + 1) * NDIG, zeros);
+      e = cudaGetLastError();
+      if (e != cudaSuccess) return (int)e;
+    }
     prof_mark(s, WVLT_STAGE_SCAN0 + p);
     PassArgs pa;
     memset(&pa, 0, sizeof(pa));
@@ -1986,8 +2124,8 @@ int wvlt_build_host(const void* host_text, int sym_bytes, int64_t n, int64_t sig
     e = cudaMemcpyAsync(dev_text, host_text, (size_t)n * sym_bytes, cudaMemcpyHostToDevice, s);
     if (e != cudaSuccess) return (int)e;
   }
-  int rc = wvlt_build_device(dev_text, sym_bytes, n, sigma, kind, dev_level_words, dzeros, dhist, nullptr, workspace,
-                             workspace_bytes, dstatus, s);
+  int rc = wvlt_build_device(dev_text, sym_bytes, n, sigma, kind, dev_level_words, dzeros, host_hist ? dhist : nullptr,
+                             nullptr, workspace, workspace_bytes, dstatus, s);
   if (rc) return rc;
   const int64_t nwords = (n + 63) >> 6;
   if (w > 0 && nwords > 0) {

@@ -56,7 +56,7 @@ class DeviceBuild:
         """(level_words uint64 ndarray, zeros list, hist ndarray) after a device->host copy."""
         lw = self.level_words.cpu().numpy().view(np.uint64)
         zeros = [int(z) for z in self.zeros.cpu().tolist()] if self.width else []
-        return lw, zeros, self.hist.cpu().numpy()
+        return lw, zeros, (self.hist.cpu().numpy() if self.hist is not None else None)
 
 
 class DeviceBuilder:
@@ -92,12 +92,15 @@ class DeviceBuilder:
         return lw, zeros, hist, bd, status
 
     # -- builds --------------------------------------------------------------
-    def build(self, text, sigma: int, kind: str = "wm", *, borders: bool = False, outputs=None,
-              stream=None, check: bool = True) -> DeviceBuild:
+    def build(self, text, sigma: int, kind: str = "wm", *, borders: bool = False, histogram: bool = False,
+              outputs=None, stream=None, check: bool = True) -> DeviceBuild:
         """Build from a device tensor of uint8/uint16/uint32 symbols in [0, sigma).
 
         ``outputs`` may pass preallocated (level_words, zeros, hist, borders, status)
         from ``alloc_outputs`` (the benchmark does, to time the build alone).
+        ``histogram`` also returns the symbol histogram; a WM build without
+        histogram or borders skips the histogram kernel altogether (its tables
+        come from the per-pass tile counts).
         With ``check`` the range status is read back (one device->host sync) and
         a bad symbol raises ValueError like construct._validated (construct.py:183-187).
         """
@@ -127,19 +130,21 @@ class DeviceBuilder:
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
         rc = self.lib.wvlt_build_device(
             text.data_ptr() if n else None, sb, n, sigma, _lib.KINDS[kind],
-            lw.data_ptr() if lw.numel() else None, zeros.data_ptr() if w else None, hist.data_ptr(),
+            lw.data_ptr() if lw.numel() else None, zeros.data_ptr() if w else None,
+            hist.data_ptr() if histogram else None,
             bd.data_ptr() if bd is not None else None, ws.data_ptr(), need, status.data_ptr(), s.cuda_stream)
         _lib.check(rc)
         if check and int(status.item()) & _lib.STATUS_RANGE:
             raise ValueError(f"symbols must lie in [0, {sigma})")
-        return DeviceBuild(kind, n, sigma, w, lw, zeros, hist, bd, status)
+        return DeviceBuild(kind, n, sigma, w, lw, zeros, hist if histogram else None, bd, status)
 
     def build_host(self, arr: np.ndarray, sigma: int, kind: str, *, out_words: np.ndarray | None = None,
-                   stream=None):
+                   histogram: bool = False, stream=None):
         """Host buffers in and out through wvlt_build_host (H2D, build, D2H, sync).
 
         ``arr`` is a contiguous uint8/uint16/uint32 host array (page-locked for
-        full PCIe bandwidth).  Returns (level_words uint64[w, ceil(n/64)], zeros, hist).
+        full PCIe bandwidth).  Returns (level_words uint64[w, ceil(n/64)], zeros,
+        hist or None).
         """
         torch = _torch()
         if arr.dtype not in (np.uint8, np.uint16, np.uint32) or not arr.flags.c_contiguous:
@@ -159,12 +164,13 @@ class DeviceBuilder:
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
         rc = self.lib.wvlt_build_host(
             arr.ctypes.data if n else None, sb, n, sigma, _lib.KINDS[kind],
-            out_words.ctypes.data if out_words.size else None, zeros.ctypes.data, hist.ctypes.data,
+            out_words.ctypes.data if out_words.size else None, zeros.ctypes.data,
+            hist.ctypes.data if histogram else None,
             dev_text.data_ptr(), dev_words.data_ptr(), dev_small.data_ptr(), ws.data_ptr(), need, s.cuda_stream)
         if rc == _lib.E_RANGE:
             raise ValueError(f"symbols must lie in [0, {sigma})")
         _lib.check(rc)
-        return out_words, [int(z) for z in zeros[:w]], hist
+        return out_words, [int(z) for z in zeros[:w]], (hist if histogram else None)
 
     def merge_bits(self, dst_words, word_lo: int, word_hi: int, n_bits: int, bounds, src_starts, src_words,
                    stream=None, dst_offset_words: int = 0) -> None:

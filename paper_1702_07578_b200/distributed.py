@@ -262,7 +262,7 @@ class CudaOps:
 
             text = torch.from_numpy(_device_text(np.ascontiguousarray(np.asarray(text)), sigma))
         text = text.to(self.device)
-        res = self.builder.build(text, sigma, kind, check=False)
+        res = self.builder.build(text, sigma, kind, histogram=True, check=False)
         bad = bool(int(res.status.item()) & 1) if res.status is not None else False
         return res.level_words, res.hist, bad
 

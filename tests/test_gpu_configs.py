@@ -99,11 +99,17 @@ def test_config_full_size_properties(config, kind):
     torch.cuda.empty_cache()
     text = workloads.generate(config)
     b = DeviceBuilder()
+    # histogram-free build (the WM default), checked against a build that also
+    # returns the histogram: identical levels and zero counts
     res = b.build(text, sigma, kind)
     width = res.width
     levels = res.level_words
+    full = b.build(text, sigma, kind, histogram=True)
+    assert torch.equal(full.level_words, levels)
+    assert torch.equal(full.zeros, res.zeros)
     # zero counts vs the histogram (and vs rank0 of each level)
-    hist = res.hist.cpu().numpy()
+    hist = full.hist.cpu().numpy()
+    del full
     h = hist.copy()
     exp_zeros = []
     for l in range(width - 1, -1, -1):

@@ -122,11 +122,15 @@ def test_histogram_zeros_and_borders_vs_oracle(rng):
         hist = oracle.histogram(text, sigma)
         w = wv.code_width(sigma)
         for kind in ("wt", "wm"):
-            res = b.build(t, sigma, kind, borders=True)
+            res = b.build(t, sigma, kind, borders=True, histogram=True)
             words, zeros, h = res.to_host()
             assert np.array_equal(h, hist)
             _, ozeros, _ = oracle.build(text, sigma, "wm", "pc")
             assert zeros == ozeros
+            # histogram-free build (WM default): same words and zero counts
+            lw, lz, lh = b.build(t, sigma, kind).to_host()
+            assert lh is None
+            assert np.array_equal(lw, words) and lz == zeros
             if w >= 2:
                 assert np.array_equal(res.borders.cpu().numpy()[: (1 << w) - 2], oracle.borders(hist, w, kind))
 
