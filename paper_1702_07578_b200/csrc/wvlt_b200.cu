@@ -161,6 +161,28 @@ __device__ __forceinline__ uint32_t shr_mul(uint32_t v) {
   return d;
 }
 
+// Inclusive warp scan (sum): shfl.up's in-range predicate guards the add, two
+// instructions per step.
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v) {
+#ifdef U8_PLAIN_SCAN
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(FULL, v, o);
+    if ((threadIdx.x & 31) >= o) v += t;
+  }
+  return v;
+#else
+  asm("{\n\t.reg .u32 t;\n\t.reg .pred p;\n\t"
+      "shfl.sync.up.b32 t|p, %0, 1, 0, -1;\n\t@p add.u32 %0, %0, t;\n\t"
+      "shfl.sync.up.b32 t|p, %0, 2, 0, -1;\n\t@p add.u32 %0, %0, t;\n\t"
+      "shfl.sync.up.b32 t|p, %0, 4, 0, -1;\n\t@p add.u32 %0, %0, t;\n\t"
+      "shfl.sync.up.b32 t|p, %0, 8, 0, -1;\n\t@p add.u32 %0, %0, t;\n\t"
+      "shfl.sync.up.b32 t|p, %0, 16, 0, -1;\n\t@p add.u32 %0, %0, t;\n\t}"
+      : "+r"(v));
+  return v;
+#endif
+}
+
 // mbarrier + bulk async copy (global -> shared), completion by transaction bytes
 __device__ __forceinline__ void mbar_init(uint32_t mbar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(mbar), "r"(count) : "memory");
@@ -1438,12 +1460,7 @@ __global__ void __launch_bounds__(U8_THREADS + U8_TABW, U8_CTAS_PER_SM) level_pa
       if (j + 1 == K && !a.has_out) break;
       // CTA-wide exclusive scans of both halves' ones counts (packed 16|16)
       const uint32_t pk = ones0 | (ones1 << 16);
-      uint32_t incl = pk;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t t = __shfl_up_sync(FULL, incl, o);
-        if (lane >= o) incl += t;
-      }
+      const uint32_t incl = warp_incl_scan(pk);
       if (lane == 31) s_wtot[j & 1][wid] = incl;
       bar_sync(1, U8_THREADS);
       const uint32_t wv = lane < NW ? s_wtot[j & 1][lane] : 0u;
