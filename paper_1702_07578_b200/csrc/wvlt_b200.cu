@@ -1441,8 +1441,9 @@ __global__ void __launch_bounds__(U8_THREADS + U8_TABW, U8_CTAS_PER_SM) level_pa
       const uint32_t m0 = ((b[1] * 16u + b[0]) * 0x01020408u) >> 24;
       const uint32_t m1 = ((b[3] * 16u + b[2]) * 0x01020408u) >> 24;
 #else
-      const uint32_t m0 = ((b[0] * 0x01020408u) >> 24) | (((b[1] * 0x01020408u) >> 24) << 4);
-      const uint32_t m1 = ((b[2] * 0x01020408u) >> 24) | (((b[3] * 0x01020408u) >> 24) << 4);
+      // one multiply gathers a half's 8 flags (bits at 8i and 8i + 4 -> 24 + i, 28 + i)
+      const uint32_t m0 = ((b[1] * 16u + b[0]) * 0x01020408u) >> 24;
+      const uint32_t m1 = ((b[3] * 16u + b[2]) * 0x01020408u) >> 24;
 #endif
       const uint32_t ones0 = __popc(m0), ones1 = __popc(m1);
       if (j == 0) {
