@@ -1498,16 +1498,10 @@ __global__ void __launch_bounds__(U8_THREADS + U8_TABW, U8_CTAS_PER_SM) level_pa
           for (int kk = 0; kk < 8; ++kk) {
             const uint32_t v = sv[kk >> 2];
             const uint32_t vb = (kk & 3) == 0 ? v : (kk & 3) == 1 ? shr_mul<8>(v) : (kk & 3) == 2 ? shr_mul<16>(v) : shr_mul<24>(v);
-#ifdef U8_DUAL_ST
-            // two predicated stores (zeros run / ones run): no address select on the ALU pipe
-            asm volatile(
-                "{\n\t.reg .pred p;\n\tsetp.lt.u32 p, %2, %3;\n\t@p st.shared.u8 [%0], %4;\n\t"
-                "@!p st.shared.u8 [%1], %4;\n\t}" ::"r"(za + kk), "r"(oa + kk), "r"(kk), "r"(nz), "r"(vb)
-                : "memory");
-#else
+            // (measured: predicated dual stores and a flag-table IMAD address are
+            // both slower than this compare + select)
             const uint32_t addr = (kk < nz ? za : oa) + kk;
             asm volatile("st.shared.u8 [%0], %1;" ::"r"(addr), "r"(vb) : "memory");
-#endif
           }
         }
         bar_sync(1, U8_THREADS);
