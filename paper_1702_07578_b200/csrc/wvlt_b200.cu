@@ -429,7 +429,7 @@ __global__ void __launch_bounds__(256) digits_kernel(const void* __restrict__ te
 // the range check only -- the WM placement tables need nothing finer than each
 // pass's digit totals, which the tile scans provide.  One warp per tile,
 // lane-private 32-bit counter columns (fire-and-forget atomics, no overflow).
-template <typename TIn>
+template <typename TIn, bool CHECK>
 __global__ void __launch_bounds__(256) digits_fast_kernel(const TIn* __restrict__ text, int64_t n, int tile, int dshift,
                                                           int nd0, int64_t ntiles, uint32_t vmax_ok,
                                                           uint32_t* __restrict__ tcnt0, int32_t* __restrict__ status) {
@@ -461,16 +461,16 @@ __global__ void __launch_bounds__(256) digits_fast_kernel(const TIn* __restrict_
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           if (sizeof(TIn) == 1) {
-            vmax = __vmaxu4(vmax, wd[u]);
+            if (CHECK) vmax = __vmaxu4(vmax, wd[u]);
             const uint32_t dg = (wd[u] >> dshift) & (dmask * 0x01010101u);
 #pragma unroll
             for (int b = 0; b < 4; ++b) atomicAdd(cl + prmt(dg, 0, 0x4440 + b) * 32, 1u);
           } else if (sizeof(TIn) == 2) {
-            vmax = __vmaxu2(vmax, wd[u]);
+            if (CHECK) vmax = __vmaxu2(vmax, wd[u]);
             atomicAdd(cl + (((wd[u] & 0xFFFFu) >> dshift) & dmask) * 32, 1u);
             atomicAdd(cl + ((wd[u] >> (16 + dshift)) & dmask) * 32, 1u);
           } else {
-            vmax = max(vmax, wd[u]);
+            if (CHECK) vmax = max(vmax, wd[u]);
             atomicAdd(cl + ((dshift >= 32 ? 0u : (wd[u] >> dshift)) & dmask) * 32, 1u);
           }
         }
@@ -496,7 +496,7 @@ __global__ void __launch_bounds__(256) digits_fast_kernel(const TIn* __restrict_
   // SIMD maxima hold per-lane maxima of byte / halfword lanes: fold them
   if (sizeof(TIn) == 1) vmax = max(max(vmax & 0xFFu, (vmax >> 8) & 0xFFu), max((vmax >> 16) & 0xFFu, vmax >> 24));
   if (sizeof(TIn) == 2) vmax = max(vmax & 0xFFFFu, vmax >> 16);
-  if (vmax > vmax_ok) atomicOr(status, WVLT_STATUS_RANGE);
+  if (CHECK && vmax > vmax_ok) atomicOr(status, WVLT_STATUS_RANGE);
 }
 
 // Per-pass WM tables from the pass's digit totals (lean builds): the G table
@@ -1855,15 +1855,21 @@ cudaError_t launch_digits_fast(const void* text, int sym_bytes, int64_t n, int w
   const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((ntiles0 + 7) / 8, (int64_t)sm_count() * 8));
   const uint32_t vmax_ok = (uint32_t)std::min<int64_t>(sigma - 1, 0xFFFFFFFFll);
   const int dshift = w - K0;
-  if (sym_bytes == 1)
-    digits_fast_kernel<uint8_t><<<blocks, 256, 0, s>>>((const uint8_t*)text, n, tile0, dshift, 1 << K0, ntiles0,
-                                                         vmax_ok, tcnt0, status);
-  else if (sym_bytes == 2)
-    digits_fast_kernel<uint16_t><<<blocks, 256, 0, s>>>((const uint16_t*)text, n, tile0, dshift, 1 << K0, ntiles0,
-                                                          vmax_ok, tcnt0, status);
-  else
-    digits_fast_kernel<uint32_t><<<blocks, 256, 0, s>>>((const uint32_t*)text, n, tile0, dshift, 1 << K0, ntiles0,
-                                                          vmax_ok, tcnt0, status);
+  // every stored value is in range when sigma covers the whole storage type
+  const bool check = sym_bytes == 4 ? vmax_ok < 0xFFFFFFFFu : vmax_ok < (1u << (8 * sym_bytes)) - 1u;
+#define WVLT_DG(T)                                                                                           \
+  do {                                                                                                       \
+    if (check)                                                                                               \
+      digits_fast_kernel<T, true><<<blocks, 256, 0, s>>>((const T*)text, n, tile0, dshift, 1 << K0, ntiles0, \
+                                                         vmax_ok, tcnt0, status);                            \
+    else                                                                                                     \
+      digits_fast_kernel<T, false><<<blocks, 256, 0, s>>>((const T*)text, n, tile0, dshift, 1 << K0,         \
+                                                          ntiles0, vmax_ok, tcnt0, status);                  \
+  } while (0)
+  if (sym_bytes == 1) WVLT_DG(uint8_t);
+  else if (sym_bytes == 2) WVLT_DG(uint16_t);
+  else WVLT_DG(uint32_t);
+#undef WVLT_DG
   return cudaGetLastError();
 }
 

@@ -20,7 +20,7 @@ out.mkdir(exist_ok=True)
 
 
 def short(name):
-    for k in ("hist_u8_kernel", "hist_generic_kernel", "digits_kernel", "tables_kernel", "scan_reduce_kernel",
+    for k in ("hist_u8_kernel", "hist_generic_kernel", "digits_fast_kernel", "digits_kernel", "wm_pass_tables_kernel", "tables_kernel", "scan_reduce_kernel",
               "scan_apply_kernel", "level_pass_u8_kernel", "level_pass_kernel", "merge_bits_kernel", "widen_kernel"):
         i = name.find(k)
         if i >= 0:
@@ -95,7 +95,7 @@ for r in full:
     if "level_pass" in name:
         traffic[f"pass{pass_idx}"] = (rd + wr) * 1e6
         pass_idx += 1
-    elif "hist" in name:
+    elif "hist" in name or "digits" in name:
         traffic["hist"] = (rd + wr) * 1e6
 (out / f"{tag}_summary.md").write_text("\n".join(lines) + "\n")
 json.dump(traffic, open(out / "ncu_traffic_c2_wm.json", "w"), indent=1)
