@@ -112,6 +112,9 @@ int wvlt_build_host(const void* host_text, int sym_bytes, int64_t n, int64_t sig
                     void* dev_text, uint64_t* dev_level_words, void* dev_small,
                     void* workspace, size_t workspace_bytes, void* stream);
 
+/* Number of this library's kernels the calling thread's last build launched. */
+int wvlt_last_launches(void);
+
 /*
  * Stream ordered bit intervals into whole destination words: destination bit
  * range [bounds[t], bounds[t+1]) receives source bits starting at src_starts[t],

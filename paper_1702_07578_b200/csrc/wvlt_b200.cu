@@ -1881,6 +1881,9 @@ cudaError_t launch_scan(const uint32_t* cnt, int K, int64_t ntiles, int64_t* bsu
   return cudaGetLastError();
 }
 
+// kernels launched by the calling thread's last build (bench evidence)
+thread_local int g_launches = 0;
+
 // optional per-stage CUDA-event timing of wvlt_build_device (bench / profiling)
 constexpr int PROF_MAX = 3 + 2 * MAXP + 1;
 struct Prof {
@@ -1905,6 +1908,12 @@ void prof_mark(cudaStream_t s, int stage_id) {
 }
 
 }  // namespace
+
+namespace {
+int build_device_impl(const void* text, int sym_bytes, int64_t n, int64_t sigma, int kind, uint64_t* level_words,
+                      int64_t* zeros, int64_t* hist, int64_t* borders, void* workspace, size_t workspace_bytes,
+                      int32_t* status, void* stream, void (*pass_done)(void*, int, int), void* ctx);
+}
 
 // ---------------------------------------------------------------------------
 // C ABI
@@ -1971,6 +1980,18 @@ int wvlt_histogram(const void* text, int sym_bytes, int64_t n, int64_t sigma, in
 int wvlt_build_device(const void* text, int sym_bytes, int64_t n, int64_t sigma, int kind, uint64_t* level_words,
                       int64_t* zeros, int64_t* hist, int64_t* borders, void* workspace, size_t workspace_bytes,
                       int32_t* status, void* stream) {
+  return build_device_impl(text, sym_bytes, n, sigma, kind, level_words, zeros, hist, borders, workspace,
+                           workspace_bytes, status, stream, nullptr, nullptr);
+}
+}  // extern "C"
+
+namespace {
+// The build; `pass_done(ctx, l0, K)` (optional) is called right after pass
+// l0..l0+K-1 is enqueued, when those levels' words are final on `stream`.
+int build_device_impl(const void* text, int sym_bytes, int64_t n, int64_t sigma, int kind, uint64_t* level_words,
+                      int64_t* zeros, int64_t* hist, int64_t* borders, void* workspace, size_t workspace_bytes,
+                      int32_t* status, void* stream, void (*pass_done)(void*, int, int), void* ctx) {
+  g_launches = 0;
   if (!(sym_bytes == 1 || sym_bytes == 2 || sym_bytes == 4) || n < 0 || sigma < 1) return WVLT_E_ARG;
   if (kind != WVLT_KIND_WT && kind != WVLT_KIND_WM) return WVLT_E_ARG;
   Plan P;
@@ -2038,6 +2059,7 @@ int wvlt_build_device(const void* text, int sym_bytes, int64_t n, int64_t sigma,
   }
   const void* src0 = text;
   if (P.widen_bytes) {
+    ++g_launches;
     void* wide = ws + P.off_wide;
     const int blocks = sm_count() * 8;
     if (P.widen_bytes == 2) widen_kernel<uint8_t, uint16_t><<<blocks, 256, 0, s>>>((const uint8_t*)text, (uint16_t*)wide, n);
@@ -2048,6 +2070,7 @@ int wvlt_build_device(const void* text, int sym_bytes, int64_t n, int64_t sigma,
     src0 = wide;
   }
   prof_mark(s, WVLT_STAGE_MEMSET);
+  g_launches += lean ? 1 : (P.in_bytes[0] == 1 && w <= 8 && P.tile[0] == TILE_U8 && (((uintptr_t)src0) & 15) == 0 ? 1 : 2);
   if (lean) {
     e = launch_digits_fast(src0, P.in_bytes[0], n, w, sigma, P.K[0], P.tile[0], P.ntiles[0],
                            (uint32_t*)(ws + P.off_tcnt[0]), st_flag, s);
@@ -2074,6 +2097,7 @@ int wvlt_build_device(const void* text, int sym_bytes, int64_t n, int64_t sigma,
   ta.status = st_flag;
   if (!lean) {
     tables_kernel<<<1, TAB_THREADS, 0, s>>>(ta);
+    ++g_launches;
     e = cudaGetLastError();
     if (e != cudaSuccess) return (int)e;
   }
@@ -2084,8 +2108,10 @@ int wvlt_build_device(const void* text, int sym_bytes, int64_t n, int64_t sigma,
     uint32_t* tcnt = (uint32_t*)(ws + P.off_tcnt[p]);
     int64_t* tpre = (int64_t*)(ws + P.off_tpre[p]);
     e = launch_scan(tcnt, P.K[p], P.ntiles[p], bsum, tpre, s);
+    g_launches += 2;
     if (e != cudaSuccess) return (int)e;
     if (lean) {
+      ++g_launches;
       wm_pass_tables_kernel<<<1, 32, 0, s>>>(tcnt, tpre, P.ntiles[p], P.K[p], P.lvl[p],
                                              wm_base + (int64_t)p * (KMAX + 1) * NDIG, zeros);
       e = cudaGetLastError();
@@ -2116,12 +2142,40 @@ int wvlt_build_device(const void* text, int sym_bytes, int64_t n, int64_t sigma,
     pa.corr = corr;
     for (int j = 0; j <= KMAX; ++j) pa.corr_off[j] = P.corr_off[p][j];
     e = launch_pass(P.in_bytes[p], P.out_bytes[p], P.K[p], pa, P.ntiles[p], s);
+    ++g_launches;
     if (e != cudaSuccess) return (int)e;
     prof_mark(s, WVLT_STAGE_PASS0 + p);
+    if (pass_done) pass_done(ctx, P.lvl[p], P.K[p]);
     cur = pa.dst;
   }
   return 0;
 }
+
+// wvlt_build_host: the level words of a finished pass go device->host on a copy
+// stream while the next pass runs.
+struct HostCopy {
+  cudaStream_t main, copy;
+  cudaEvent_t ev[MAXP];
+  int nev;
+  uint64_t* host;
+  const uint64_t* dev;
+  int64_t nwords;
+  cudaError_t err;
+};
+
+void host_copy_pass(void* c, int l0, int K) {
+  HostCopy& h = *(HostCopy*)c;
+  if (h.err != cudaSuccess || h.nev >= MAXP || h.nwords == 0) return;
+  cudaEvent_t e = h.ev[h.nev++];
+  h.err = cudaEventRecord(e, h.main);
+  if (h.err == cudaSuccess) h.err = cudaStreamWaitEvent(h.copy, e, 0);
+  if (h.err == cudaSuccess)
+    h.err = cudaMemcpyAsync(h.host + (int64_t)l0 * h.nwords, h.dev + (int64_t)l0 * h.nwords, (size_t)K * h.nwords * 8,
+                            cudaMemcpyDeviceToHost, h.copy);
+}
+}  // namespace
+
+extern "C" {
 
 int wvlt_build_host(const void* host_text, int sym_bytes, int64_t n, int64_t sigma, int kind,
                     uint64_t* host_level_words, int64_t* host_zeros, int64_t* host_hist, void* dev_text,
@@ -2142,12 +2196,36 @@ int wvlt_build_host(const void* host_text, int sym_bytes, int64_t n, int64_t sig
     e = cudaMemcpyAsync(dev_text, host_text, (size_t)n * sym_bytes, cudaMemcpyHostToDevice, s);
     if (e != cudaSuccess) return (int)e;
   }
-  int rc = wvlt_build_device(dev_text, sym_bytes, n, sigma, kind, dev_level_words, dzeros, host_hist ? dhist : nullptr,
-                             nullptr, workspace, workspace_bytes, dstatus, s);
-  if (rc) return rc;
   const int64_t nwords = (n + 63) >> 6;
-  if (w > 0 && nwords > 0) {
-    if (!host_level_words) return WVLT_E_ARG;
+  if (w > 0 && nwords > 0 && !host_level_words) return WVLT_E_ARG;
+  // level words of each finished pass stream back while the next pass runs
+  static thread_local cudaStream_t copy_stream = nullptr;
+  static thread_local cudaEvent_t evs[MAXP];
+  if (!copy_stream) {
+    e = cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return (int)e;
+    for (int i = 0; i < MAXP; ++i) {
+      e = cudaEventCreateWithFlags(&evs[i], cudaEventDisableTiming);
+      if (e != cudaSuccess) return (int)e;
+    }
+  }
+  HostCopy hc;
+  hc.main = s;
+  hc.copy = copy_stream;
+  for (int i = 0; i < MAXP; ++i) hc.ev[i] = evs[i];
+  hc.nev = 0;
+  hc.host = host_level_words;
+  hc.dev = dev_level_words;
+  hc.nwords = (w > 0) ? nwords : 0;
+  hc.err = cudaSuccess;
+  int rc = build_device_impl(dev_text, sym_bytes, n, sigma, kind, dev_level_words, dzeros, host_hist ? dhist : nullptr,
+                             nullptr, workspace, workspace_bytes, dstatus, s, host_copy_pass, &hc);
+  if (rc) {
+    cudaStreamSynchronize(copy_stream);
+    return rc;
+  }
+  if (hc.err != cudaSuccess) return (int)hc.err;
+  if (w > 0 && nwords > 0 && hc.nev == 0) {  // degenerate shapes: no passes ran
     e = cudaMemcpyAsync(host_level_words, dev_level_words, (size_t)w * nwords * 8, cudaMemcpyDeviceToHost, s);
     if (e != cudaSuccess) return (int)e;
   }
@@ -2164,8 +2242,12 @@ int wvlt_build_host(const void* host_text, int sym_bytes, int64_t n, int64_t sig
   }
   e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) return (int)e;
+  e = cudaStreamSynchronize(copy_stream);
+  if (e != cudaSuccess) return (int)e;
   return (hstatus & WVLT_STATUS_RANGE) ? WVLT_E_RANGE : 0;
 }
+
+int wvlt_last_launches(void) { return g_launches; }
 
 int wvlt_merge_bits(uint64_t* dst_words, int64_t word_lo, int64_t word_hi, int64_t n_bits, const int64_t* bounds,
                     const int64_t* src_starts, int64_t ntasks, const uint64_t* src_words, void* stream) {
