@@ -129,6 +129,42 @@ int wvlt_merge_bits(uint64_t* dst_words, int64_t word_lo, int64_t word_hi, int64
                     const uint64_t* src_words, void* stream);
 
 /*
+ * Rank/select directories of nvec bit vectors of `length` bits stored back to
+ * back (ceil(length/64) words each, the level layout above).  Replaces
+ * RankSelectBitVector._build (bitvec.py:135-163), same arrays per vector:
+ *   super_zeros  int64[nvec][ceil(length/2048)]  zeros before each 2048-bit superblock
+ *   block_zeros  int64[nvec][ceil(length/256)]   zeros before each 256-bit block, relative
+ *                                                to its superblock
+ *   samples1/0   int64[nvec][ceil(length/8192)]  position of the (8192k+1)-th one / zero;
+ *                                                the first ceil(count/8192) entries are valid
+ *   ones         int64[nvec]                     ones per vector
+ * workspace: >= wvlt_rank_select_workspace_bytes(nvec, length) bytes.
+ */
+size_t wvlt_rank_select_workspace_bytes(int64_t nvec, int64_t length);
+int wvlt_rank_select_build(const uint64_t* words, int64_t nvec, int64_t length, int64_t* super_zeros,
+                           int64_t* block_zeros, int64_t* samples1, int64_t* samples0, int64_t* ones,
+                           void* workspace, size_t workspace_bytes, void* stream);
+
+/* query operations of wvlt_query */
+#define WVLT_Q_ACCESS 0 /* out[q] = symbol at position arg[q] */
+#define WVLT_Q_RANK 1   /* out[q] = occurrences of symbol c in [0, arg[q]) */
+#define WVLT_Q_SELECT 2 /* out[q] = position of the arg[q]-th (1-based) c, or -1 when absent */
+#define WVLT_Q_BITRANK 3 /* out[q] = ones of level c in bit positions [0, arg[q]) (0 <= c < width) */
+
+/*
+ * Batched queries on a built structure with its level directories (one
+ * thread per query): access / rank / select of LevelWiseWaveletTree and
+ * WaveletMatrix (structures.py:107-256).  The symbol c of query q is sym[q],
+ * or sym_scalar when sym is NULL.  Arguments must be in range (access:
+ * 0 <= i < n; rank: 0 <= i <= n, 0 <= c < 2^width; select: j >= 1) -- the
+ * caller validates, as the reference's _check_* helpers do.
+ */
+int wvlt_query(int kind, int op, const uint64_t* level_words, int64_t n, int width, const int64_t* zeros,
+               const int64_t* super_zeros, const int64_t* block_zeros, const int64_t* samples1,
+               const int64_t* samples0, const int64_t* ones, const int64_t* sym, int64_t sym_scalar,
+               const int64_t* arg, int64_t* out, int64_t count, void* stream);
+
+/*
  * Optional per-stage timing (CUDA events on the build stream) of the calling
  * thread's wvlt_build_device calls.  Stage ids: WVLT_STAGE_MEMSET (output and
  * look-back reset), WVLT_STAGE_HIST (K1), WVLT_STAGE_TABLES (K2),

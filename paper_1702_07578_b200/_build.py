@@ -21,6 +21,7 @@ LIB_NAME = "_wvlt_b200.so"
 LIB_PATH = PKG_DIR / LIB_NAME
 
 SOURCES = [CSRC / "wvlt_b200.cu"]
+INCLUDED = [CSRC / "support.cuh"]  # #included by wvlt_b200.cu
 HEADERS = [INCLUDE / "wvlt_b200.h"]
 
 NVCC_FLAGS = [
@@ -44,7 +45,7 @@ def is_stale() -> bool:
     if not LIB_PATH.exists():
         return True
     built = LIB_PATH.stat().st_mtime
-    return any(src.stat().st_mtime > built for src in SOURCES + HEADERS)
+    return any(src.stat().st_mtime > built for src in SOURCES + INCLUDED + HEADERS)
 
 
 def build(force: bool = False, verbose: bool = False) -> Path:

@@ -59,6 +59,12 @@ def load():
     L.wvlt_merge_bits.restype = i32
     L.wvlt_last_launches.argtypes = []
     L.wvlt_last_launches.restype = i32
+    L.wvlt_rank_select_workspace_bytes.argtypes = [i64, i64]
+    L.wvlt_rank_select_workspace_bytes.restype = sz
+    L.wvlt_rank_select_build.argtypes = [vp, i64, i64, vp, vp, vp, vp, vp, vp, sz, vp]
+    L.wvlt_rank_select_build.restype = i32
+    L.wvlt_query.argtypes = [i32, i32, vp, i64, i32, vp, vp, vp, vp, vp, vp, vp, i64, vp, vp, i64, vp]
+    L.wvlt_query.restype = i32
     L.wvlt_profile_enable.argtypes = [i32]
     L.wvlt_profile_enable.restype = i32
     L.wvlt_profile_read.argtypes = [vp, vp, i32]

@@ -2264,3 +2264,5 @@ int wvlt_merge_bits(uint64_t* dst_words, int64_t word_lo, int64_t word_hi, int64
 }
 
 }  // extern "C"
+
+#include "support.cuh"

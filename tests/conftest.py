@@ -59,3 +59,12 @@ def golden_cases():
 @pytest.fixture
 def rng():
     return np.random.default_rng(0x574C54)
+
+
+GOLDEN_NEXT_PATH = ROOT / "tests" / "golden" / "golden_next.npz"
+
+
+@lru_cache(maxsize=1)
+def golden_next():
+    """Reference outputs of the §8f consumers (tests/golden/make_golden_next.py)."""
+    return dict(np.load(GOLDEN_NEXT_PATH, allow_pickle=False))
