@@ -49,32 +49,46 @@ __device__ __forceinline__ int select_in_word64(uint64_t word, int k) {
   return pos;
 }
 
-// Pass 1: one warp per superblock (lane = word): word popcounts, block zeros
-// relative to the superblock, superblock one counts.
+// Pass 1: one warp per RS_SB_PER_WARP superblocks (lane = word, all loads in
+// flight first): word popcounts, block zeros relative to the superblock,
+// superblock one counts.
+constexpr int RS_SB_PER_WARP = 4;
 __global__ void __launch_bounds__(RS_WARPS * 32) rs_blocks_kernel(const uint64_t* __restrict__ words, int64_t length,
                                                                  int64_t* __restrict__ block_zeros,
                                                                  uint32_t* __restrict__ sup_ones) {
   const RsShape sh = rs_shape(length);
   const int v = blockIdx.y;
   const int lane = threadIdx.x & 31;
-  const int64_t sb = (int64_t)blockIdx.x * RS_WARPS + (threadIdx.x >> 5);
-  if (sb >= sh.nsuper) return;
-  const int64_t w = sb * RS_SB_WORDS + lane;
-  const uint64_t word = w < sh.nwords ? words[(int64_t)v * sh.nwords + w] : 0ull;
-  const uint32_t pc = (uint32_t)__popcll(word);
-  const uint32_t incl = warp_incl_scan(pc);
-  const uint32_t excl = incl - pc;
-  if ((lane & 3) == 0) {
-    const int64_t b = sb * RS_BLK_PER_SB + (lane >> 2);
-    if (b < sh.nblocks) block_zeros[(int64_t)v * sh.nblocks + b] = (int64_t)(lane >> 2) * RS_BLK_BITS - (int64_t)excl;
+  const int64_t sb0 = ((int64_t)blockIdx.x * RS_WARPS + (threadIdx.x >> 5)) * RS_SB_PER_WARP;
+  if (sb0 >= sh.nsuper) return;
+  uint64_t word[RS_SB_PER_WARP];
+#pragma unroll
+  for (int u = 0; u < RS_SB_PER_WARP; ++u) {
+    const int64_t w = (sb0 + u) * RS_SB_WORDS + lane;
+    word[u] = w < sh.nwords ? __ldcs(reinterpret_cast<const unsigned long long*>(words) + (int64_t)v * sh.nwords + w)
+                            : 0ull;
   }
-  if (lane == 31) sup_ones[(int64_t)v * sh.nsuper + sb] = incl;
+#pragma unroll
+  for (int u = 0; u < RS_SB_PER_WARP; ++u) {
+    const int64_t sb = sb0 + u;
+    if (sb >= sh.nsuper) break;
+    const uint32_t pc = (uint32_t)__popcll(word[u]);
+    const uint32_t incl = warp_incl_scan(pc);
+    const uint32_t excl = incl - pc;
+    if ((lane & 3) == 0) {
+      const int64_t b = sb * RS_BLK_PER_SB + (lane >> 2);
+      if (b < sh.nblocks)
+        block_zeros[(int64_t)v * sh.nblocks + b] = (int64_t)(lane >> 2) * RS_BLK_BITS - (int64_t)excl;
+    }
+    if (lane == 31) sup_ones[(int64_t)v * sh.nsuper + sb] = incl;
+  }
 }
 
 // Pass 2 (after the scan of superblock one counts into `super_zeros`): turn
 // the exclusive one prefixes into zero prefixes, record the select samples
-// falling into this superblock (at most one per bit value: 2048 < 8192), and
-// the vector's one total.
+// (at most one per bit value per superblock: 2048 < 8192) and the vector's one
+// total.  A warp takes 32 superblocks, one per lane; only the superblocks that
+// hold a sample are revisited word by word, cooperatively.
 __global__ void __launch_bounds__(RS_WARPS * 32) rs_samples_kernel(const uint64_t* __restrict__ words, int64_t length,
                                                                   const uint32_t* __restrict__ sup_ones,
                                                                   int64_t* __restrict__ super_zeros,
@@ -84,34 +98,51 @@ __global__ void __launch_bounds__(RS_WARPS * 32) rs_samples_kernel(const uint64_
   const RsShape sh = rs_shape(length);
   const int v = blockIdx.y;
   const int lane = threadIdx.x & 31;
-  const int64_t sb = (int64_t)blockIdx.x * RS_WARPS + (threadIdx.x >> 5);
-  if (sb >= sh.nsuper) return;
-  const int64_t cum1 = super_zeros[(int64_t)v * sh.nsuper + sb];  // ones before sb (scan output)
-  const uint32_t ones = sup_ones[(int64_t)v * sh.nsuper + sb];
-  const int64_t sb_bits = min((int64_t)RS_SB_BITS, length - sb * RS_SB_BITS);
-  __syncwarp();
-  if (lane == 0) {
+  const int64_t sb0 = ((int64_t)blockIdx.x * RS_WARPS + (threadIdx.x >> 5)) * 32;
+  if (sb0 >= sh.nsuper) return;
+  const int64_t sb = sb0 + lane;
+  const bool in = sb < sh.nsuper;
+  int64_t cum1 = 0;
+  uint32_t ones = 0;
+  if (in) {
+    cum1 = super_zeros[(int64_t)v * sh.nsuper + sb];  // ones before sb (scan output)
+    ones = sup_ones[(int64_t)v * sh.nsuper + sb];
     super_zeros[(int64_t)v * sh.nsuper + sb] = sb * RS_SB_BITS - cum1;
     if (sb == sh.nsuper - 1) ones_out[v] = cum1 + ones;
   }
-  const int64_t w = sb * RS_SB_WORDS + lane;
-  const uint64_t word = w < sh.nwords ? words[(int64_t)v * sh.nwords + w] : 0ull;
-  const int64_t wbits = min((int64_t)64, max((int64_t)0, length - w * 64));
-  const uint64_t valid = wbits >= 64 ? ~0ull : ((1ull << wbits) - 1ull);
+  const int64_t sb_bits = in ? min((int64_t)RS_SB_BITS, length - sb * RS_SB_BITS) : 0;
+  // does a sample (ordinal 8192 k + 1) of ones / zeros fall into this superblock?
+  int64_t kx[2];
+  int needx[2];
+  bool has[2];
 #pragma unroll
-  for (int x = 1; x >= 0; --x) {
+  for (int x = 0; x < 2; ++x) {
     const int64_t before = x ? cum1 : sb * RS_SB_BITS - cum1;
     const int64_t inside = x ? (int64_t)ones : sb_bits - (int64_t)ones;
-    const int64_t k = (before + RS_SAMPLE - 1) / RS_SAMPLE;  // first sample ordinal S k + 1 > before
-    if (inside <= 0 || k * RS_SAMPLE > before + inside - 1) continue;
-    const int need = (int)(k * RS_SAMPLE - before + 1);  // 1-based inside the superblock
-    const uint64_t wx = x ? word : (~word & valid);
-    const uint32_t pc = (uint32_t)__popcll(wx);
-    const uint32_t incl = warp_incl_scan(pc);
-    const uint32_t excl = incl - pc;
-    if ((int)excl < need && need <= (int)incl) {
-      const int64_t pos = w * 64 + select_in_word64(wx, need - (int)excl);
-      (x ? samples1 : samples0)[(int64_t)v * sh.nsamp + k] = pos;
+    kx[x] = (before + RS_SAMPLE - 1) / RS_SAMPLE;
+    has[x] = in && inside > 0 && kx[x] * RS_SAMPLE <= before + inside - 1;
+    needx[x] = has[x] ? (int)(kx[x] * RS_SAMPLE - before + 1) : 0;
+  }
+#pragma unroll
+  for (int x = 0; x < 2; ++x) {
+    uint32_t todo = __ballot_sync(FULL, has[x]);
+    while (todo) {
+      const int src = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const int64_t s = sb0 + src;
+      const int need = __shfl_sync(FULL, needx[x], src);
+      const int64_t k = __shfl_sync(FULL, kx[x], src);
+      const int64_t w = s * RS_SB_WORDS + lane;
+      uint64_t word = w < sh.nwords ? words[(int64_t)v * sh.nwords + w] : 0ull;
+      if (!x) {
+        const int64_t wbits = min((int64_t)64, max((int64_t)0, length - w * 64));
+        word = ~word & (wbits >= 64 ? ~0ull : ((1ull << wbits) - 1ull));
+      }
+      const uint32_t pc = (uint32_t)__popcll(word);
+      const uint32_t incl = warp_incl_scan(pc);
+      const uint32_t excl = incl - pc;
+      if ((int)excl < need && need <= (int)incl)
+        (x ? samples1 : samples0)[(int64_t)v * sh.nsamp + k] = w * 64 + select_in_word64(word, need - (int)excl);
     }
   }
 }
@@ -369,13 +400,15 @@ int wvlt_rank_select_build(const uint64_t* words, int64_t nvec, int64_t length, 
   const RsShape sh = rs_shape(length);
   uint32_t* sup_ones = (uint32_t*)workspace;
   int64_t* bsum = (int64_t*)((unsigned char*)workspace + align_up((size_t)nvec * sh.nsuper * 4, 256));
-  const dim3 g((unsigned)((sh.nsuper + RS_WARPS - 1) / RS_WARPS), (unsigned)nvec);
-  rs_blocks_kernel<<<g, RS_WARPS * 32, 0, s>>>(words, length, block_zeros, sup_ones);
+  const int64_t per_cta = (int64_t)RS_WARPS * RS_SB_PER_WARP;
+  const dim3 gb((unsigned)((sh.nsuper + per_cta - 1) / per_cta), (unsigned)nvec);
+  rs_blocks_kernel<<<gb, RS_WARPS * 32, 0, s>>>(words, length, block_zeros, sup_ones);
   const int64_t nblk = (sh.nsuper + SCAN_TILE - 1) / SCAN_TILE;
   const dim3 gs((unsigned)nblk, (unsigned)nvec);
   scan_reduce_kernel<<<gs, SCAN_THREADS, 0, s>>>(sup_ones, sh.nsuper, nblk, bsum);
   scan_apply_kernel<<<gs, SCAN_THREADS, 0, s>>>(sup_ones, sh.nsuper, nblk, bsum, super_zeros);
-  rs_samples_kernel<<<g, RS_WARPS * 32, 0, s>>>(words, length, sup_ones, super_zeros, samples1, samples0, ones);
+  const dim3 gsm((unsigned)((sh.nsuper + RS_WARPS * 32 - 1) / (RS_WARPS * 32)), (unsigned)nvec);
+  rs_samples_kernel<<<gsm, RS_WARPS * 32, 0, s>>>(words, length, sup_ones, super_zeros, samples1, samples0, ones);
   return (int)cudaGetLastError();
 }
 

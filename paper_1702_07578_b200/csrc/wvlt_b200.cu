@@ -1567,42 +1567,70 @@ __global__ void __launch_bounds__(U8_THREADS + U8_TABW, U8_CTAS_PER_SM) level_pa
 // ---------------------------------------------------------------------------
 // K5: merge (gather_bits)
 // ---------------------------------------------------------------------------
+// destination word wd of a gather_bits plan, walking forward from task t
+__device__ __forceinline__ uint64_t merge_word(int64_t wd, int64_t nbits, const int64_t* __restrict__ bounds,
+                                               const int64_t* __restrict__ src_starts,
+                                               const uint64_t* __restrict__ src, int64_t t) {
+  const int64_t wb = wd << 6;
+  int64_t nb = nbits - wb;
+  if (nb > 64) nb = 64;
+  uint64_t acc = 0;
+  int filled = 0;
+  while (filled < nb) {
+    const int64_t here = wb + filled;
+    while (__ldg(bounds + t + 1) <= here) ++t;
+    int64_t take = nb - filled;
+    const int64_t avail = __ldg(bounds + t + 1) - here;
+    if (avail < take) take = avail;
+    const int64_t sp = __ldg(src_starts + t) + (here - __ldg(bounds + t));
+    const int64_t wi = sp >> 6;
+    const int sh = (int)(sp & 63);
+    uint64_t chunk = __ldcs(reinterpret_cast<const unsigned long long*>(src) + wi) >> sh;
+    if (sh + take > 64) chunk |= __ldcs(reinterpret_cast<const unsigned long long*>(src) + wi + 1) << (64 - sh);
+    if (take < 64) chunk &= (1ull << take) - 1ull;
+    acc |= chunk << filled;
+    filled += (int)take;
+  }
+  return acc;
+}
+
+constexpr int MERGE_WORDS_PER_LANE = 4;
+
 __global__ void __launch_bounds__(256) merge_bits_kernel(uint64_t* __restrict__ dst, int64_t wlo, int64_t whi,
                                                          int64_t nbits, const int64_t* __restrict__ bounds,
                                                          const int64_t* __restrict__ src_starts, int64_t ntasks,
                                                          const uint64_t* __restrict__ src) {
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t wd = wlo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; wd < whi; wd += stride) {
-    const int64_t wb = wd << 6;
-    int64_t nb = nbits - wb;
-    if (nb > 64) nb = 64;
-    uint64_t acc = 0;
-    if (nb > 0) {
-      // task containing bit wb: last t with bounds[t] <= wb
-      int64_t lo = 0, hi = ntasks;  // answer in [0, ntasks)
+  // a warp owns 32 * MERGE_WORDS_PER_LANE consecutive destination words
+  // (coalesced stores; within a task coalesced source loads); lane 0
+  // binary-searches the task of the warp's first bit, every lane walks forward
+  constexpr int CH = 32 * MERGE_WORDS_PER_LANE;
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t w0 = wlo + ((((int64_t)blockIdx.x * blockDim.x) >> 5) + (threadIdx.x >> 5)) * CH; w0 < whi;
+       w0 += nwarps * CH) {
+    int64_t t0 = 0;
+    if (lane == 0 && (w0 << 6) < nbits) {
+      int64_t lo = 0, hi = ntasks;  // last t with bounds[t] <= bit
+      const int64_t bit = w0 << 6;
       while (hi - lo > 1) {
         const int64_t mid = (lo + hi) >> 1;
-        if (bounds[mid] <= wb) lo = mid; else hi = mid;
+        if (__ldg(bounds + mid) <= bit) lo = mid;
+        else hi = mid;
       }
-      int64_t t = lo;
-      int filled = 0;
-      while (filled < nb) {
-        const int64_t here = wb + filled;
-        while (bounds[t + 1] <= here) ++t;
-        int64_t take = nb - filled;
-        const int64_t avail = bounds[t + 1] - here;
-        if (avail < take) take = avail;
-        const int64_t sp = src_starts[t] + (here - bounds[t]);
-        const int64_t wi = sp >> 6;
-        const int sh = (int)(sp & 63);
-        uint64_t chunk = src[wi] >> sh;
-        if (sh + take > 64) chunk |= src[wi + 1] << (64 - sh);
-        if (take < 64) chunk &= (1ull << take) - 1ull;
-        acc |= chunk << filled;
-        filled += (int)take;
-      }
+      t0 = lo;
     }
-    dst[wd] = acc;
+    t0 = __shfl_sync(FULL, t0, 0);
+    uint64_t v[MERGE_WORDS_PER_LANE];
+#pragma unroll
+    for (int k = 0; k < MERGE_WORDS_PER_LANE; ++k) {
+      const int64_t wd = w0 + 32 * k + lane;
+      v[k] = (wd < whi && (wd << 6) < nbits) ? merge_word(wd, nbits, bounds, src_starts, src, t0) : 0ull;
+    }
+#pragma unroll
+    for (int k = 0; k < MERGE_WORDS_PER_LANE; ++k) {
+      const int64_t wd = w0 + 32 * k + lane;
+      if (wd < whi) __stcs(reinterpret_cast<unsigned long long*>(dst) + wd, v[k]);
+    }
   }
 }
 
@@ -2255,8 +2283,8 @@ int wvlt_merge_bits(uint64_t* dst_words, int64_t word_lo, int64_t word_hi, int64
   if (word_hi == word_lo) return 0;
   if (!dst_words || (n_bits > 0 && (!bounds || !src_starts || !src_words || ntasks < 1))) return WVLT_E_ARG;
   const int64_t nw = word_hi - word_lo;
-  int64_t blocks = (nw + 255) / 256;
-  const int64_t cap = (int64_t)sm_count() * 8;
+  int64_t blocks = (nw + 256 * MERGE_WORDS_PER_LANE - 1) / (256 * MERGE_WORDS_PER_LANE);
+  const int64_t cap = (int64_t)sm_count() * 32;
   if (blocks > cap) blocks = cap;
   merge_bits_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(dst_words, word_lo, word_hi, n_bits, bounds,
                                                                          src_starts, ntasks, src_words);

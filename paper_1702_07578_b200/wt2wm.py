@@ -19,7 +19,7 @@ from .bitperm import bit_reversal_permutation, code_width
 from .structures import BitVector, LevelWiseWaveletTree, WaveletMatrix, zeros_from_histogram
 
 __all__ = ["unary_histogram", "interval_start_table", "TreeToMatrixMap", "recover_histogram", "convert_wt_to_wm",
-           "convert_levels_device"]
+           "convert_levels_device", "ConversionPlan"]
 
 
 def _torch():
@@ -157,30 +157,48 @@ def _level_plans(counts: np.ndarray, width: int):
     return chain, plans
 
 
-def convert_levels_device(tree_words, n: int, sigma: int, counts, builder=None):
+class ConversionPlan:
+    """Device-resident gather_bits plans of every level >= 2 (one H2D copy)."""
+
+    def __init__(self, counts, n: int, sigma: int, device):
+        torch = _torch()
+        self.n, self.sigma, self.width = int(n), int(sigma), code_width(sigma)
+        chain, plans = _level_plans(np.asarray(counts, dtype=np.int64), self.width)
+        self.zeros = [int(zeros_from_histogram(chain[ell + 1])) for ell in range(self.width)]
+        parts, self.slices = [], {}
+        off = 0
+        for ell, (bounds, src) in plans.items():
+            self.slices[ell] = (off, bounds.size, off + bounds.size, src.size)
+            parts += [bounds, src]
+            off += bounds.size + src.size
+        flat = np.concatenate(parts) if parts else np.zeros(1, dtype=np.int64)
+        host = torch.from_numpy(flat).pin_memory() if torch.cuda.is_available() else torch.from_numpy(flat)
+        self.buf = host.to(device, non_blocking=True)
+
+    def run(self, tree_words, out, builder):
+        nwords = (self.n + 63) >> 6
+        for ell in range(min(self.width, 2)):
+            out[ell].copy_(tree_words[ell])
+        if self.n == 0:
+            return out
+        for ell, (b0, nb, s0, ns) in self.slices.items():
+            builder.merge_bits(out[ell], 0, nwords, self.n, self.buf[b0 : b0 + nb], self.buf[s0 : s0 + ns],
+                               tree_words[ell], dst_offset_words=0)
+        return out
+
+
+def convert_levels_device(tree_words, n: int, sigma: int, counts, builder=None, plan=None):
     """Device conversion core: int64 tensor [width, ceil(n/64)] of tree level words
     -> (matrix level words tensor, zero counts).  Levels >= 2 go through
     wvlt_merge_bits; levels 0 and 1 are copied."""
     torch = _torch()
     from .device import default_builder
 
-    width = code_width(sigma)
-    counts = np.asarray(counts, dtype=np.int64)
     b = builder or default_builder(tree_words.device)
+    plan = plan or ConversionPlan(counts, n, sigma, tree_words.device)
     out = torch.empty_like(tree_words)
-    nwords = (n + 63) >> 6
-    chain, plans = _level_plans(counts, width)
-    zeros = [int(zeros_from_histogram(chain[ell + 1])) for ell in range(width)]
-    for ell in range(min(width, 2)):
-        out[ell].copy_(tree_words[ell])
-    for ell in range(2, width):
-        bounds, src = plans[ell]
-        if n == 0:
-            continue
-        bt = torch.from_numpy(bounds).to(tree_words.device)
-        st = torch.from_numpy(src).to(tree_words.device)
-        b.merge_bits(out[ell], 0, nwords, n, bt, st, tree_words[ell], dst_offset_words=0)
-    return out, zeros
+    plan.run(tree_words, out, b)
+    return out, list(plan.zeros)
 
 
 def convert_wt_to_wm(wt: LevelWiseWaveletTree, text=None, histogram=None) -> WaveletMatrix:
