@@ -1,0 +1,574 @@
+// K8: the whole build of a byte text with code width 5 <= W <= 8 in ONE fused
+// pass.  For a wavelet matrix the symbols of level l with equal l-bit key keep
+// their text order (A_l is the stable LSD sort of the text by the key), and
+// for the tree the same holds per prefix group, so every level's contribution
+// of a text tile is a set of contiguous runs placed by the tile prefix of its
+// W-bit digit counts.  One CTA per 8192-symbol tile runs the W-1 stable
+// one-bit splits in shared memory and emits all W levels -- no intermediate
+// order ever goes back to HBM, no second pass.  Needs per-tile counts of all
+// 2^W digits (hist8_kernel) and their prefix over tiles (scan8_* kernels).
+// Included from wvlt_b200.cu (same translation unit).
+
+namespace {
+
+// ---- K1: per-tile counts of every W-bit value (tile-major [tile][2^W]) ----
+// One warp per tile; lane-private 16-bit counters paired (p, p + 2^(W-1)) as in
+// hist_u8_kernel, zeroed after every tile so the per-tile row sums never carry.
+constexpr int H8_WARPS = 4;
+
+template <int W>
+__global__ void __launch_bounds__(H8_WARPS * 32) hist8_kernel(const uint8_t* __restrict__ text, int64_t n,
+                                                             int64_t ntiles, uint32_t vmax_ok, int check,
+                                                             uint32_t* __restrict__ tcnt8,
+                                                             int32_t* __restrict__ status) {
+  constexpr int NB = 1 << W;
+  constexpr int HALF = NB / 2;
+  constexpr int WORDS = HALF * 32;
+  extern __shared__ __align__(16) uint32_t s_cols[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint32_t* c32 = s_cols + (size_t)wid * WORDS;
+  uint32_t* c32w = c32 + lane;
+  for (int i = lane; i < WORDS; i += 32) c32[i] = 0;
+  __syncwarp();
+  uint32_t vmax = 0;
+  const bool aligned = (((uintptr_t)text) & 15) == 0;
+  const int64_t nwarps = (int64_t)gridDim.x * H8_WARPS;
+  for (int64_t t = (int64_t)blockIdx.x * H8_WARPS + wid; t < ntiles; t += nwarps) {
+    const int64_t first = t * TILE_U8;
+    const int cnt = (int)min((int64_t)TILE_U8, n - first);
+    if (cnt == TILE_U8 && aligned) {
+      const uint4* v4 = reinterpret_cast<const uint4*>(text + first);
+#pragma unroll 1
+      for (int k0 = 0; k0 < TILE_U8 / 16 / 32; k0 += 8) {
+        uint4 q[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) q[k] = __ldcs(v4 + (k0 + k) * 32 + lane);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t wd[4] = {q[k].x, q[k].y, q[k].z, q[k].w};
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if (check) vmax = __vmaxu4(vmax, wd[u]);
+            const uint32_t lo = wd[u] & ((uint32_t)(HALF - 1) * 0x01010101u);
+            const uint32_t hb = (wd[u] >> (W - 1)) & 0x01010101u;
+#pragma unroll
+            for (int b = 0; b < 4; ++b)
+              atomicAdd(c32w + prmt(lo, 0, 0x4440 + b) * 32, prmt(hb, 0, 0x4440 + b) * 0xFFFFu + 1u);
+          }
+        }
+      }
+    } else {
+      for (int i = lane; i < cnt; i += 32) {
+        const uint32_t v = text[first + i];
+        vmax = max(vmax, v);
+        atomicAdd(c32w + (v & (HALF - 1)) * 32, ((v >> (W - 1)) & 1u) ? 0x10000u : 1u);
+      }
+    }
+    __syncwarp();
+    // row p (bins p, p + HALF) summed over the 32 lane columns; lane l takes rows
+    // l, l + 32, ...; skewed reads keep the 32 lanes on distinct banks
+    uint32_t* row_out = tcnt8 + t * NB;
+    for (int p = lane; p < HALF; p += 32) {
+      uint32_t s = 0;
+#pragma unroll 8
+      for (int k = 0; k < 32; ++k) s += c32[p * 32 + ((k + lane) & 31)];
+      row_out[p] = s & 0xFFFFu;
+      row_out[p + HALF] = s >> 16;
+    }
+    __syncwarp();
+    for (int i = lane * 4; i < WORDS; i += 128) *reinterpret_cast<uint4*>(c32 + i) = make_uint4(0, 0, 0, 0);
+    __syncwarp();
+  }
+  if (check) {
+    vmax = max(max(vmax & 0xFFu, (vmax >> 8) & 0xFFu), max((vmax >> 16) & 0xFFu, vmax >> 24));
+    if (vmax > vmax_ok) atomicOr(status, WVLT_STATUS_RANGE);
+  }
+}
+
+// ---- S8: exclusive prefix over tiles of every column of tcnt8 ----
+// chunks of S8_CHUNK tiles: per-chunk column sums (thread = column, 16 loads
+// in flight), a block-wide scan of each column over the chunks, then the
+// per-tile prefixes from the chunk carries.
+constexpr int S8_CHUNK = 64;     // tiles per chunk
+constexpr int S8_UNROLL = 16;
+constexpr int S8_SCAN_THREADS = 512;
+
+__global__ void __launch_bounds__(256) scan8_chunks_kernel(const uint32_t* __restrict__ tcnt8, int64_t ntiles,
+                                                          int nb, uint32_t* __restrict__ chunk) {
+  const int d = threadIdx.x;
+  const int64_t t0 = (int64_t)blockIdx.x * S8_CHUNK, t1 = min(t0 + S8_CHUNK, ntiles);
+  uint32_t s = 0;
+  for (int64_t t = t0; t < t1; t += S8_UNROLL) {
+    uint32_t v[S8_UNROLL];
+#pragma unroll
+    for (int u = 0; u < S8_UNROLL; ++u) v[u] = t + u < t1 ? __ldcs(tcnt8 + (t + u) * nb + d) : 0u;
+#pragma unroll
+    for (int u = 0; u < S8_UNROLL; ++u) s += v[u];
+  }
+  chunk[(int64_t)blockIdx.x * nb + d] = s;
+}
+
+// one block per column: exclusive scan of the column over the chunks (in
+// place) and the column total
+__global__ void __launch_bounds__(S8_SCAN_THREADS) scan8_carry_kernel(uint32_t* __restrict__ chunk, int64_t nchunks,
+                                                                     int nb, int64_t* __restrict__ totals) {
+  __shared__ uint32_t s_w[S8_SCAN_THREADS / 32];
+  const int d = blockIdx.x;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint32_t carry = 0;
+  for (int64_t b0 = 0; b0 < nchunks; b0 += S8_SCAN_THREADS) {
+    const int64_t b = b0 + threadIdx.x;
+    const uint32_t v = b < nchunks ? chunk[b * nb + d] : 0u;
+    const uint32_t incl = warp_incl_scan(v);
+    if (lane == 31) s_w[wid] = incl;
+    __syncthreads();
+    uint32_t wpre = 0, tot = 0;
+#pragma unroll
+    for (int k = 0; k < S8_SCAN_THREADS / 32; ++k) {
+      const uint32_t t = s_w[k];
+      wpre += k < wid ? t : 0u;
+      tot += t;
+    }
+    if (b < nchunks) chunk[b * nb + d] = carry + wpre + incl - v;
+    carry += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) totals[d] = carry;
+}
+
+__global__ void __launch_bounds__(256) scan8_apply_kernel(const uint32_t* __restrict__ tcnt8, int64_t ntiles, int nb,
+                                                         const uint32_t* __restrict__ chunk,
+                                                         uint32_t* __restrict__ tpre8) {
+  const int d = threadIdx.x;
+  const int64_t t0 = (int64_t)blockIdx.x * S8_CHUNK, t1 = min(t0 + S8_CHUNK, ntiles);
+  uint32_t run = chunk[(int64_t)blockIdx.x * nb + d];
+  for (int64_t t = t0; t < t1; t += S8_UNROLL) {
+    uint32_t v[S8_UNROLL];
+#pragma unroll
+    for (int u = 0; u < S8_UNROLL; ++u) v[u] = t + u < t1 ? __ldcs(tcnt8 + (t + u) * nb + d) : 0u;
+#pragma unroll
+    for (int u = 0; u < S8_UNROLL; ++u) {
+      if (t + u < t1) tpre8[(t + u) * nb + d] = run;
+      run += v[u];
+    }
+  }
+}
+
+// ---- T8: global placement tables from the digit totals ----
+// base[j * 256 + d], 1 <= j < W, d < 2^j an LSD digit: where the group of d
+// starts in level j (WM: exclusive prefix of the group sizes in LSD-digit
+// order; WT: interval start of the numeric prefix rev(d)).  Also the zero
+// counts per level and (optionally) the histogram.
+__global__ void tables8_kernel(const int64_t* __restrict__ totals, int W, int kind, int64_t* __restrict__ base,
+                               int64_t* __restrict__ zeros, int64_t* __restrict__ hist) {
+  __shared__ int64_t s_cnt[256];
+  const int nb = 1 << W;
+  const int tid = threadIdx.x;
+  if (hist && tid < nb) hist[tid] = totals[tid];
+  if (tid == 0) {
+    for (int l = 0; l < W; ++l) {
+      int64_t z = 0;
+      for (int e = 0; e < nb; ++e)
+        if (!((e >> (W - 1 - l)) & 1)) z += totals[e];
+      if (zeros) zeros[l] = z;
+    }
+    for (int j = 1; j < W; ++j) {
+      const int mj = 1 << j;
+      for (int d = 0; d < mj; ++d) s_cnt[d] = 0;
+      for (int e = 0; e < nb; ++e) {
+        if (kind == WVLT_KIND_WM) s_cnt[rev_bits((unsigned)e, W) & (mj - 1)] += totals[e];
+        else s_cnt[e >> (W - j)] += totals[e];  // numeric j-bit prefix
+      }
+      int64_t run = 0;
+      if (kind == WVLT_KIND_WM) {
+        for (int d = 0; d < mj; ++d) {
+          base[j * 256 + d] = run;
+          run += s_cnt[d];
+        }
+      } else {
+        for (int P = 0; P < mj; ++P) {
+          base[j * 256 + rev_bits((unsigned)P, j)] = run;
+          run += s_cnt[P];
+        }
+      }
+    }
+  }
+}
+
+// ---- K3 (K8): the fused pass ----
+struct Pass8Args {
+  const uint8_t* src;
+  uint64_t* words;
+  int64_t nwords, n, ntiles;
+  const uint32_t* tcnt8;
+  const uint32_t* tpre8;
+  const int64_t* base;  // [8][256]
+};
+
+// Runs of levels 1..W-1 flattened: run r = 2^j - 2 + d (j = level, d = LSD digit).
+struct Tables8 {
+  int cnt[256];       // run sizes
+  int ls[256];        // run starts in the tile-local order of its level
+  int64_t gs[256];    // run starts in the global level
+  int64_t lb[256];    // symbols of earlier tiles in the run's group (scratch)
+  int wpre[256];      // emission: destination words before each run (+ total)
+  int cW[256];        // level-W digit counts (scratch)
+  uint32_t lbW[256];  // level-W tile prefixes (scratch)
+  int64_t base[256];  // global group starts of every run (copy of Pass8Args::base)
+};
+
+template <int W>
+__device__ __forceinline__ void table8_warp(const Pass8Args& a, Tables8& tt, int64_t tile, int lane, int allt) {
+  constexpr int NB = 1 << W;
+  constexpr int NR = NB - 2;
+  const uint32_t* cr = a.tcnt8 + tile * NB;
+  const uint32_t* pr = a.tpre8 + tile * NB;
+  // every global input up front: one round trip instead of one per level
+  for (int e = lane; e < NB; e += 32) {
+    const int d = (int)rev_bits((unsigned)e, W);
+    tt.cW[d] = (int)__ldg(cr + e);
+    tt.lbW[d] = __ldg(pr + e);
+  }
+  for (int r = lane; r < NR; r += 32) {
+    const int j = 31 - __clz(r + 2);
+    tt.base[r] = __ldg(a.base + j * 256 + (r + 2 - (1 << j)));
+  }
+  __syncwarp();
+  // fold: level j's digit d collects the level j+1 digits d and d + 2^j
+#pragma unroll 1
+  for (int j = W - 1; j >= 1; --j) {
+    const int mj = 1 << j;
+    for (int d = lane; d < mj; d += 32) {
+      int c;
+      int64_t lb;
+      if (j == W - 1) {
+        c = tt.cW[d] + tt.cW[d + mj];
+        lb = (int64_t)tt.lbW[d] + (int64_t)tt.lbW[d + mj];
+      } else {
+        const int up = (2 << j) - 2;
+        c = tt.cnt[up + d] + tt.cnt[up + d + mj];
+        lb = tt.lb[up + d] + tt.lb[up + d + mj];
+      }
+      const int r = mj - 2 + d;
+      tt.cnt[r] = c;
+      tt.lb[r] = lb;
+      tt.gs[r] = tt.base[r] + lb;
+    }
+    __syncwarp();
+  }
+  // tile-local run starts: exclusive prefix of each level's run sizes
+#pragma unroll 1
+  for (int j = 1; j < W; ++j) {
+    const int mj = 1 << j, r0 = mj - 2;
+    const int per = (mj + 31) / 32;  // consecutive runs per lane
+    int loc = 0;
+    for (int k = 0; k < per; ++k) {
+      const int d = lane * per + k;
+      if (d < mj) loc += tt.cnt[r0 + d];
+    }
+    const int ex = (int)warp_incl_scan((uint32_t)loc) - loc;
+    int run = ex;
+    for (int k = 0; k < per; ++k) {
+      const int d = lane * per + k;
+      if (d < mj) {
+        tt.ls[r0 + d] = run;
+        run += tt.cnt[r0 + d];
+      }
+    }
+  }
+  __syncwarp();
+  // destination words per run, flattened exclusive prefix
+  {
+    constexpr int per = (NR + 31) / 32;
+    int nw[per];
+    int loc = 0;
+#pragma unroll
+    for (int k = 0; k < per; ++k) {
+      const int r = lane * per + k;
+      nw[k] = 0;
+      if (r < NR) {
+        const int c = tt.cnt[r];
+        if (c) {
+          const int64_t g = tt.gs[r];
+          nw[k] = (int)(((g + c - 1) >> 6) - (g >> 6) + 1);
+        }
+      }
+      loc += nw[k];
+    }
+    const int ex = (int)warp_incl_scan((uint32_t)loc) - loc;
+    int run = ex;
+#pragma unroll
+    for (int k = 0; k < per; ++k) {
+      const int r = lane * per + k;
+      if (r < NR) tt.wpre[r] = run;
+      run += nw[k];
+    }
+    if (lane == 31) tt.wpre[NR] = run;
+  }
+  __threadfence_block();
+  bar_arrive(2, allt);
+}
+
+template <int W>
+__global__ void __launch_bounds__(U8_THREADS + TAB_WARP_THREADS, U8_CTAS_PER_SM) level_pass8_kernel(const Pass8Args a) {
+  constexpr int T = U8_THREADS * 16;
+  constexpr int H = T / 2;
+  constexpr int NC = T / 32;
+  constexpr int NW = U8_THREADS / 32;
+  constexpr int ALLT = U8_THREADS + TAB_WARP_THREADS;
+  constexpr int NR = (1 << W) - 2;
+  constexpr uint32_t B1 = 0x01010101u;
+  extern __shared__ __align__(128) unsigned char smem[];
+  // [stage | ping-pong order buffer | level bits of levels 1..W-1]
+  uint32_t* bits = reinterpret_cast<uint32_t*>(smem + 2 * T);
+  __shared__ Tables8 tt;
+  __shared__ __align__(16) uint32_t s_wtot[2][NW];
+  __shared__ uint32_t s_lut[256];
+  __shared__ __align__(8) uint64_t s_mbar;
+
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int64_t tile = blockIdx.x;
+  const int64_t base = tile * T;
+  const int cnt = (int)min((int64_t)T, a.n - base);
+  const uint8_t* text = a.src;
+  if (wid == NW) {
+    table8_warp<W>(a, tt, tile, lane, ALLT);
+    return;
+  }
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
+  const uint32_t mbar = (uint32_t)__cvta_generic_to_shared(&s_mbar);
+  const bool bulk = (((uintptr_t)text) & 15) == 0 && cnt == T;
+  if (tid == 0 && bulk) {
+    mbar_init(mbar, 1);
+    fence_mbar_init();
+    bulk_load(sbase, text + base, T, mbar);
+  }
+  for (int i = tid; i < 256; i += U8_THREADS) s_lut[i] = g_sort_lut.sel[i];
+  if (bulk) {
+    bar_sync(1, U8_THREADS);  // mbarrier initialised
+    mbar_wait(mbar, 0);
+  } else {
+    for (int p = tid; p < T; p += U8_THREADS) smem[p] = p < cnt ? text[base + p] : (uint8_t)0xFF;
+    bar_sync(1, U8_THREADS);
+  }
+  uint8_t* bits8 = reinterpret_cast<uint8_t*>(bits);
+
+#pragma unroll
+  for (int j = 0; j < W; ++j) {
+    const int sh = W - 1 - j;
+    const uint8_t* cur = smem + (size_t)(j & 1) * T;
+    const uint2 q0 = reinterpret_cast<const uint2*>(cur)[tid];
+    const uint2 q1 = reinterpret_cast<const uint2*>(cur + H)[tid];
+    const uint32_t x[4] = {q0.x, q0.y, q1.x, q1.y};
+    uint32_t b[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) b[k] = (x[k] >> sh) & B1;
+    const uint32_t m0 = ((b[1] * 16u + b[0]) * 0x01020408u) >> 24;
+    const uint32_t m1 = ((b[3] * 16u + b[2]) * 0x01020408u) >> 24;
+    const uint32_t ones0 = __popc(m0), ones1 = __popc(m1);
+    if (j == 0) {
+      uint8_t* g8 = reinterpret_cast<uint8_t*>(a.words) + (base >> 3);
+      const int64_t lim = 8 * a.nwords - (base >> 3);
+      const int f0 = 8 * tid, f1 = H + 8 * tid;
+      if (tid < lim) g8[tid] = (uint8_t)(f0 + 8 <= cnt ? m0 : (f0 >= cnt ? 0u : (m0 & ((1u << (cnt - f0)) - 1u))));
+      if (H / 8 + tid < lim)
+        g8[H / 8 + tid] = (uint8_t)(f1 + 8 <= cnt ? m1 : (f1 >= cnt ? 0u : (m1 & ((1u << (cnt - f1)) - 1u))));
+    } else {
+      bits8[j * 4 * (NC + 4) + tid] = (uint8_t)m0;
+      bits8[j * 4 * (NC + 4) + H / 8 + tid] = (uint8_t)m1;
+    }
+    if (j + 1 == W) break;
+    const uint32_t pk = ones0 | (ones1 << 16);
+    const uint32_t incl = warp_incl_scan(pk);
+    if (lane == 31) s_wtot[j & 1][wid] = incl;
+    bar_sync(1, U8_THREADS);
+    const uint32_t wv = lane < NW ? s_wtot[j & 1][lane] : 0u;
+    const uint32_t wpre = __reduce_add_sync(FULL, lane < wid ? wv : 0u);
+    const uint32_t tot = __reduce_add_sync(FULL, wv);
+    const uint32_t ex = wpre + incl - pk;
+    const int tot0 = (int)(tot & 0xFFFFu), tot1 = (int)(tot >> 16);
+    const int Z = T - tot0 - tot1;
+    const int opre0 = (int)(ex & 0xFFFFu);
+    const int opre1 = tot0 + (int)(ex >> 16);
+    const int OB[2] = {Z + opre0 - 1, Z + opre1 - 1};
+    const int ZB[2] = {8 * tid - opre0, H + 8 * tid - opre1};
+    const uint32_t nxt = sbase + (uint32_t)((j + 1) & 1) * T;
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+      const uint32_t sel = s_lut[hh ? m1 : m0];
+      const uint32_t sv[2] = {prmt(x[2 * hh], x[2 * hh + 1], sel), prmt(x[2 * hh], x[2 * hh + 1], sel >> 16)};
+      const int nz = 8 - (int)(hh ? ones1 : ones0);
+      const uint32_t za = opaque(nxt + (uint32_t)ZB[hh]);
+      const uint32_t oa = opaque(nxt + (uint32_t)(OB[hh] + 1 - nz));
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        const uint32_t v = sv[kk >> 2];
+        const uint32_t vb = (kk & 3) == 0 ? v : (kk & 3) == 1 ? (v >> 8) : (kk & 3) == 2 ? (v >> 16) : (v >> 24);
+        const uint32_t addr = (kk < nz ? za : oa) + kk;
+        asm volatile("st.shared.u8 [%0], %1;" ::"r"(addr), "r"(vb) : "memory");
+      }
+    }
+    bar_sync(1, U8_THREADS);
+  }
+  bar_sync(1, U8_THREADS);  // every warp's level bits are stored
+  bar_sync(2, ALLT);        // run tables
+  // emission of levels 1..W-1: one destination word per task, the runs of all
+  // levels flattened (consecutive tasks = consecutive words of one run, so
+  // the stores of a warp coalesce); whole words stored, run-edge words OR-ed
+  // (runs of neighbouring tiles share them; the levels were zeroed)
+  const int total = tt.wpre[NR];
+  for (int q = tid; q < total; q += U8_THREADS) {
+    int r = 0;  // last run with wpre[r] <= q (empty runs share prefix values)
+#pragma unroll
+    for (int s = 128; s >= 1; s >>= 1)
+      if (r + s < NR && tt.wpre[r + s] <= q) r += s;
+    const int j = 31 - __clz(r + 2);
+    const int64_t g = tt.gs[r];
+    const int c = tt.cnt[r];
+    const int64_t wd = (g >> 6) + (q - tt.wpre[r]);
+    const int64_t wb = wd << 6;
+    const int64_t lo = g > wb ? g : wb;
+    const int64_t hi = (g + c) < wb + 64 ? (g + c) : wb + 64;
+    const int len = (int)(hi - lo);
+    const uint32_t* L = bits + j * (NC + 4);
+    const uint64_t v = extract_bits(L, tt.ls[r] + (int)(lo - g), len) << (lo - wb);
+    uint64_t* dstw = a.words + (int64_t)j * a.nwords + wd;
+    if (len == 64) *dstw = v;
+    else if (v) atomicOr(reinterpret_cast<unsigned long long*>(dstw), (unsigned long long)v);
+  }
+}
+
+template <int W>
+cudaError_t launch_pass8(const Pass8Args& a, cudaStream_t s) {
+  constexpr int T = U8_THREADS * 16;
+  const size_t smem = 2 * (size_t)T + (size_t)W * (T / 32 + 4) * 4;
+  auto kern = level_pass8_kernel<W>;
+  static bool set = false;
+  if (!set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
+    if (e != cudaSuccess) return e;
+    set = true;
+  }
+  kern<<<(unsigned)a.ntiles, U8_THREADS + TAB_WARP_THREADS, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+template <int W>
+cudaError_t launch_hist8(const uint8_t* text, int64_t n, int64_t ntiles, uint32_t vmax_ok, int check,
+                         uint32_t* tcnt8, int32_t* status, cudaStream_t s) {
+  constexpr size_t sb = (size_t)H8_WARPS * (1 << (W - 1)) * 32 * 4;
+  static bool set = false;
+  if (!set) {
+    cudaError_t e = cudaFuncSetAttribute(hist8_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
+    if (e != cudaSuccess) return e;
+    set = true;
+  }
+  const int per_sm = (int)std::min<size_t>(8, (size_t)(220 * 1024) / (sb + 1024));
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((ntiles + H8_WARPS - 1) / H8_WARPS,
+                                                                 (int64_t)sm_count() * per_sm));
+  hist8_kernel<W><<<(unsigned)blocks, H8_WARPS * 32, sb, s>>>(text, n, ntiles, vmax_ok, check, tcnt8, status);
+  return cudaGetLastError();
+}
+
+// Workspace of the single-pass byte build.
+struct K8Layout {
+  size_t off_tcnt, off_tpre, off_chunk, off_totals, off_base, total;
+  int64_t ntiles, nchunks;
+};
+
+inline bool k8_eligible(int sym_bytes, int w, int64_t n) {
+#ifdef WVLT_NO_K8
+  return false;
+#else
+  return sym_bytes == 1 && w >= 5 && w <= 8 && n > 0 && n < (1ll << 32);
+#endif
+}
+
+inline K8Layout k8_layout(int64_t n, int w) {
+  K8Layout L;
+  const int nb = 1 << w;
+  L.ntiles = (n + TILE_U8 - 1) / TILE_U8;
+  L.nchunks = (L.ntiles + S8_CHUNK - 1) / S8_CHUNK;
+  size_t off = 0;
+  L.off_tcnt = off;
+  off = align_up(off + (size_t)L.ntiles * nb * 4, 256);
+  L.off_tpre = off;
+  off = align_up(off + (size_t)L.ntiles * nb * 4, 256);
+  L.off_chunk = off;
+  off = align_up(off + (size_t)L.nchunks * nb * 4, 256);
+  L.off_totals = off;
+  off = align_up(off + (size_t)nb * 8, 256);
+  L.off_base = off;
+  off = align_up(off + (size_t)8 * 256 * 8, 256);
+  L.total = off + 256;  // + status scratch
+  return L;
+}
+
+// The whole single-pass build (called by build_device_impl).
+int build_k8(const uint8_t* text, int64_t n, int64_t sigma, int w, int kind, uint64_t* level_words,
+             int64_t* zeros, int64_t* hist, void* workspace, int32_t* status, cudaStream_t s,
+             void (*pass_done)(void*, int, int), void* ctx) {
+  const K8Layout L = k8_layout(n, w);
+  const int nb = 1 << w;
+  unsigned char* ws = (unsigned char*)workspace;
+  uint32_t* tcnt8 = (uint32_t*)(ws + L.off_tcnt);
+  uint32_t* tpre8 = (uint32_t*)(ws + L.off_tpre);
+  uint32_t* chunk = (uint32_t*)(ws + L.off_chunk);
+  int64_t* totals = (int64_t*)(ws + L.off_totals);
+  int64_t* base = (int64_t*)(ws + L.off_base);
+  int32_t* st_flag = status ? status : (int32_t*)(ws + L.total - 256);
+  const int64_t nwords = (n + 63) >> 6;
+  cudaError_t e;
+  g_prof.n = 0;
+  prof_mark(s, -1);
+  e = cudaMemsetAsync(level_words, 0, (size_t)w * nwords * 8, s);
+  if (e != cudaSuccess) return (int)e;
+  if (!status) {
+    e = cudaMemsetAsync(st_flag, 0, 4, s);
+    if (e != cudaSuccess) return (int)e;
+  }
+  prof_mark(s, WVLT_STAGE_MEMSET);
+  const uint32_t vmax_ok = (uint32_t)std::min<int64_t>(sigma - 1, 255);
+  const int check = vmax_ok < 255 ? 1 : 0;
+  switch (w) {
+    case 5: e = launch_hist8<5>(text, n, L.ntiles, vmax_ok, check, tcnt8, st_flag, s); break;
+    case 6: e = launch_hist8<6>(text, n, L.ntiles, vmax_ok, check, tcnt8, st_flag, s); break;
+    case 7: e = launch_hist8<7>(text, n, L.ntiles, vmax_ok, check, tcnt8, st_flag, s); break;
+    default: e = launch_hist8<8>(text, n, L.ntiles, vmax_ok, check, tcnt8, st_flag, s); break;
+  }
+  if (e != cudaSuccess) return (int)e;
+  ++g_launches;
+  prof_mark(s, WVLT_STAGE_HIST);
+  scan8_chunks_kernel<<<(unsigned)L.nchunks, nb, 0, s>>>(tcnt8, L.ntiles, nb, chunk);
+  scan8_carry_kernel<<<nb, S8_SCAN_THREADS, 0, s>>>(chunk, L.nchunks, nb, totals);
+  scan8_apply_kernel<<<(unsigned)L.nchunks, nb, 0, s>>>(tcnt8, L.ntiles, nb, chunk, tpre8);
+  tables8_kernel<<<1, 256, 0, s>>>(totals, w, kind, base, zeros, hist);
+  g_launches += 4;
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return (int)e;
+  prof_mark(s, WVLT_STAGE_SCAN0);
+  Pass8Args a;
+  a.src = text;
+  a.words = level_words;
+  a.nwords = nwords;
+  a.n = n;
+  a.ntiles = L.ntiles;
+  a.tcnt8 = tcnt8;
+  a.tpre8 = tpre8;
+  a.base = base;
+  switch (w) {
+    case 5: e = launch_pass8<5>(a, s); break;
+    case 6: e = launch_pass8<6>(a, s); break;
+    case 7: e = launch_pass8<7>(a, s); break;
+    default: e = launch_pass8<8>(a, s); break;
+  }
+  if (e != cudaSuccess) return (int)e;
+  ++g_launches;
+  prof_mark(s, WVLT_STAGE_PASS0);
+  if (pass_done) pass_done(ctx, 0, w);
+  return 0;
+}
+
+}  // namespace

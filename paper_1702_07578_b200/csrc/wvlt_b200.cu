@@ -1937,6 +1937,8 @@ void prof_mark(cudaStream_t s, int stage_id) {
 
 }  // namespace
 
+#include "k8.cuh"
+
 namespace {
 int build_device_impl(const void* text, int sym_bytes, int64_t n, int64_t sigma, int kind, uint64_t* level_words,
                       int64_t* zeros, int64_t* hist, int64_t* borders, void* workspace, size_t workspace_bytes,
@@ -1988,6 +1990,7 @@ size_t wvlt_workspace_bytes(int64_t n, int sym_bytes, int64_t sigma, int kind) {
   Plan P;
   if (n < 0 || !(sym_bytes == 1 || sym_bytes == 2 || sym_bytes == 4)) return 0;
   if (!make_plan(n, sym_bytes, sigma, kind, &P)) return 0;
+  if (k8_eligible(sym_bytes, P.width, n) && !P.widen_bytes) return std::max(P.total, k8_layout(n, P.width).total);
   return P.total;
 }
 
@@ -2057,6 +2060,12 @@ int build_device_impl(const void* text, int sym_bytes, int64_t n, int64_t sigma,
     return 0;
   }
   if (!text || !level_words || !workspace) return WVLT_E_ARG;
+  if (k8_eligible(sym_bytes, w, n) && !borders && !P.widen_bytes) {
+    // byte text, 5 <= w <= 8: every level in one fused pass (k8.cuh)
+    if (workspace_bytes < k8_layout(n, w).total) return WVLT_E_WORKSPACE;
+    return build_k8((const uint8_t*)text, n, sigma, w, kind, level_words, zeros, hist, workspace, status, s,
+                    pass_done, ctx);
+  }
   if (workspace_bytes < P.total) return WVLT_E_WORKSPACE;
   unsigned char* ws = (unsigned char*)workspace;
   int64_t* chain = (int64_t*)(ws + P.off_chain);
