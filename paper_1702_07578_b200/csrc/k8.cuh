@@ -11,6 +11,10 @@
 
 namespace {
 
+#ifndef U8_K8_CTAS
+#define U8_K8_CTAS 4  // 16 warps per CTA, no table warp
+#endif
+
 // ---- K1: per-tile counts of every W-bit value (tile-major [tile][2^W]) ----
 // One warp per tile; lane-private 16-bit counters paired (p, p + 2^(W-1)) as in
 // hist_u8_kernel, zeroed after every tile so the per-tile row sums never carry.
@@ -305,23 +309,57 @@ __device__ __forceinline__ void table8_warp(const Pass8Args& a, Tables8& tt, int
     }
     if (lane == 31) tt.wpre[NR] = run;
   }
-  __threadfence_block();
-  bar_arrive(2, allt);
+  if (allt > 0) {
+    __threadfence_block();
+    bar_arrive(2, allt);
+  }
+}
+
+// Compact per-tile run table written by tiles8_kernel and bulk-copied into
+// the pass kernel's shared memory with the tile: positions fit 32 bits (the
+// single-pass path needs n < 2^32), sizes and offsets inside a tile 16 bits.
+struct Tab8 {
+  uint32_t gs[256];   // run starts in the global level
+  uint16_t cnt[256];  // run sizes
+  uint16_t ls[256];   // run starts in the tile-local order of the level
+  uint16_t wpre[256]; // destination words before each run; wpre[NR] = total
+};
+static_assert(sizeof(Tab8) % 16 == 0, "bulk-copy granularity");
+
+constexpr int T8_WARPS = 4;
+
+// One warp per tile: the tile's run tables (table8_warp) into the compact
+// global layout, off the pass kernel's critical path.
+template <int W>
+__global__ void __launch_bounds__(T8_WARPS * 32) tiles8_kernel(const Pass8Args a, Tab8* __restrict__ out) {
+  extern __shared__ __align__(16) unsigned char t8_smem[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  Tables8& tt = reinterpret_cast<Tables8*>(t8_smem)[wid];
+  const int64_t tile = (int64_t)blockIdx.x * T8_WARPS + wid;
+  if (tile >= a.ntiles) return;
+  table8_warp<W>(a, tt, tile, lane, 0);
+  __syncwarp();
+  Tab8* o = out + tile;
+  for (int r = lane; r < 256; r += 32) {
+    o->gs[r] = (uint32_t)tt.gs[r];
+    o->cnt[r] = (uint16_t)tt.cnt[r];
+    o->ls[r] = (uint16_t)tt.ls[r];
+    o->wpre[r] = (uint16_t)tt.wpre[r];
+  }
 }
 
 template <int W>
-__global__ void __launch_bounds__(U8_THREADS + TAB_WARP_THREADS, U8_CTAS_PER_SM) level_pass8_kernel(const Pass8Args a) {
+__global__ void __launch_bounds__(U8_THREADS, U8_K8_CTAS) level_pass8_kernel(const Pass8Args a, const Tab8* __restrict__ tabs) {
   constexpr int T = U8_THREADS * 16;
   constexpr int H = T / 2;
   constexpr int NC = T / 32;
   constexpr int NW = U8_THREADS / 32;
-  constexpr int ALLT = U8_THREADS + TAB_WARP_THREADS;
   constexpr int NR = (1 << W) - 2;
   constexpr uint32_t B1 = 0x01010101u;
   extern __shared__ __align__(128) unsigned char smem[];
-  // [stage | ping-pong order buffer | level bits of levels 1..W-1]
-  uint32_t* bits = reinterpret_cast<uint32_t*>(smem + 2 * T);
-  __shared__ Tables8 tt;
+  // [stage | ping-pong order buffer | run table | level bits of levels 1..W-1]
+  Tab8& tt = *reinterpret_cast<Tab8*>(smem + 2 * T);
+  uint32_t* bits = reinterpret_cast<uint32_t*>(smem + 2 * T + sizeof(Tab8));
   __shared__ __align__(16) uint32_t s_wtot[2][NW];
   __shared__ uint32_t s_lut[256];
   __shared__ __align__(8) uint64_t s_mbar;
@@ -331,26 +369,31 @@ __global__ void __launch_bounds__(U8_THREADS + TAB_WARP_THREADS, U8_CTAS_PER_SM)
   const int64_t base = tile * T;
   const int cnt = (int)min((int64_t)T, a.n - base);
   const uint8_t* text = a.src;
-  if (wid == NW) {
-    table8_warp<W>(a, tt, tile, lane, ALLT);
-    return;
-  }
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
   const uint32_t mbar = (uint32_t)__cvta_generic_to_shared(&s_mbar);
   const bool bulk = (((uintptr_t)text) & 15) == 0 && cnt == T;
-  if (tid == 0 && bulk) {
+  if (tid == 0) {
     mbar_init(mbar, 1);
     fence_mbar_init();
-    bulk_load(sbase, text + base, T, mbar);
+    // the run table always comes by bulk copy, the tile when it is whole and aligned
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar),
+                 "r"((uint32_t)(sizeof(Tab8) + (bulk ? T : 0)))
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     sbase + 2 * T),
+                 "l"(tabs + tile), "r"((uint32_t)sizeof(Tab8)), "r"(mbar)
+                 : "memory");
+    if (bulk)
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       sbase),
+                   "l"(text + base), "r"((uint32_t)T), "r"(mbar)
+                   : "memory");
   }
   for (int i = tid; i < 256; i += U8_THREADS) s_lut[i] = g_sort_lut.sel[i];
-  if (bulk) {
-    bar_sync(1, U8_THREADS);  // mbarrier initialised
-    mbar_wait(mbar, 0);
-  } else {
+  if (!bulk)
     for (int p = tid; p < T; p += U8_THREADS) smem[p] = p < cnt ? text[base + p] : (uint8_t)0xFF;
-    bar_sync(1, U8_THREADS);
-  }
+  bar_sync(1, U8_THREADS);  // mbarrier initialised, direct staging done
+  mbar_wait(mbar, 0);
   uint8_t* bits8 = reinterpret_cast<uint8_t*>(bits);
 
 #pragma unroll
@@ -411,7 +454,6 @@ __global__ void __launch_bounds__(U8_THREADS + TAB_WARP_THREADS, U8_CTAS_PER_SM)
     bar_sync(1, U8_THREADS);
   }
   bar_sync(1, U8_THREADS);  // every warp's level bits are stored
-  bar_sync(2, ALLT);        // run tables
   // emission of levels 1..W-1: one destination word per task, the runs of all
   // levels flattened (consecutive tasks = consecutive words of one run, so
   // the stores of a warp coalesce); whole words stored, run-edge words OR-ed
@@ -439,9 +481,20 @@ __global__ void __launch_bounds__(U8_THREADS + TAB_WARP_THREADS, U8_CTAS_PER_SM)
 }
 
 template <int W>
-cudaError_t launch_pass8(const Pass8Args& a, cudaStream_t s) {
+cudaError_t launch_pass8(const Pass8Args& a, Tab8* tabs, cudaStream_t s) {
   constexpr int T = U8_THREADS * 16;
-  const size_t smem = 2 * (size_t)T + (size_t)W * (T / 32 + 4) * 4;
+  // per-tile run tables, one warp per tile
+  {
+    constexpr size_t sm = (size_t)T8_WARPS * sizeof(Tables8);
+    static bool set = false;
+    if (!set) {
+      cudaError_t e = cudaFuncSetAttribute(tiles8_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      if (e != cudaSuccess) return e;
+      set = true;
+    }
+    tiles8_kernel<W><<<(unsigned)((a.ntiles + T8_WARPS - 1) / T8_WARPS), T8_WARPS * 32, sm, s>>>(a, tabs);
+  }
+  const size_t smem = 2 * (size_t)T + sizeof(Tab8) + (size_t)W * (T / 32 + 4) * 4;
   auto kern = level_pass8_kernel<W>;
   static bool set = false;
   if (!set) {
@@ -451,7 +504,7 @@ cudaError_t launch_pass8(const Pass8Args& a, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     set = true;
   }
-  kern<<<(unsigned)a.ntiles, U8_THREADS + TAB_WARP_THREADS, smem, s>>>(a);
+  kern<<<(unsigned)a.ntiles, U8_THREADS, smem, s>>>(a, tabs);
   return cudaGetLastError();
 }
 
@@ -474,7 +527,7 @@ cudaError_t launch_hist8(const uint8_t* text, int64_t n, int64_t ntiles, uint32_
 
 // Workspace of the single-pass byte build.
 struct K8Layout {
-  size_t off_tcnt, off_tpre, off_chunk, off_totals, off_base, total;
+  size_t off_tcnt, off_tpre, off_chunk, off_totals, off_base, off_tabs, total;
   int64_t ntiles, nchunks;
 };
 
@@ -502,6 +555,8 @@ inline K8Layout k8_layout(int64_t n, int w) {
   off = align_up(off + (size_t)nb * 8, 256);
   L.off_base = off;
   off = align_up(off + (size_t)8 * 256 * 8, 256);
+  L.off_tabs = off;
+  off = align_up(off + (size_t)L.ntiles * sizeof(Tab8), 256);
   L.total = off + 256;  // + status scratch
   return L;
 }
@@ -558,14 +613,15 @@ int build_k8(const uint8_t* text, int64_t n, int64_t sigma, int w, int kind, uin
   a.tcnt8 = tcnt8;
   a.tpre8 = tpre8;
   a.base = base;
+  Tab8* tabs = (Tab8*)(ws + L.off_tabs);
   switch (w) {
-    case 5: e = launch_pass8<5>(a, s); break;
-    case 6: e = launch_pass8<6>(a, s); break;
-    case 7: e = launch_pass8<7>(a, s); break;
-    default: e = launch_pass8<8>(a, s); break;
+    case 5: e = launch_pass8<5>(a, tabs, s); break;
+    case 6: e = launch_pass8<6>(a, tabs, s); break;
+    case 7: e = launch_pass8<7>(a, tabs, s); break;
+    default: e = launch_pass8<8>(a, tabs, s); break;
   }
   if (e != cudaSuccess) return (int)e;
-  ++g_launches;
+  g_launches += 2;
   prof_mark(s, WVLT_STAGE_PASS0);
   if (pass_done) pass_done(ctx, 0, w);
   return 0;
