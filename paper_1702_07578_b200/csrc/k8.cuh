@@ -163,37 +163,43 @@ __global__ void __launch_bounds__(256) scan8_apply_kernel(const uint32_t* __rest
 // starts in level j (WM: exclusive prefix of the group sizes in LSD-digit
 // order; WT: interval start of the numeric prefix rev(d)).  Also the zero
 // counts per level and (optionally) the histogram.
-__global__ void tables8_kernel(const int64_t* __restrict__ totals, int W, int kind, int64_t* __restrict__ base,
-                               int64_t* __restrict__ zeros, int64_t* __restrict__ hist) {
-  __shared__ int64_t s_cnt[256];
+__global__ void __launch_bounds__(256) tables8_kernel(const int64_t* __restrict__ totals, int W, int kind,
+                                                      int64_t* __restrict__ base, int64_t* __restrict__ zeros,
+                                                      int64_t* __restrict__ hist) {
+  __shared__ int64_t s_tot[256];
+  __shared__ int64_t s_cnt[8][256];
   const int nb = 1 << W;
   const int tid = threadIdx.x;
-  if (hist && tid < nb) hist[tid] = totals[tid];
-  if (tid == 0) {
-    for (int l = 0; l < W; ++l) {
-      int64_t z = 0;
-      for (int e = 0; e < nb; ++e)
-        if (!((e >> (W - 1 - l)) & 1)) z += totals[e];
-      if (zeros) zeros[l] = z;
+  if (tid < nb) {
+    s_tot[tid] = totals[tid];
+    if (hist) hist[tid] = totals[tid];
+  }
+  for (int i = tid; i < 8 * 256; i += 256) s_cnt[i >> 8][i & 255] = 0;
+  __syncthreads();
+  if (tid < W && zeros) {  // thread l: symbols whose level-l bit is 0
+    int64_t z = 0;
+    for (int e = 0; e < nb; ++e)
+      if (!((e >> (W - 1 - tid)) & 1)) z += s_tot[e];
+    zeros[tid] = z;
+  }
+  if (tid >= 32 && tid < 32 + W - 1) {  // thread of level j: its group sizes, then their prefix
+    const int j = tid - 31;
+    const int mj = 1 << j;
+    int64_t* c = s_cnt[j];
+    for (int e = 0; e < nb; ++e) {
+      if (kind == WVLT_KIND_WM) c[rev_bits((unsigned)e, W) & (mj - 1)] += s_tot[e];
+      else c[e >> (W - j)] += s_tot[e];  // numeric j-bit prefix
     }
-    for (int j = 1; j < W; ++j) {
-      const int mj = 1 << j;
-      for (int d = 0; d < mj; ++d) s_cnt[d] = 0;
-      for (int e = 0; e < nb; ++e) {
-        if (kind == WVLT_KIND_WM) s_cnt[rev_bits((unsigned)e, W) & (mj - 1)] += totals[e];
-        else s_cnt[e >> (W - j)] += totals[e];  // numeric j-bit prefix
+    int64_t run = 0;
+    if (kind == WVLT_KIND_WM) {
+      for (int d = 0; d < mj; ++d) {
+        base[j * 256 + d] = run;
+        run += c[d];
       }
-      int64_t run = 0;
-      if (kind == WVLT_KIND_WM) {
-        for (int d = 0; d < mj; ++d) {
-          base[j * 256 + d] = run;
-          run += s_cnt[d];
-        }
-      } else {
-        for (int P = 0; P < mj; ++P) {
-          base[j * 256 + rev_bits((unsigned)P, j)] = run;
-          run += s_cnt[P];
-        }
+    } else {
+      for (int P = 0; P < mj; ++P) {
+        base[j * 256 + rev_bits((unsigned)P, j)] = run;
+        run += c[P];
       }
     }
   }
@@ -210,32 +216,29 @@ struct Pass8Args {
 };
 
 // Runs of levels 1..W-1 flattened: run r = 2^j - 2 + d (j = level, d = LSD digit).
+// (positions fit 32 bits: the single-pass path needs n < 2^32)
 struct Tables8 {
-  int cnt[256];       // run sizes
-  int ls[256];        // run starts in the tile-local order of its level
-  int64_t gs[256];    // run starts in the global level
-  int64_t lb[256];    // symbols of earlier tiles in the run's group (scratch)
-  int wpre[256];      // emission: destination words before each run (+ total)
-  int cW[256];        // level-W digit counts (scratch)
+  uint16_t cnt[256];  // run sizes
+  uint16_t ls[256];   // run starts in the tile-local order of its level
+  uint32_t gs[256];   // run starts in the global level
+  uint32_t lb[256];   // symbols of earlier tiles in the run's group (scratch)
+  uint16_t wpre[256]; // emission: destination words before each run (+ total)
+  uint16_t cW[256];   // level-W digit counts (scratch)
   uint32_t lbW[256];  // level-W tile prefixes (scratch)
-  int64_t base[256];  // global group starts of every run (copy of Pass8Args::base)
 };
 
 template <int W>
-__device__ __forceinline__ void table8_warp(const Pass8Args& a, Tables8& tt, int64_t tile, int lane, int allt) {
+__device__ __forceinline__ void table8_warp(const Pass8Args& a, Tables8& tt, const uint32_t* s_base, int64_t tile,
+                                            int lane, int allt) {
   constexpr int NB = 1 << W;
   constexpr int NR = NB - 2;
   const uint32_t* cr = a.tcnt8 + tile * NB;
   const uint32_t* pr = a.tpre8 + tile * NB;
-  // every global input up front: one round trip instead of one per level
+  // every global input up front: one round trip
   for (int e = lane; e < NB; e += 32) {
     const int d = (int)rev_bits((unsigned)e, W);
-    tt.cW[d] = (int)__ldg(cr + e);
+    tt.cW[d] = (uint16_t)__ldg(cr + e);
     tt.lbW[d] = __ldg(pr + e);
-  }
-  for (int r = lane; r < NR; r += 32) {
-    const int j = 31 - __clz(r + 2);
-    tt.base[r] = __ldg(a.base + j * 256 + (r + 2 - (1 << j)));
   }
   __syncwarp();
   // fold: level j's digit d collects the level j+1 digits d and d + 2^j
@@ -244,19 +247,19 @@ __device__ __forceinline__ void table8_warp(const Pass8Args& a, Tables8& tt, int
     const int mj = 1 << j;
     for (int d = lane; d < mj; d += 32) {
       int c;
-      int64_t lb;
+      uint32_t lb;
       if (j == W - 1) {
         c = tt.cW[d] + tt.cW[d + mj];
-        lb = (int64_t)tt.lbW[d] + (int64_t)tt.lbW[d + mj];
+        lb = tt.lbW[d] + tt.lbW[d + mj];
       } else {
         const int up = (2 << j) - 2;
         c = tt.cnt[up + d] + tt.cnt[up + d + mj];
         lb = tt.lb[up + d] + tt.lb[up + d + mj];
       }
       const int r = mj - 2 + d;
-      tt.cnt[r] = c;
+      tt.cnt[r] = (uint16_t)c;
       tt.lb[r] = lb;
-      tt.gs[r] = tt.base[r] + lb;
+      tt.gs[r] = s_base[r] + lb;
     }
     __syncwarp();
   }
@@ -275,7 +278,7 @@ __device__ __forceinline__ void table8_warp(const Pass8Args& a, Tables8& tt, int
     for (int k = 0; k < per; ++k) {
       const int d = lane * per + k;
       if (d < mj) {
-        tt.ls[r0 + d] = run;
+        tt.ls[r0 + d] = (uint16_t)run;
         run += tt.cnt[r0 + d];
       }
     }
@@ -304,10 +307,10 @@ __device__ __forceinline__ void table8_warp(const Pass8Args& a, Tables8& tt, int
 #pragma unroll
     for (int k = 0; k < per; ++k) {
       const int r = lane * per + k;
-      if (r < NR) tt.wpre[r] = run;
+      if (r < NR) tt.wpre[r] = (uint16_t)run;
       run += nw[k];
     }
-    if (lane == 31) tt.wpre[NR] = run;
+    if (lane == 31) tt.wpre[NR] = (uint16_t)run;
   }
   if (allt > 0) {
     __threadfence_block();
@@ -326,25 +329,32 @@ struct Tab8 {
 };
 static_assert(sizeof(Tab8) % 16 == 0, "bulk-copy granularity");
 
-constexpr int T8_WARPS = 4;
+constexpr int T8_WARPS = 8;
 
 // One warp per tile: the tile's run tables (table8_warp) into the compact
 // global layout, off the pass kernel's critical path.
 template <int W>
 __global__ void __launch_bounds__(T8_WARPS * 32) tiles8_kernel(const Pass8Args a, Tab8* __restrict__ out) {
+  constexpr int NR = (1 << W) - 2;
   extern __shared__ __align__(16) unsigned char t8_smem[];
+  __shared__ uint32_t s_base[256];  // global group starts of every run
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int r = threadIdx.x; r < NR; r += T8_WARPS * 32) {
+    const int j = 31 - __clz(r + 2);
+    s_base[r] = (uint32_t)__ldg(a.base + j * 256 + (r + 2 - (1 << j)));
+  }
+  __syncthreads();
   Tables8& tt = reinterpret_cast<Tables8*>(t8_smem)[wid];
   const int64_t tile = (int64_t)blockIdx.x * T8_WARPS + wid;
   if (tile >= a.ntiles) return;
-  table8_warp<W>(a, tt, tile, lane, 0);
+  table8_warp<W>(a, tt, s_base, tile, lane, 0);
   __syncwarp();
   Tab8* o = out + tile;
   for (int r = lane; r < 256; r += 32) {
-    o->gs[r] = (uint32_t)tt.gs[r];
-    o->cnt[r] = (uint16_t)tt.cnt[r];
-    o->ls[r] = (uint16_t)tt.ls[r];
-    o->wpre[r] = (uint16_t)tt.wpre[r];
+    o->gs[r] = tt.gs[r];
+    o->cnt[r] = tt.cnt[r];
+    o->ls[r] = tt.ls[r];
+    o->wpre[r] = tt.wpre[r];
   }
 }
 
