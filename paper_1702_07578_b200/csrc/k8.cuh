@@ -453,6 +453,22 @@ __global__ void __launch_bounds__(U8_THREADS, U8_K8_CTAS) level_pass8_kernel(con
       const int nz = 8 - (int)(hh ? ones1 : ones0);
       const uint32_t za = opaque(nxt + (uint32_t)ZB[hh]);
       const uint32_t oa = opaque(nxt + (uint32_t)(OB[hh] + 1 - nz));
+#ifndef K8_SEL_ADDR
+      // address selection mostly off the integer ALU pipe (its bound): the
+      // carry of (15 - nz) 2^28 + (kk + 1) 2^28 out of 32 bits is [kk >= nz],
+      // read as the high word of one mad.wide; then addr = za + flag (oa - za)
+      const uint32_t F = (uint32_t)(15 - nz) << 28;
+      const uint32_t dz = oa - za;
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        const uint32_t v = sv[kk >> 2];
+        const uint32_t vb = (kk & 3) == 0 ? v : (kk & 3) == 1 ? shr_mul<8>(v) : (kk & 3) == 2 ? shr_mul<16>(v) : shr_mul<24>(v);
+        uint64_t t;
+        asm("mad.wide.u32 %0, %1, 1, %2;" : "=l"(t) : "r"(F), "l"((uint64_t)(kk + 1) << 28));
+        const uint32_t addr = za + (uint32_t)(t >> 32) * dz + kk;
+        asm volatile("st.shared.u8 [%0], %1;" ::"r"(addr), "r"(vb) : "memory");
+      }
+#else
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk) {
         const uint32_t v = sv[kk >> 2];
@@ -460,6 +476,7 @@ __global__ void __launch_bounds__(U8_THREADS, U8_K8_CTAS) level_pass8_kernel(con
         const uint32_t addr = (kk < nz ? za : oa) + kk;
         asm volatile("st.shared.u8 [%0], %1;" ::"r"(addr), "r"(vb) : "memory");
       }
+#endif
     }
     bar_sync(1, U8_THREADS);
   }
