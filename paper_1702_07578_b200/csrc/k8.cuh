@@ -71,11 +71,17 @@ __global__ void __launch_bounds__(H8_WARPS * 32) hist8_kernel(const uint8_t* __r
     __syncwarp();
     // row p (bins p, p + HALF) summed over the 32 lane columns; lane l takes rows
     // l, l + 32, ...; skewed reads keep the 32 lanes on distinct banks
+    // (16-byte reads: lane l takes chunk k ^ (l & 7) of its row, so the 8
+    // lanes of a wavefront hit 8 different bank quads)
     uint32_t* row_out = tcnt8 + t * NB;
     for (int p = lane; p < HALF; p += 32) {
+      const uint4* row = reinterpret_cast<const uint4*>(c32 + p * 32);
       uint32_t s = 0;
-#pragma unroll 8
-      for (int k = 0; k < 32; ++k) s += c32[p * 32 + ((k + lane) & 31)];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint4 q = row[k ^ (lane & 7)];
+        s += (q.x + q.y) + (q.z + q.w);
+      }
       row_out[p] = s & 0xFFFFu;
       row_out[p + HALF] = s >> 16;
     }
