@@ -491,19 +491,24 @@ __global__ void __launch_bounds__(U8_THREADS, U8_K8_CTAS) level_pass8_kernel(con
   // levels flattened (consecutive tasks = consecutive words of one run, so
   // the stores of a warp coalesce); whole words stored, run-edge words OR-ed
   // (runs of neighbouring tiles share them; the levels were zeroed)
+#ifdef K8_NO_EMIT
+  const int total = 0;
+#else
   const int total = tt.wpre[NR];
+#endif
   for (int q = tid; q < total; q += U8_THREADS) {
     int r = 0;  // last run with wpre[r] <= q (empty runs share prefix values)
 #pragma unroll
     for (int s = 128; s >= 1; s >>= 1)
       if (r + s < NR && tt.wpre[r + s] <= q) r += s;
     const int j = 31 - __clz(r + 2);
-    const int64_t g = tt.gs[r];
-    const int c = tt.cnt[r];
-    const int64_t wd = (g >> 6) + (q - tt.wpre[r]);
-    const int64_t wb = wd << 6;
-    const int64_t lo = g > wb ? g : wb;
-    const int64_t hi = (g + c) < wb + 64 ? (g + c) : wb + 64;
+    // 32-bit bit positions: the single-pass path keeps n < 2^32 - 64
+    const uint32_t g = tt.gs[r];
+    const uint32_t c = tt.cnt[r];
+    const uint32_t wd = (g >> 6) + (uint32_t)(q - tt.wpre[r]);
+    const uint32_t wb = wd << 6;
+    const uint32_t lo = g > wb ? g : wb;
+    const uint32_t hi = (g + c) < wb + 64 ? (g + c) : wb + 64;
     const int len = (int)(hi - lo);
     const uint32_t* L = bits + j * (NC + 4);
     const uint64_t v = extract_bits(L, tt.ls[r] + (int)(lo - g), len) << (lo - wb);
@@ -568,7 +573,7 @@ inline bool k8_eligible(int sym_bytes, int w, int64_t n) {
 #ifdef WVLT_NO_K8
   return false;
 #else
-  return sym_bytes == 1 && w >= 5 && w <= 8 && n > 0 && n < (1ll << 32);
+  return sym_bytes == 1 && w >= 5 && w <= 8 && n > 0 && n < (1ll << 32) - 64;
 #endif
 }
 
