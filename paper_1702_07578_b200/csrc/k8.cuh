@@ -616,7 +616,9 @@ int build_k8(const uint8_t* text, int64_t n, int64_t sigma, int w, int kind, uin
   cudaError_t e;
   g_prof.n = 0;
   prof_mark(s, -1);
-  e = cudaMemsetAsync(level_words, 0, (size_t)w * nwords * 8, s);
+  // level 0 is written whole (every byte of its words) by the pass; the
+  // other levels' run-edge words are OR-ed and need zeros
+  e = cudaMemsetAsync(level_words + nwords, 0, (size_t)(w - 1) * nwords * 8, s);
   if (e != cudaSuccess) return (int)e;
   if (!status) {
     e = cudaMemsetAsync(st_flag, 0, 4, s);
