@@ -518,20 +518,23 @@ __global__ void __launch_bounds__(U8_THREADS, U8_K8_CTAS) level_pass8_kernel(con
   }
 }
 
+// per-tile run tables, one warp per tile
+template <int W>
+cudaError_t launch_tiles8(const Pass8Args& a, Tab8* tabs, cudaStream_t s) {
+  constexpr size_t sm = (size_t)T8_WARPS * sizeof(Tables8);
+  static bool set = false;
+  if (!set) {
+    cudaError_t e = cudaFuncSetAttribute(tiles8_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    set = true;
+  }
+  tiles8_kernel<W><<<(unsigned)((a.ntiles + T8_WARPS - 1) / T8_WARPS), T8_WARPS * 32, sm, s>>>(a, tabs);
+  return cudaGetLastError();
+}
+
 template <int W>
 cudaError_t launch_pass8(const Pass8Args& a, Tab8* tabs, cudaStream_t s) {
   constexpr int T = U8_THREADS * 16;
-  // per-tile run tables, one warp per tile
-  {
-    constexpr size_t sm = (size_t)T8_WARPS * sizeof(Tables8);
-    static bool set = false;
-    if (!set) {
-      cudaError_t e = cudaFuncSetAttribute(tiles8_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      if (e != cudaSuccess) return e;
-      set = true;
-    }
-    tiles8_kernel<W><<<(unsigned)((a.ntiles + T8_WARPS - 1) / T8_WARPS), T8_WARPS * 32, sm, s>>>(a, tabs);
-  }
   const size_t smem = 2 * (size_t)T + sizeof(Tab8) + (size_t)W * (T / 32 + 4) * 4;
   auto kern = level_pass8_kernel<W>;
   static bool set = false;
@@ -639,11 +642,12 @@ int build_k8(const uint8_t* text, int64_t n, int64_t sigma, int w, int kind, uin
   scan8_chunks_kernel<<<(unsigned)L.nchunks, nb, 0, s>>>(tcnt8, L.ntiles, nb, chunk);
   scan8_carry_kernel<<<nb, S8_SCAN_THREADS, 0, s>>>(chunk, L.nchunks, nb, totals);
   scan8_apply_kernel<<<(unsigned)L.nchunks, nb, 0, s>>>(tcnt8, L.ntiles, nb, chunk, tpre8);
-  tables8_kernel<<<1, 256, 0, s>>>(totals, w, kind, base, zeros, hist);
-  g_launches += 4;
+  g_launches += 3;
   e = cudaGetLastError();
   if (e != cudaSuccess) return (int)e;
   prof_mark(s, WVLT_STAGE_SCAN0);
+  tables8_kernel<<<1, 256, 0, s>>>(totals, w, kind, base, zeros, hist);
+  ++g_launches;
   Pass8Args a;
   a.src = text;
   a.words = level_words;
@@ -655,13 +659,22 @@ int build_k8(const uint8_t* text, int64_t n, int64_t sigma, int w, int kind, uin
   a.base = base;
   Tab8* tabs = (Tab8*)(ws + L.off_tabs);
   switch (w) {
+    case 5: e = launch_tiles8<5>(a, tabs, s); break;
+    case 6: e = launch_tiles8<6>(a, tabs, s); break;
+    case 7: e = launch_tiles8<7>(a, tabs, s); break;
+    default: e = launch_tiles8<8>(a, tabs, s); break;
+  }
+  if (e != cudaSuccess) return (int)e;
+  ++g_launches;
+  prof_mark(s, WVLT_STAGE_TABLES);
+  switch (w) {
     case 5: e = launch_pass8<5>(a, tabs, s); break;
     case 6: e = launch_pass8<6>(a, tabs, s); break;
     case 7: e = launch_pass8<7>(a, tabs, s); break;
     default: e = launch_pass8<8>(a, tabs, s); break;
   }
   if (e != cudaSuccess) return (int)e;
-  g_launches += 2;
+  ++g_launches;
   prof_mark(s, WVLT_STAGE_PASS0);
   if (pass_done) pass_done(ctx, 0, w);
   return 0;

@@ -20,7 +20,9 @@ out.mkdir(exist_ok=True)
 
 
 def short(name):
-    for k in ("hist_u8_kernel", "hist_generic_kernel", "digits_fast_kernel", "digits_kernel", "wm_pass_tables_kernel", "tables_kernel", "scan_reduce_kernel",
+    for k in ("hist8_kernel", "tiles8_kernel", "level_pass8_kernel", "scan8_chunks_kernel", "scan8_carry_kernel",
+              "scan8_apply_kernel", "tables8_kernel",
+              "hist_u8_kernel", "hist_generic_kernel", "digits_fast_kernel", "digits_kernel", "wm_pass_tables_kernel", "tables_kernel", "scan_reduce_kernel",
               "scan_apply_kernel", "level_pass_u8_kernel", "level_pass_kernel", "merge_bits_kernel", "widen_kernel"):
         i = name.find(k)
         if i >= 0:
@@ -97,6 +99,8 @@ for r in full:
         pass_idx += 1
     elif "hist" in name or "digits" in name:
         traffic["hist"] = (rd + wr) * 1e6
+    elif "tiles8" in name:
+        traffic["tiles8"] = (rd + wr) * 1e6
 (out / f"{tag}_summary.md").write_text("\n".join(lines) + "\n")
 json.dump(traffic, open(out / "ncu_traffic_c2_wm.json", "w"), indent=1)
 print("\n".join(lines))
