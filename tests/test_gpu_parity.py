@@ -45,7 +45,7 @@ def test_running_example():
 
 
 @pytest.mark.parametrize("kind", ["wt", "wm"])
-@pytest.mark.parametrize("sigma", SIGMA_GRID + (4, 256, 1000, 1 << 16, 1 << 20))
+@pytest.mark.parametrize("sigma", SIGMA_GRID + (4, 17, 33, 100, 256, 1000, 1 << 16, 1 << 20))
 def test_tile_boundaries_vs_oracle(kind, sigma):
     rng = np.random.default_rng(sigma * 7 + (kind == "wm"))
     for n in (1, 31, 32, 33, 63, 64, 65, 4095, 4096, 4097, 8191, 8192, 8193, 16383, 16384, 16385, 40961,
@@ -191,3 +191,24 @@ def test_sharded_build_world1_nccl_matches_single_build(rng):
                 assert list(res.zeros) == zeros
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("sigma", [17, 100, 200, 256, 1000])
+def test_unaligned_device_text(sigma):
+    """A device text that does not start on a 16-byte boundary: the staging and
+    counting kernels take their element-wise paths (single-pass byte kernels
+    included), with identical output."""
+    from paper_1702_07578_b200.device import DeviceBuilder
+
+    rng = np.random.default_rng(sigma)
+    n = 3 * 8192 + 777
+    base = random_text(rng, n + 1, sigma)
+    dev = torch.from_numpy(base).cuda()[1:]  # offset by one element
+    assert dev.data_ptr() % 16 != 0
+    b = DeviceBuilder()
+    for kind in ("wt", "wm"):
+        words, zeros, _ = b.build(dev, sigma, kind).to_host()
+        ow, oz, _ = oracle.build(base[1:], sigma, kind, "pc")
+        assert np.array_equal(words, ow), kind
+        if kind == "wm":
+            assert zeros == oz
