@@ -20,10 +20,12 @@ namespace {
 // hist_u8_kernel, zeroed after every tile so the per-tile row sums never carry.
 constexpr int H8_WARPS = 4;
 
+// It also writes level 0 (the top code bit of every symbol, already in text
+// order), so that level can leave for the host while the rest is built.
 template <int W>
 __global__ void __launch_bounds__(H8_WARPS * 32) hist8_kernel(const uint8_t* __restrict__ text, int64_t n,
                                                              int64_t ntiles, uint32_t vmax_ok, int check,
-                                                             uint32_t* __restrict__ tcnt8,
+                                                             uint32_t* __restrict__ tcnt8, uint64_t* __restrict__ level0,
                                                              int32_t* __restrict__ status) {
   constexpr int NB = 1 << W;
   constexpr int HALF = NB / 2;
@@ -50,23 +52,39 @@ __global__ void __launch_bounds__(H8_WARPS * 32) hist8_kernel(const uint8_t* __r
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           const uint32_t wd[4] = {q[k].x, q[k].y, q[k].z, q[k].w};
+          uint32_t m16 = 0;  // level-0 bits of this lane's 16 symbols
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             if (check) vmax = __vmaxu4(vmax, wd[u]);
             const uint32_t lo = wd[u] & ((uint32_t)(HALF - 1) * 0x01010101u);
             const uint32_t hb = (wd[u] >> (W - 1)) & 0x01010101u;
+            m16 |= ((hb * 0x01020408u) >> 24) << (4 * u);
 #pragma unroll
             for (int b = 0; b < 4; ++b)
               atomicAdd(c32w + prmt(lo, 0, 0x4440 + b) * 32, prmt(hb, 0, 0x4440 + b) * 0xFFFFu + 1u);
           }
+          // lanes 4i..4i+3 hold 64 consecutive symbols: one level-0 word
+          const uint32_t m32 = m16 | (__shfl_down_sync(FULL, m16, 1) << 16);
+          const uint32_t hi32 = __shfl_down_sync(FULL, m32, 2);
+          if ((lane & 3) == 0)
+            level0[(first >> 6) + ((k0 + k) * 32 + lane) / 4] = (uint64_t)m32 | ((uint64_t)hi32 << 32);
         }
       }
     } else {
-      for (int i = lane; i < cnt; i += 32) {
-        const uint32_t v = text[first + i];
-        vmax = max(vmax, v);
-        atomicAdd(c32w + (v & (HALF - 1)) * 32, ((v >> (W - 1)) & 1u) ? 0x10000u : 1u);
+      uint32_t* l0 = reinterpret_cast<uint32_t*>(level0) + (first >> 5);
+      for (int i0 = 0; i0 < cnt; i0 += 32) {
+        const int i = i0 + lane;
+        uint32_t v = 0;
+        if (i < cnt) {
+          v = text[first + i];
+          vmax = max(vmax, v);
+          atomicAdd(c32w + (v & (HALF - 1)) * 32, ((v >> (W - 1)) & 1u) ? 0x10000u : 1u);
+        }
+        const uint32_t b = __ballot_sync(FULL, i < cnt && ((v >> (W - 1)) & 1u));
+        if (lane == 0) l0[i0 >> 5] = b;
       }
+      // a tail tile ending inside a 64-bit word: zero its upper half
+      if (lane == 0 && (((first + cnt + 31) >> 5) & 1)) l0[(cnt + 31) >> 5] = 0u;
     }
     __syncwarp();
     // row p (bins p, p + HALF) summed over the 32 lane columns; lane l takes rows
@@ -425,14 +443,7 @@ __global__ void __launch_bounds__(U8_THREADS, U8_K8_CTAS) level_pass8_kernel(con
     const uint32_t m0 = ((b[1] * 16u + b[0]) * 0x01020408u) >> 24;
     const uint32_t m1 = ((b[3] * 16u + b[2]) * 0x01020408u) >> 24;
     const uint32_t ones0 = __popc(m0), ones1 = __popc(m1);
-    if (j == 0) {
-      uint8_t* g8 = reinterpret_cast<uint8_t*>(a.words) + (base >> 3);
-      const int64_t lim = 8 * a.nwords - (base >> 3);
-      const int f0 = 8 * tid, f1 = H + 8 * tid;
-      if (tid < lim) g8[tid] = (uint8_t)(f0 + 8 <= cnt ? m0 : (f0 >= cnt ? 0u : (m0 & ((1u << (cnt - f0)) - 1u))));
-      if (H / 8 + tid < lim)
-        g8[H / 8 + tid] = (uint8_t)(f1 + 8 <= cnt ? m1 : (f1 >= cnt ? 0u : (m1 & ((1u << (cnt - f1)) - 1u))));
-    } else {
+    if (j > 0) {  // level 0 was written by hist8_kernel
       bits8[j * 4 * (NC + 4) + tid] = (uint8_t)m0;
       bits8[j * 4 * (NC + 4) + H / 8 + tid] = (uint8_t)m1;
     }
@@ -551,7 +562,7 @@ cudaError_t launch_pass8(const Pass8Args& a, Tab8* tabs, cudaStream_t s) {
 
 template <int W>
 cudaError_t launch_hist8(const uint8_t* text, int64_t n, int64_t ntiles, uint32_t vmax_ok, int check,
-                         uint32_t* tcnt8, int32_t* status, cudaStream_t s) {
+                         uint32_t* tcnt8, uint64_t* level0, int32_t* status, cudaStream_t s) {
   constexpr size_t sb = (size_t)H8_WARPS * (1 << (W - 1)) * 32 * 4;
   static bool set = false;
   if (!set) {
@@ -562,7 +573,8 @@ cudaError_t launch_hist8(const uint8_t* text, int64_t n, int64_t ntiles, uint32_
   const int per_sm = (int)std::min<size_t>(8, (size_t)(220 * 1024) / (sb + 1024));
   const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((ntiles + H8_WARPS - 1) / H8_WARPS,
                                                                  (int64_t)sm_count() * per_sm));
-  hist8_kernel<W><<<(unsigned)blocks, H8_WARPS * 32, sb, s>>>(text, n, ntiles, vmax_ok, check, tcnt8, status);
+  hist8_kernel<W><<<(unsigned)blocks, H8_WARPS * 32, sb, s>>>(text, n, ntiles, vmax_ok, check, tcnt8, level0,
+                                                              status);
   return cudaGetLastError();
 }
 
@@ -619,8 +631,8 @@ int build_k8(const uint8_t* text, int64_t n, int64_t sigma, int w, int kind, uin
   cudaError_t e;
   g_prof.n = 0;
   prof_mark(s, -1);
-  // level 0 is written whole (every byte of its words) by the pass; the
-  // other levels' run-edge words are OR-ed and need zeros
+  // level 0 is written whole (every word) by hist8_kernel; the other
+  // levels' run-edge words are OR-ed and need zeros
   e = cudaMemsetAsync(level_words + nwords, 0, (size_t)(w - 1) * nwords * 8, s);
   if (e != cudaSuccess) return (int)e;
   if (!status) {
@@ -631,14 +643,15 @@ int build_k8(const uint8_t* text, int64_t n, int64_t sigma, int w, int kind, uin
   const uint32_t vmax_ok = (uint32_t)std::min<int64_t>(sigma - 1, 255);
   const int check = vmax_ok < 255 ? 1 : 0;
   switch (w) {
-    case 5: e = launch_hist8<5>(text, n, L.ntiles, vmax_ok, check, tcnt8, st_flag, s); break;
-    case 6: e = launch_hist8<6>(text, n, L.ntiles, vmax_ok, check, tcnt8, st_flag, s); break;
-    case 7: e = launch_hist8<7>(text, n, L.ntiles, vmax_ok, check, tcnt8, st_flag, s); break;
-    default: e = launch_hist8<8>(text, n, L.ntiles, vmax_ok, check, tcnt8, st_flag, s); break;
+    case 5: e = launch_hist8<5>(text, n, L.ntiles, vmax_ok, check, tcnt8, level_words, st_flag, s); break;
+    case 6: e = launch_hist8<6>(text, n, L.ntiles, vmax_ok, check, tcnt8, level_words, st_flag, s); break;
+    case 7: e = launch_hist8<7>(text, n, L.ntiles, vmax_ok, check, tcnt8, level_words, st_flag, s); break;
+    default: e = launch_hist8<8>(text, n, L.ntiles, vmax_ok, check, tcnt8, level_words, st_flag, s); break;
   }
   if (e != cudaSuccess) return (int)e;
   ++g_launches;
   prof_mark(s, WVLT_STAGE_HIST);
+  if (pass_done) pass_done(ctx, 0, 1);  // level 0 is final: it may leave now
   scan8_chunks_kernel<<<(unsigned)L.nchunks, nb, 0, s>>>(tcnt8, L.ntiles, nb, chunk);
   scan8_carry_kernel<<<nb, S8_SCAN_THREADS, 0, s>>>(chunk, L.nchunks, nb, totals);
   scan8_apply_kernel<<<(unsigned)L.nchunks, nb, 0, s>>>(tcnt8, L.ntiles, nb, chunk, tpre8);
@@ -676,7 +689,7 @@ int build_k8(const uint8_t* text, int64_t n, int64_t sigma, int w, int kind, uin
   if (e != cudaSuccess) return (int)e;
   ++g_launches;
   prof_mark(s, WVLT_STAGE_PASS0);
-  if (pass_done) pass_done(ctx, 0, w);
+  if (pass_done) pass_done(ctx, 1, w - 1);
   return 0;
 }
 
