@@ -251,20 +251,60 @@ struct Tables8 {
   uint32_t lbW[256];  // level-W tile prefixes (scratch)
 };
 
+// a tile's count / prefix row into registers (entry e = lane + 32 k)
+template <int W>
+__device__ __forceinline__ void table8_load(const Pass8Args& a, int64_t tile, int lane, uint32_t (&rc)[8],
+                                            uint32_t (&rp)[8]) {
+  constexpr int NB = 1 << W;
+  const uint32_t* cr = a.tcnt8 + tile * NB;
+  const uint32_t* pr = a.tpre8 + tile * NB;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int e = lane + 32 * k;
+    rc[k] = e < NB ? __ldcs(cr + e) : 0u;
+    rp[k] = e < NB ? __ldcs(pr + e) : 0u;
+  }
+}
+
+// ... and into the scratch in LSD-digit order
+template <int W>
+__device__ __forceinline__ void table8_stage(Tables8& tt, int lane, const uint32_t (&rc)[8], const uint32_t (&rp)[8]) {
+  constexpr int NB = 1 << W;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int e = lane + 32 * k;
+    if (e < NB) {
+      const int d = (int)rev_bits((unsigned)e, W);
+      tt.cW[d] = (uint16_t)rc[k];
+      tt.lbW[d] = rp[k];
+    }
+  }
+  __syncwarp();
+}
+
+template <int W>
+__device__ __forceinline__ void table8_compute(Tables8& tt, const uint32_t* s_base, int lane);
+
 template <int W>
 __device__ __forceinline__ void table8_warp(const Pass8Args& a, Tables8& tt, const uint32_t* s_base, int64_t tile,
                                             int lane, int allt) {
   constexpr int NB = 1 << W;
   constexpr int NR = NB - 2;
-  const uint32_t* cr = a.tcnt8 + tile * NB;
-  const uint32_t* pr = a.tpre8 + tile * NB;
-  // every global input up front: one round trip
-  for (int e = lane; e < NB; e += 32) {
-    const int d = (int)rev_bits((unsigned)e, W);
-    tt.cW[d] = (uint16_t)__ldg(cr + e);
-    tt.lbW[d] = __ldg(pr + e);
+  uint32_t rc[8], rp[8];
+  table8_load<W>(a, tile, lane, rc, rp);
+  table8_stage<W>(tt, lane, rc, rp);
+  table8_compute<W>(tt, s_base, lane);
+  if (allt > 0) {
+    __threadfence_block();
+    bar_arrive(2, allt);
   }
-  __syncwarp();
+}
+
+template <int W>
+__device__ __forceinline__ void table8_compute(Tables8& tt, const uint32_t* s_base, int lane) {
+  constexpr int NB = 1 << W;
+  constexpr int NR = NB - 2;
+
   // fold: level j's digit d collects the level j+1 digits d and d + 2^j
 #pragma unroll 1
   for (int j = W - 1; j >= 1; --j) {
@@ -336,10 +376,6 @@ __device__ __forceinline__ void table8_warp(const Pass8Args& a, Tables8& tt, con
     }
     if (lane == 31) tt.wpre[NR] = (uint16_t)run;
   }
-  if (allt > 0) {
-    __threadfence_block();
-    bar_arrive(2, allt);
-  }
 }
 
 // Compact per-tile run table written by tiles8_kernel and bulk-copied into
@@ -369,16 +405,24 @@ __global__ void __launch_bounds__(T8_WARPS * 32) tiles8_kernel(const Pass8Args a
   }
   __syncthreads();
   Tables8& tt = reinterpret_cast<Tables8*>(t8_smem)[wid];
-  const int64_t tile = (int64_t)blockIdx.x * T8_WARPS + wid;
+  const int64_t nw = (int64_t)gridDim.x * T8_WARPS;
+  int64_t tile = (int64_t)blockIdx.x * T8_WARPS + wid;
   if (tile >= a.ntiles) return;
-  table8_warp<W>(a, tt, s_base, tile, lane, 0);
-  __syncwarp();
-  Tab8* o = out + tile;
-  for (int r = lane; r < 256; r += 32) {
-    o->gs[r] = tt.gs[r];
-    o->cnt[r] = tt.cnt[r];
-    o->ls[r] = tt.ls[r];
-    o->wpre[r] = tt.wpre[r];
+  uint32_t rc[8], rp[8];
+  table8_load<W>(a, tile, lane, rc, rp);
+  for (; tile < a.ntiles; tile += nw) {
+    table8_stage<W>(tt, lane, rc, rp);
+    if (tile + nw < a.ntiles) table8_load<W>(a, tile + nw, lane, rc, rp);  // next row in flight
+    table8_compute<W>(tt, s_base, lane);
+    __syncwarp();
+    Tab8* o = out + tile;
+    for (int r = lane; r < 256; r += 32) {
+      o->gs[r] = tt.gs[r];
+      o->cnt[r] = tt.cnt[r];
+      o->ls[r] = tt.ls[r];
+      o->wpre[r] = tt.wpre[r];
+    }
+    __syncwarp();
   }
 }
 
@@ -539,7 +583,8 @@ cudaError_t launch_tiles8(const Pass8Args& a, Tab8* tabs, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     set = true;
   }
-  tiles8_kernel<W><<<(unsigned)((a.ntiles + T8_WARPS - 1) / T8_WARPS), T8_WARPS * 32, sm, s>>>(a, tabs);
+  const int64_t blocks = std::min<int64_t>((a.ntiles + T8_WARPS - 1) / T8_WARPS, (int64_t)sm_count() * 4);
+  tiles8_kernel<W><<<(unsigned)blocks, T8_WARPS * 32, sm, s>>>(a, tabs);
   return cudaGetLastError();
 }
 
