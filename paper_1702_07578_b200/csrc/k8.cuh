@@ -426,19 +426,34 @@ __global__ void __launch_bounds__(T8_WARPS * 32) tiles8_kernel(const Pass8Args a
   }
 }
 
-template <int W>
-__global__ void __launch_bounds__(U8_THREADS, U8_K8_CTAS) level_pass8_kernel(const Pass8Args a, const Tab8* __restrict__ tabs) {
-  constexpr int T = U8_THREADS * 16;
-  constexpr int H = T / 2;
+// Threads of the pass kernel: Q 8-symbol runs ("quarters") per thread, the
+// tile split into Q regions of T / Q symbols (run k of thread t covers
+// [k T/Q + 8 t, k T/Q + 8 t + 8)).  More runs per thread amortize the scan.
+#ifndef K8_Q
+#define K8_Q 4
+#endif
+constexpr int K8_TILE = 8192;
+template <int Q>
+struct K8Cfg {
+  static constexpr int NT = K8_TILE / (8 * Q);
+  static constexpr int CTAS = Q == 2 ? 4 : Q == 4 ? 7 : 8;
+};
+
+template <int W, int Q>
+__global__ void __launch_bounds__(K8Cfg<Q>::NT, K8Cfg<Q>::CTAS) level_pass8_kernel(const Pass8Args a, const Tab8* __restrict__ tabs) {
+  constexpr int T = K8_TILE;
+  constexpr int NT = K8Cfg<Q>::NT;
+  constexpr int R = T / Q;  // region of run k
   constexpr int NC = T / 32;
-  constexpr int NW = U8_THREADS / 32;
+  constexpr int NW = NT / 32;
   constexpr int NR = (1 << W) - 2;
+  constexpr int P = Q / 2;  // packed 16|16 scan values
   constexpr uint32_t B1 = 0x01010101u;
   extern __shared__ __align__(128) unsigned char smem[];
   // [stage | ping-pong order buffer | run table | level bits of levels 1..W-1]
   Tab8& tt = *reinterpret_cast<Tab8*>(smem + 2 * T);
-  uint32_t* bits = reinterpret_cast<uint32_t*>(smem + 2 * T + sizeof(Tab8));
-  __shared__ __align__(16) uint32_t s_wtot[2][NW];
+  uint32_t* bits = reinterpret_cast<uint32_t*>(smem + 2 * T + sizeof(Tab8)) - (NC + 4);  // level j at j (NC+4)
+  __shared__ __align__(16) uint32_t s_wtot[2][P][NW];
   __shared__ uint32_t s_lut[256];
   __shared__ __align__(8) uint64_t s_mbar;
 
@@ -467,10 +482,10 @@ __global__ void __launch_bounds__(U8_THREADS, U8_K8_CTAS) level_pass8_kernel(con
                    "l"(text + base), "r"((uint32_t)T), "r"(mbar)
                    : "memory");
   }
-  for (int i = tid; i < 256; i += U8_THREADS) s_lut[i] = g_sort_lut.sel[i];
+  for (int i = tid; i < 256; i += NT) s_lut[i] = g_sort_lut.sel[i];
   if (!bulk)
-    for (int p = tid; p < T; p += U8_THREADS) smem[p] = p < cnt ? text[base + p] : (uint8_t)0xFF;
-  bar_sync(1, U8_THREADS);  // mbarrier initialised, direct staging done
+    for (int p = tid; p < T; p += NT) smem[p] = p < cnt ? text[base + p] : (uint8_t)0xFF;
+  bar_sync(1, NT);  // mbarrier initialised, direct staging done
   mbar_wait(mbar, 0);
   uint8_t* bits8 = reinterpret_cast<uint8_t*>(bits);
 
@@ -478,42 +493,54 @@ __global__ void __launch_bounds__(U8_THREADS, U8_K8_CTAS) level_pass8_kernel(con
   for (int j = 0; j < W; ++j) {
     const int sh = W - 1 - j;
     const uint8_t* cur = smem + (size_t)(j & 1) * T;
-    const uint2 q0 = reinterpret_cast<const uint2*>(cur)[tid];
-    const uint2 q1 = reinterpret_cast<const uint2*>(cur + H)[tid];
-    const uint32_t x[4] = {q0.x, q0.y, q1.x, q1.y};
-    uint32_t b[4];
+    uint32_t x[2 * Q];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) b[k] = (x[k] >> sh) & B1;
-    const uint32_t m0 = ((b[1] * 16u + b[0]) * 0x01020408u) >> 24;
-    const uint32_t m1 = ((b[3] * 16u + b[2]) * 0x01020408u) >> 24;
-    const uint32_t ones0 = __popc(m0), ones1 = __popc(m1);
-    if (j > 0) {  // level 0 was written by hist8_kernel
-      bits8[j * 4 * (NC + 4) + tid] = (uint8_t)m0;
-      bits8[j * 4 * (NC + 4) + H / 8 + tid] = (uint8_t)m1;
+    for (int k = 0; k < Q; ++k) {
+      const uint2 qv = reinterpret_cast<const uint2*>(cur + k * R)[tid];
+      x[2 * k] = qv.x;
+      x[2 * k + 1] = qv.y;
+    }
+    uint32_t m[Q], ones[Q];
+#pragma unroll
+    for (int k = 0; k < Q; ++k) {
+      // one multiply gathers a run's 8 flags (bits at 8i and 8i + 4 -> 24 + i, 28 + i)
+      const uint32_t b0 = (x[2 * k] >> sh) & B1, b1 = (x[2 * k + 1] >> sh) & B1;
+      m[k] = ((b1 * 16u + b0) * 0x01020408u) >> 24;
+      ones[k] = __popc(m[k]);
+      if (j > 0) bits8[j * 4 * (NC + 4) + k * (R / 8) + tid] = (uint8_t)m[k];  // level 0: hist8_kernel
     }
     if (j + 1 == W) break;
-    const uint32_t pk = ones0 | (ones1 << 16);
-    const uint32_t incl = warp_incl_scan(pk);
-    if (lane == 31) s_wtot[j & 1][wid] = incl;
-    bar_sync(1, U8_THREADS);
-    const uint32_t wv = lane < NW ? s_wtot[j & 1][lane] : 0u;
-    const uint32_t wpre = __reduce_add_sync(FULL, lane < wid ? wv : 0u);
-    const uint32_t tot = __reduce_add_sync(FULL, wv);
-    const uint32_t ex = wpre + incl - pk;
-    const int tot0 = (int)(tot & 0xFFFFu), tot1 = (int)(tot >> 16);
-    const int Z = T - tot0 - tot1;
-    const int opre0 = (int)(ex & 0xFFFFu);
-    const int opre1 = tot0 + (int)(ex >> 16);
-    const int OB[2] = {Z + opre0 - 1, Z + opre1 - 1};
-    const int ZB[2] = {8 * tid - opre0, H + 8 * tid - opre1};
+    uint32_t pk[P], incl[P];
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      pk[p] = ones[2 * p] | (ones[2 * p + 1] << 16);
+      incl[p] = warp_incl_scan(pk[p]);
+      if (lane == 31) s_wtot[j & 1][p][wid] = incl[p];
+    }
+    bar_sync(1, NT);
+    int opre[Q];
+    int run_tot = 0;
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      const uint32_t wv = lane < NW ? s_wtot[j & 1][p][lane] : 0u;
+      const uint32_t wpre = __reduce_add_sync(FULL, lane < wid ? wv : 0u);
+      const uint32_t tot = __reduce_add_sync(FULL, wv);
+      const uint32_t ex = wpre + incl[p] - pk[p];
+      opre[2 * p] = run_tot + (int)(ex & 0xFFFFu);
+      run_tot += (int)(tot & 0xFFFFu);
+      opre[2 * p + 1] = run_tot + (int)(ex >> 16);
+      run_tot += (int)(tot >> 16);
+    }
+    const int Z = T - run_tot;
     const uint32_t nxt = sbase + (uint32_t)((j + 1) & 1) * T;
 #pragma unroll
-    for (int hh = 0; hh < 2; ++hh) {
-      const uint32_t sel = s_lut[hh ? m1 : m0];
-      const uint32_t sv[2] = {prmt(x[2 * hh], x[2 * hh + 1], sel), prmt(x[2 * hh], x[2 * hh + 1], sel >> 16)};
-      const int nz = 8 - (int)(hh ? ones1 : ones0);
-      const uint32_t za = opaque(nxt + (uint32_t)ZB[hh]);
-      const uint32_t oa = opaque(nxt + (uint32_t)(OB[hh] + 1 - nz));
+    for (int k = 0; k < Q; ++k) {
+      const uint32_t sel = s_lut[m[k]];  // prmt reads selector bits 0-15
+      const uint32_t sv[2] = {prmt(x[2 * k], x[2 * k + 1], sel), prmt(x[2 * k], x[2 * k + 1], sel >> 16)};
+      const int nz = 8 - (int)ones[k];
+      // zeros of run k go to k R + 8 t - opre (its zeros before), ones to Z + opre
+      const uint32_t za = opaque(nxt + (uint32_t)(k * R + 8 * tid - opre[k]));
+      const uint32_t oa = opaque(nxt + (uint32_t)(Z + opre[k] - nz));
 #ifndef K8_SEL_ADDR
       // address selection mostly off the integer ALU pipe (its bound): the
       // carry of (15 - nz) 2^28 + (kk + 1) 2^28 out of 32 bits is [kk >= nz],
@@ -539,9 +566,9 @@ __global__ void __launch_bounds__(U8_THREADS, U8_K8_CTAS) level_pass8_kernel(con
       }
 #endif
     }
-    bar_sync(1, U8_THREADS);
+    bar_sync(1, NT);
   }
-  bar_sync(1, U8_THREADS);  // every warp's level bits are stored
+  bar_sync(1, NT);  // every warp's level bits are stored
   // emission of levels 1..W-1: one destination word per task, the runs of all
   // levels flattened (consecutive tasks = consecutive words of one run, so
   // the stores of a warp coalesce); whole words stored, run-edge words OR-ed
@@ -551,7 +578,7 @@ __global__ void __launch_bounds__(U8_THREADS, U8_K8_CTAS) level_pass8_kernel(con
 #else
   const int total = tt.wpre[NR];
 #endif
-  for (int q = tid; q < total; q += U8_THREADS) {
+  for (int q = tid; q < total; q += NT) {
     int r = 0;  // last run with wpre[r] <= q (empty runs share prefix values)
 #pragma unroll
     for (int s = 128; s >= 1; s >>= 1)
@@ -590,9 +617,10 @@ cudaError_t launch_tiles8(const Pass8Args& a, Tab8* tabs, cudaStream_t s) {
 
 template <int W>
 cudaError_t launch_pass8(const Pass8Args& a, Tab8* tabs, cudaStream_t s) {
-  constexpr int T = U8_THREADS * 16;
-  const size_t smem = 2 * (size_t)T + sizeof(Tab8) + (size_t)W * (T / 32 + 4) * 4;
-  auto kern = level_pass8_kernel<W>;
+  constexpr int T = K8_TILE;
+  // level bits of levels 1..W-1 only (level 0 comes from hist8_kernel)
+  const size_t smem = 2 * (size_t)T + sizeof(Tab8) + (size_t)(W - 1) * (T / 32 + 4) * 4;
+  auto kern = level_pass8_kernel<W, K8_Q>;
   static bool set = false;
   if (!set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -601,7 +629,7 @@ cudaError_t launch_pass8(const Pass8Args& a, Tab8* tabs, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     set = true;
   }
-  kern<<<(unsigned)a.ntiles, U8_THREADS, smem, s>>>(a, tabs);
+  kern<<<(unsigned)a.ntiles, K8Cfg<K8_Q>::NT, smem, s>>>(a, tabs);
   return cudaGetLastError();
 }
 
