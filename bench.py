@@ -55,7 +55,7 @@ def code_width(sigma: int) -> int:
 def pass_plan(n: int, sym_bytes: int, sigma: int, kind: str):
     """Mirror of the device plan (make_plan() / k8_eligible() in csrc): (level, K, in_bytes, out_bytes) per pass."""
     w = code_width(sigma)
-    if sym_bytes == 1 and 5 <= w <= 8 and 0 < n < (1 << 32) - 64:
+    if sym_bytes == 1 and 2 <= w <= 8 and 0 < n < (1 << 32) - 64:
         return [(0, w, 1, 0)]  # k8.cuh: every level in one fused pass
     vbits = 8 * sym_bytes
     bb = lambda b: 1 if b <= 8 else 2 if b <= 16 else 4  # noqa: E731

@@ -1,4 +1,4 @@
-// K8: the whole build of a byte text with code width 5 <= W <= 8 in ONE fused
+// K8: the whole build of a byte text with code width 2 <= W <= 8 in ONE fused
 // pass.  For a wavelet matrix the symbols of level l with equal l-bit key keep
 // their text order (A_l is the stable LSD sort of the text by the key), and
 // for the tree the same holds per prefix group, so every level's contribution
@@ -661,7 +661,7 @@ inline bool k8_eligible(int sym_bytes, int w, int64_t n) {
 #ifdef WVLT_NO_K8
   return false;
 #else
-  return sym_bytes == 1 && w >= 5 && w <= 8 && n > 0 && n < (1ll << 32) - 64;
+  return sym_bytes == 1 && w >= 2 && w <= 8 && n > 0 && n < (1ll << 32) - 64;
 #endif
 }
 
@@ -716,6 +716,9 @@ int build_k8(const uint8_t* text, int64_t n, int64_t sigma, int w, int kind, uin
   const uint32_t vmax_ok = (uint32_t)std::min<int64_t>(sigma - 1, 255);
   const int check = vmax_ok < 255 ? 1 : 0;
   switch (w) {
+    case 2: e = launch_hist8<2>(text, n, L.ntiles, vmax_ok, check, tcnt8, level_words, st_flag, s); break;
+    case 3: e = launch_hist8<3>(text, n, L.ntiles, vmax_ok, check, tcnt8, level_words, st_flag, s); break;
+    case 4: e = launch_hist8<4>(text, n, L.ntiles, vmax_ok, check, tcnt8, level_words, st_flag, s); break;
     case 5: e = launch_hist8<5>(text, n, L.ntiles, vmax_ok, check, tcnt8, level_words, st_flag, s); break;
     case 6: e = launch_hist8<6>(text, n, L.ntiles, vmax_ok, check, tcnt8, level_words, st_flag, s); break;
     case 7: e = launch_hist8<7>(text, n, L.ntiles, vmax_ok, check, tcnt8, level_words, st_flag, s); break;
@@ -745,6 +748,9 @@ int build_k8(const uint8_t* text, int64_t n, int64_t sigma, int w, int kind, uin
   a.base = base;
   Tab8* tabs = (Tab8*)(ws + L.off_tabs);
   switch (w) {
+    case 2: e = launch_tiles8<2>(a, tabs, s); break;
+    case 3: e = launch_tiles8<3>(a, tabs, s); break;
+    case 4: e = launch_tiles8<4>(a, tabs, s); break;
     case 5: e = launch_tiles8<5>(a, tabs, s); break;
     case 6: e = launch_tiles8<6>(a, tabs, s); break;
     case 7: e = launch_tiles8<7>(a, tabs, s); break;
@@ -754,6 +760,9 @@ int build_k8(const uint8_t* text, int64_t n, int64_t sigma, int w, int kind, uin
   ++g_launches;
   prof_mark(s, WVLT_STAGE_TABLES);
   switch (w) {
+    case 2: e = launch_pass8<2>(a, tabs, s); break;
+    case 3: e = launch_pass8<3>(a, tabs, s); break;
+    case 4: e = launch_pass8<4>(a, tabs, s); break;
     case 5: e = launch_pass8<5>(a, tabs, s); break;
     case 6: e = launch_pass8<6>(a, tabs, s); break;
     case 7: e = launch_pass8<7>(a, tabs, s); break;

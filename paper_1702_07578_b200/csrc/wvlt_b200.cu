@@ -2061,7 +2061,7 @@ int build_device_impl(const void* text, int sym_bytes, int64_t n, int64_t sigma,
   }
   if (!text || !level_words || !workspace) return WVLT_E_ARG;
   if (k8_eligible(sym_bytes, w, n) && !borders && !P.widen_bytes) {
-    // byte text, 5 <= w <= 8: every level in one fused pass (k8.cuh)
+    // byte text, 2 <= w <= 8: every level in one fused pass (k8.cuh)
     if (workspace_bytes < k8_layout(n, w).total) return WVLT_E_WORKSPACE;
     return build_k8((const uint8_t*)text, n, sigma, w, kind, level_words, zeros, hist, workspace, status, s,
                     pass_done, ctx);
