@@ -145,3 +145,35 @@ def test_config_bytes_vs_oracle_ps(config):
         assert np.array_equal(words, ow), kind
         if kind == "wm":
             assert zeros == oz
+
+
+@pytest.mark.parametrize("kind", ["wm", "wt"])
+def test_byte_text_beyond_2_31_symbols(kind):
+    """The single fused pass keeps 32-bit bit positions (n < 2^32 - 64): a c2-like
+    text of 2^31 + 12345 symbols (past every signed 32-bit boundary), checked by
+    decode, zero counts and popcounts."""
+    n = (1 << 31) + 12345
+    torch.cuda.empty_cache()
+    text = workloads.generate("c2", n=n)
+    b = DeviceBuilder()
+    res = b.build(text, 256, kind, histogram=True)
+    levels = res.level_words
+    hist = res.hist.cpu().numpy()
+    assert int(hist.sum()) == n
+    h = hist.copy()
+    exp_zeros = []
+    for _ in range(8):
+        exp_zeros.append(int(h[0::2].sum()))
+        h = h[0::2] + h[1::2]
+    exp_zeros = exp_zeros[::-1]
+    assert [int(z) for z in res.zeros.cpu().tolist()] == exp_zeros
+    for ell in range(8):
+        assert int(popcount64(levels[ell]).sum()) == n - exp_zeros[ell], ell
+    g = torch.Generator(device="cuda")
+    g.manual_seed(9)
+    pos = torch.randint(0, n, (1 << 16,), generator=g, device="cuda", dtype=torch.int64)
+    pos[:4] = torch.tensor([0, (1 << 31) - 1, 1 << 31, n - 1], device="cuda")
+    got = decode(kind, levels, res.zeros, n, 8, pos)
+    assert torch.equal(got, text[pos].to(torch.int64))
+    del res, text, levels
+    torch.cuda.empty_cache()
