@@ -26,7 +26,7 @@ template <int W>
 __global__ void __launch_bounds__(H8_WARPS * 32) hist8_kernel(const uint8_t* __restrict__ text, int64_t n,
                                                              int64_t ntiles, uint32_t vmax_ok, int check,
                                                              uint32_t* __restrict__ tcnt8, uint64_t* __restrict__ level0,
-                                                             int32_t* __restrict__ status) {
+                                                             int64_t nwords, int32_t* __restrict__ status) {
   constexpr int NB = 1 << W;
   constexpr int HALF = NB / 2;
   constexpr int WORDS = HALF * 32;
@@ -42,6 +42,17 @@ __global__ void __launch_bounds__(H8_WARPS * 32) hist8_kernel(const uint8_t* __r
   for (int64_t t = (int64_t)blockIdx.x * H8_WARPS + wid; t < ntiles; t += nwarps) {
     const int64_t first = t * TILE_U8;
     const int cnt = (int)min((int64_t)TILE_U8, n - first);
+    {
+      // zero this tile's words of levels 1..W-1 (the pass ORs run-edge words);
+      // streamed here instead of a separate memset of the same bytes
+      const int64_t w0 = first >> 6;
+      const int tw = (int)min((int64_t)(TILE_U8 / 64), nwords - w0);
+#pragma unroll
+      for (int j = 1; j < W; ++j) {
+        uint64_t* lw = level0 + j * nwords + w0;
+        for (int i = lane; i < tw; i += 32) __stcs(reinterpret_cast<unsigned long long*>(lw + i), 0ull);
+      }
+    }
     if (cnt == TILE_U8 && aligned) {
       const uint4* v4 = reinterpret_cast<const uint4*>(text + first);
 #pragma unroll 1
@@ -635,7 +646,7 @@ cudaError_t launch_pass8(const Pass8Args& a, Tab8* tabs, cudaStream_t s) {
 
 template <int W>
 cudaError_t launch_hist8(const uint8_t* text, int64_t n, int64_t ntiles, uint32_t vmax_ok, int check,
-                         uint32_t* tcnt8, uint64_t* level0, int32_t* status, cudaStream_t s) {
+                         uint32_t* tcnt8, uint64_t* level0, int64_t nwords, int32_t* status, cudaStream_t s) {
   constexpr size_t sb = (size_t)H8_WARPS * (1 << (W - 1)) * 32 * 4;
   static bool set = false;
   if (!set) {
@@ -647,7 +658,7 @@ cudaError_t launch_hist8(const uint8_t* text, int64_t n, int64_t ntiles, uint32_
   const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((ntiles + H8_WARPS - 1) / H8_WARPS,
                                                                  (int64_t)sm_count() * per_sm));
   hist8_kernel<W><<<(unsigned)blocks, H8_WARPS * 32, sb, s>>>(text, n, ntiles, vmax_ok, check, tcnt8, level0,
-                                                              status);
+                                                              nwords, status);
   return cudaGetLastError();
 }
 
@@ -704,10 +715,8 @@ int build_k8(const uint8_t* text, int64_t n, int64_t sigma, int w, int kind, uin
   cudaError_t e;
   g_prof.n = 0;
   prof_mark(s, -1);
-  // level 0 is written whole (every word) by hist8_kernel; the other
-  // levels' run-edge words are OR-ed and need zeros
-  e = cudaMemsetAsync(level_words + nwords, 0, (size_t)(w - 1) * nwords * 8, s);
-  if (e != cudaSuccess) return (int)e;
+  // level 0 is written whole (every word) by hist8_kernel, which also zeroes
+  // levels 1..w-1 (their run-edge words are OR-ed by the pass)
   if (!status) {
     e = cudaMemsetAsync(st_flag, 0, 4, s);
     if (e != cudaSuccess) return (int)e;
@@ -716,13 +725,13 @@ int build_k8(const uint8_t* text, int64_t n, int64_t sigma, int w, int kind, uin
   const uint32_t vmax_ok = (uint32_t)std::min<int64_t>(sigma - 1, 255);
   const int check = vmax_ok < 255 ? 1 : 0;
   switch (w) {
-    case 2: e = launch_hist8<2>(text, n, L.ntiles, vmax_ok, check, tcnt8, level_words, st_flag, s); break;
-    case 3: e = launch_hist8<3>(text, n, L.ntiles, vmax_ok, check, tcnt8, level_words, st_flag, s); break;
-    case 4: e = launch_hist8<4>(text, n, L.ntiles, vmax_ok, check, tcnt8, level_words, st_flag, s); break;
-    case 5: e = launch_hist8<5>(text, n, L.ntiles, vmax_ok, check, tcnt8, level_words, st_flag, s); break;
-    case 6: e = launch_hist8<6>(text, n, L.ntiles, vmax_ok, check, tcnt8, level_words, st_flag, s); break;
-    case 7: e = launch_hist8<7>(text, n, L.ntiles, vmax_ok, check, tcnt8, level_words, st_flag, s); break;
-    default: e = launch_hist8<8>(text, n, L.ntiles, vmax_ok, check, tcnt8, level_words, st_flag, s); break;
+    case 2: e = launch_hist8<2>(text, n, L.ntiles, vmax_ok, check, tcnt8, level_words, nwords, st_flag, s); break;
+    case 3: e = launch_hist8<3>(text, n, L.ntiles, vmax_ok, check, tcnt8, level_words, nwords, st_flag, s); break;
+    case 4: e = launch_hist8<4>(text, n, L.ntiles, vmax_ok, check, tcnt8, level_words, nwords, st_flag, s); break;
+    case 5: e = launch_hist8<5>(text, n, L.ntiles, vmax_ok, check, tcnt8, level_words, nwords, st_flag, s); break;
+    case 6: e = launch_hist8<6>(text, n, L.ntiles, vmax_ok, check, tcnt8, level_words, nwords, st_flag, s); break;
+    case 7: e = launch_hist8<7>(text, n, L.ntiles, vmax_ok, check, tcnt8, level_words, nwords, st_flag, s); break;
+    default: e = launch_hist8<8>(text, n, L.ntiles, vmax_ok, check, tcnt8, level_words, nwords, st_flag, s); break;
   }
   if (e != cudaSuccess) return (int)e;
   ++g_launches;
