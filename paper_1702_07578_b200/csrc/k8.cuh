@@ -494,6 +494,11 @@ __global__ void __launch_bounds__(K8Cfg<Q>::NT, K8Cfg<Q>::CTAS) level_pass8_kern
                    : "memory");
   }
   for (int i = tid; i < 256; i += NT) s_lut[i] = g_sort_lut.sel[i];
+#ifndef K8_LAST_SPLIT_BYTES
+  // level W-1 is OR-ed bit by bit from the last split (order W-1 is never
+  // materialised as bytes)
+  for (int i = tid; i < NC + 4; i += NT) bits[(W - 1) * (NC + 4) + i] = 0u;
+#endif
   if (!bulk)
     for (int p = tid; p < T; p += NT) smem[p] = p < cnt ? text[base + p] : (uint8_t)0xFF;
   bar_sync(1, NT);  // mbarrier initialised, direct staging done
@@ -521,6 +526,11 @@ __global__ void __launch_bounds__(K8Cfg<Q>::NT, K8Cfg<Q>::CTAS) level_pass8_kern
       if (j > 0) bits8[j * 4 * (NC + 4) + k * (R / 8) + tid] = (uint8_t)m[k];  // level 0: hist8_kernel
     }
     if (j + 1 == W) break;
+#ifndef K8_LAST_SPLIT_BYTES
+    constexpr bool last_bits = true;
+#else
+    constexpr bool last_bits = false;
+#endif
     uint32_t pk[P], incl[P];
 #pragma unroll
     for (int p = 0; p < P; ++p) {
@@ -543,6 +553,34 @@ __global__ void __launch_bounds__(K8Cfg<Q>::NT, K8Cfg<Q>::CTAS) level_pass8_kern
       run_tot += (int)(tot >> 16);
     }
     const int Z = T - run_tot;
+    if (last_bits && j + 2 == W) {
+      // last split: only the next level's bits are needed.  The run's flags of
+      // bit sh - 1 in split order (zeros part low, ones part high) are OR-ed
+      // into the level W-1 bit array at the two parts' positions.
+      uint32_t* LB = bits + (W - 1) * (NC + 4);
+#pragma unroll
+      for (int k = 0; k < Q; ++k) {
+        const uint32_t sel = s_lut[m[k]];
+        const uint32_t s0 = prmt(x[2 * k], x[2 * k + 1], sel), s1 = prmt(x[2 * k], x[2 * k + 1], sel >> 16);
+        const uint32_t c0 = (s0 >> (sh - 1)) & B1, c1 = (s1 >> (sh - 1)) & B1;
+        const uint32_t f = ((c1 * 16u + c0) * 0x01020408u) >> 24;
+        const int nz = 8 - (int)ones[k];
+        const uint32_t pz = (uint32_t)(k * R + 8 * tid - opre[k]);
+        const uint32_t po = (uint32_t)(Z + opre[k]);
+        const uint32_t fz = f & ((1u << nz) - 1u), fo = f >> nz;
+        if (fz) {
+          const uint64_t v = (uint64_t)fz << (pz & 31);
+          atomicOr(LB + (pz >> 5), (uint32_t)v);
+          if (v >> 32) atomicOr(LB + (pz >> 5) + 1, (uint32_t)(v >> 32));
+        }
+        if (fo) {
+          const uint64_t v = (uint64_t)fo << (po & 31);
+          atomicOr(LB + (po >> 5), (uint32_t)v);
+          if (v >> 32) atomicOr(LB + (po >> 5) + 1, (uint32_t)(v >> 32));
+        }
+      }
+      break;
+    }
     const uint32_t nxt = sbase + (uint32_t)((j + 1) & 1) * T;
 #pragma unroll
     for (int k = 0; k < Q; ++k) {
