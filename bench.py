@@ -60,7 +60,11 @@ def pass_plan(n: int, sym_bytes: int, sigma: int, kind: str):
     vbits = 8 * sym_bytes
     bb = lambda b: 1 if b <= 8 else 2 if b <= 16 else 4  # noqa: E731
     out, ell = [], 0
+    tail = kind == "wm" and w > 8 and 0 < n < (1 << 32) - 64  # make_plan(): fused byte tail
     while ell < w:
+        if tail and w - ell <= 8:
+            out.append((ell, w - ell, 1, 0))
+            break
         K = min(KMAX, w - ell)
         live_in = (w - ell) if kind == "wm" else w
         live_out = (w - ell - K) if kind == "wm" else w

@@ -19,6 +19,9 @@ namespace {
 // One warp per tile; lane-private 16-bit counters paired (p, p + 2^(W-1)) as in
 // hist_u8_kernel, zeroed after every tile so the per-tile row sums never carry.
 constexpr int H8_WARPS = 4;
+#ifndef H8_BATCH
+#define H8_BATCH 8  // 16-byte loads in flight per lane
+#endif
 
 // It also writes level 0 (the top code bit of every symbol, already in text
 // order), so that level can leave for the host while the rest is built.
@@ -56,12 +59,12 @@ __global__ void __launch_bounds__(H8_WARPS * 32) hist8_kernel(const uint8_t* __r
     if (cnt == TILE_U8 && aligned) {
       const uint4* v4 = reinterpret_cast<const uint4*>(text + first);
 #pragma unroll 1
-      for (int k0 = 0; k0 < TILE_U8 / 16 / 32; k0 += 8) {
-        uint4 q[8];
+      for (int k0 = 0; k0 < TILE_U8 / 16 / 32; k0 += H8_BATCH) {
+        uint4 q[H8_BATCH];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) q[k] = __ldcs(v4 + (k0 + k) * 32 + lane);
+        for (int k = 0; k < H8_BATCH; ++k) q[k] = __ldcs(v4 + (k0 + k) * 32 + lane);
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
+        for (int k = 0; k < H8_BATCH; ++k) {
           const uint32_t wd[4] = {q[k].x, q[k].y, q[k].z, q[k].w};
           uint32_t m16 = 0;  // level-0 bits of this lane's 16 symbols
 #pragma unroll
@@ -739,7 +742,7 @@ inline K8Layout k8_layout(int64_t n, int w) {
 // The whole single-pass build (called by build_device_impl).
 int build_k8(const uint8_t* text, int64_t n, int64_t sigma, int w, int kind, uint64_t* level_words,
              int64_t* zeros, int64_t* hist, void* workspace, int32_t* status, cudaStream_t s,
-             void (*pass_done)(void*, int, int), void* ctx) {
+             void (*pass_done)(void*, int, int), void* ctx, int lvl0, int tail_pass) {
   const K8Layout L = k8_layout(n, w);
   const int nb = 1 << w;
   unsigned char* ws = (unsigned char*)workspace;
@@ -751,15 +754,18 @@ int build_k8(const uint8_t* text, int64_t n, int64_t sigma, int w, int kind, uin
   int32_t* st_flag = status ? status : (int32_t*)(ws + L.total - 256);
   const int64_t nwords = (n + 63) >> 6;
   cudaError_t e;
-  g_prof.n = 0;
-  prof_mark(s, -1);
+  const bool tail = tail_pass >= 0;  // the fused tail of a wider WM build (levels lvl0..)
+  if (!tail) {
+    g_prof.n = 0;
+    prof_mark(s, -1);
+  }
   // level 0 is written whole (every word) by hist8_kernel, which also zeroes
   // levels 1..w-1 (their run-edge words are OR-ed by the pass)
   if (!status) {
     e = cudaMemsetAsync(st_flag, 0, 4, s);
     if (e != cudaSuccess) return (int)e;
   }
-  prof_mark(s, WVLT_STAGE_MEMSET);
+  if (!tail) prof_mark(s, WVLT_STAGE_MEMSET);
   const uint32_t vmax_ok = (uint32_t)std::min<int64_t>(sigma - 1, 255);
   const int check = vmax_ok < 255 ? 1 : 0;
   switch (w) {
@@ -773,15 +779,15 @@ int build_k8(const uint8_t* text, int64_t n, int64_t sigma, int w, int kind, uin
   }
   if (e != cudaSuccess) return (int)e;
   ++g_launches;
-  prof_mark(s, WVLT_STAGE_HIST);
-  if (pass_done) pass_done(ctx, 0, 1);  // level 0 is final: it may leave now
+  if (!tail) prof_mark(s, WVLT_STAGE_HIST);
+  if (pass_done) pass_done(ctx, lvl0, 1);  // level 0 is final: it may leave now
   scan8_chunks_kernel<<<(unsigned)L.nchunks, nb, 0, s>>>(tcnt8, L.ntiles, nb, chunk);
   scan8_carry_kernel<<<nb, S8_SCAN_THREADS, 0, s>>>(chunk, L.nchunks, nb, totals);
   scan8_apply_kernel<<<(unsigned)L.nchunks, nb, 0, s>>>(tcnt8, L.ntiles, nb, chunk, tpre8);
   g_launches += 3;
   e = cudaGetLastError();
   if (e != cudaSuccess) return (int)e;
-  prof_mark(s, WVLT_STAGE_SCAN0);
+  if (!tail) prof_mark(s, WVLT_STAGE_SCAN0);
   tables8_kernel<<<1, 256, 0, s>>>(totals, w, kind, base, zeros, hist);
   ++g_launches;
   Pass8Args a;
@@ -805,7 +811,7 @@ int build_k8(const uint8_t* text, int64_t n, int64_t sigma, int w, int kind, uin
   }
   if (e != cudaSuccess) return (int)e;
   ++g_launches;
-  prof_mark(s, WVLT_STAGE_TABLES);
+  prof_mark(s, tail ? WVLT_STAGE_SCAN0 + tail_pass : WVLT_STAGE_TABLES);
   switch (w) {
     case 2: e = launch_pass8<2>(a, tabs, s); break;
     case 3: e = launch_pass8<3>(a, tabs, s); break;
@@ -817,9 +823,11 @@ int build_k8(const uint8_t* text, int64_t n, int64_t sigma, int w, int kind, uin
   }
   if (e != cudaSuccess) return (int)e;
   ++g_launches;
-  prof_mark(s, WVLT_STAGE_PASS0);
-  if (pass_done) pass_done(ctx, 1, w - 1);
+  prof_mark(s, WVLT_STAGE_PASS0 + (tail ? tail_pass : 0));
+  if (pass_done) pass_done(ctx, lvl0 + 1, w - 1);
   return 0;
 }
+
+size_t k8_workspace_total(int64_t n, int w) { return k8_layout(n, w).total; }
 
 }  // namespace

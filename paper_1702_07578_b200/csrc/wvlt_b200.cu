@@ -568,6 +568,10 @@ struct Plan {
   size_t off_chain, off_wtstart, off_wmbase, off_corr, off_scratch, off_tcnt[MAXP], off_tpre[MAXP], off_bsum,
       off_buf0, off_buf1, off_wide;
   size_t tcnt_bytes, buf_bytes, total;
+  // WM with w > 8: the last tail_w <= 8 levels (from tail_lvl) are one fused
+  // byte pass (k8.cuh) over the u8 output of the last generic pass; its
+  // workspace is the other ping-pong buffer
+  int tail_w, tail_lvl;
 };
 
 __host__ __device__ inline int64_t chain_off(int k) { return (1ll << k) - 1; }  // level-k table in a 2^(w+1)-1 array
@@ -1216,18 +1220,18 @@ __global__ void __launch_bounds__(PASS_THREADS + TAB_WARP_THREADS, 2) level_pass
             const unsigned dig = (xv >> eshift) & (nd - 1);
             tt.row[dig][pos] = (TOut)(xv & keep);
             const unsigned h = pos >= tt.thr[dig] ? 1u : 0u;
-            atomicAdd(&s_ncnt[(((dig << 1) | h) << a.nK) | ((xv >> nshift) & nmask)], 1u);
+            if (a.ncnt) atomicAdd(&s_ncnt[(((dig << 1) | h) << a.nK) | ((xv >> nshift) & nmask)], 1u);
           } else {
             const unsigned d = rev_bits((xv >> eshift) & (nd - 1), K);
             const uint64_t P = eshift >= 32 ? 0 : ((uint64_t)xv >> eshift);
             const int64_t gpos = a.corr[a.corr_off[K] + P] + tt.lb[K][d] + pos - tt.ls[K][d];
             reinterpret_cast<TOut*>(a.dst)[gpos] = (TOut)(xv & keep);
-            atomicAdd(&a.ncnt[(int64_t)((xv >> nshift) & nmask) * a.nntiles + (gpos >> a.ntshift)], 1u);
+            if (a.ncnt) atomicAdd(&a.ncnt[(int64_t)((xv >> nshift) & nmask) * a.nntiles + (gpos >> a.ntshift)], 1u);
           }
         }
       }
       bar_sync(1, PASS_THREADS);
-      if (q1) {
+      if (q1 && a.ncnt) {
         const int ncount = 2 * nd << a.nK;
         for (int i = tid; i < ncount; i += PASS_THREADS) {
           const uint32_t v = s_ncnt[i];
@@ -1659,6 +1663,8 @@ int log2i(int v) {
   return r;
 }
 
+size_t k8_workspace_total(int64_t n, int w);  // k8.cuh
+
 bool make_plan(int64_t n, int sym_bytes, int64_t sigma, int kind, Plan* P) {
   memset(P, 0, sizeof(*P));
   const int w = code_width_host(sigma);
@@ -1675,7 +1681,12 @@ bool make_plan(int64_t n, int sym_bytes, int64_t sigma, int kind, Plan* P) {
   int l = 0, p = 0;
   int64_t corr = 0;
   size_t max_buf = 0;
-  while (l < w) {
+#ifndef WVLT_NO_K8_TAIL
+  const bool tail = kind == WVLT_KIND_WM && w > 8 && n > 0 && n < (1ll << 32) - 64;
+#else
+  const bool tail = false;
+#endif
+  while (l < w && !(tail && w - l <= 8)) {
     const int K = (w - l) < KMAX ? (w - l) : KMAX;
     P->lvl[p] = l;
     P->K[p] = K;
@@ -1699,6 +1710,10 @@ bool make_plan(int64_t n, int sym_bytes, int64_t sigma, int kind, Plan* P) {
   }
   P->npass = p;
   P->corr_total = corr;
+  if (tail) {
+    P->tail_w = w - l;
+    P->tail_lvl = l;
+  }
   size_t off = 0;
   const size_t chain_bytes = ((size_t)2 << w) * 8;
   P->off_chain = off;
@@ -1726,6 +1741,7 @@ bool make_plan(int64_t n, int sym_bytes, int64_t sigma, int kind, Plan* P) {
   }
   P->off_bsum = off;
   off = align_up(off + (size_t)NDIG * max_nblk * 8, 256);
+  if (tail) max_buf = std::max(max_buf, k8_workspace_total(n, P->tail_w));
   P->buf_bytes = align_up(max_buf ? max_buf : 16, 256);
   P->off_buf0 = off;
   off += P->buf_bytes;
@@ -2064,7 +2080,7 @@ int build_device_impl(const void* text, int sym_bytes, int64_t n, int64_t sigma,
     // byte text, 2 <= w <= 8: every level in one fused pass (k8.cuh)
     if (workspace_bytes < k8_layout(n, w).total) return WVLT_E_WORKSPACE;
     return build_k8((const uint8_t*)text, n, sigma, w, kind, level_words, zeros, hist, workspace, status, s,
-                    pass_done, ctx);
+                    pass_done, ctx, 0, -1);
   }
   if (workspace_bytes < P.total) return WVLT_E_WORKSPACE;
   unsigned char* ws = (unsigned char*)workspace;
@@ -2078,7 +2094,8 @@ int build_device_impl(const void* text, int sym_bytes, int64_t n, int64_t sigma,
 
   g_prof.n = 0;
   prof_mark(s, -1);
-  e = cudaMemsetAsync(level_words, 0, (size_t)w * nwords * 8, s);
+  // (the fused tail writes / zeroes its own levels)
+  e = cudaMemsetAsync(level_words, 0, (size_t)(P.tail_w ? P.tail_lvl : w) * nwords * 8, s);
   if (e != cudaSuccess) return (int)e;
   e = cudaMemsetAsync(ws + P.off_tcnt[0], 0, P.tcnt_bytes, s);
   if (e != cudaSuccess) return (int)e;
@@ -2169,7 +2186,9 @@ int build_device_impl(const void* text, int sym_bytes, int64_t n, int64_t sigma,
     pa.has_out = P.out_bytes[p] ? 1 : 0;
     pa.tcnt = tcnt;
     pa.tpre = tpre;
-    if (pa.has_out) {
+    if (pa.has_out && p + 1 == P.npass) {
+      pa.ntshift = 13;  // output for the fused tail, which counts its own digits
+    } else if (pa.has_out) {
       pa.ncnt = (uint32_t*)(ws + P.off_tcnt[p + 1]);
       pa.nntiles = P.ntiles[p + 1];
       pa.ntshift = P.tshift[p + 1];
@@ -2184,6 +2203,12 @@ int build_device_impl(const void* text, int sym_bytes, int64_t n, int64_t sigma,
     prof_mark(s, WVLT_STAGE_PASS0 + p);
     if (pass_done) pass_done(ctx, P.lvl[p], P.K[p]);
     cur = pa.dst;
+  }
+  if (P.tail_w) {
+    const int64_t lt = P.tail_lvl;
+    return build_k8((const uint8_t*)cur, n, (int64_t)1 << P.tail_w, P.tail_w, kind, level_words + lt * nwords,
+                    zeros ? zeros + lt : nullptr, nullptr, bufs[P.npass & 1], st_flag, s, pass_done, ctx,
+                    (int)lt, P.npass);
   }
   return 0;
 }
