@@ -3,7 +3,7 @@
 // their text order (A_l is the stable LSD sort of the text by the key), and
 // for the tree the same holds per prefix group, so every level's contribution
 // of a text tile is a set of contiguous runs placed by the tile prefix of its
-// W-bit digit counts.  One CTA per 8192-symbol tile runs the W-1 stable
+// W-bit digit counts.  One CTA per K8_TILE-symbol tile runs the W-1 stable
 // one-bit splits in shared memory and emits all W levels -- no intermediate
 // order ever goes back to HBM, no second pass.  Needs per-tile counts of all
 // 2^W digits (hist8_kernel) and their prefix over tiles (scan8_* kernels).
@@ -19,8 +19,14 @@ namespace {
 // One warp per tile; lane-private 16-bit counters paired (p, p + 2^(W-1)) as in
 // hist_u8_kernel, zeroed after every tile so the per-tile row sums never carry.
 constexpr int H8_WARPS = 4;
+#ifndef K8_TILE
+#define K8_TILE 16384  // symbols per tile of every kernel of the single pass (measured: 8192 and 32768 slower)
+#endif
+#ifndef K8_CTAS
+#define K8_CTAS (K8_TILE == 8192 ? 7 : K8_TILE == 16384 ? 4 : 2)  // pass CTAs per SM (shared memory / registers)
+#endif
 #ifndef H8_BATCH
-#define H8_BATCH 8  // 16-byte loads in flight per lane
+#define H8_BATCH 4  // 16-byte loads in flight per lane (measured: 4 < 8 < 16)
 #endif
 
 // It also writes level 0 (the top code bit of every symbol, already in text
@@ -43,23 +49,23 @@ __global__ void __launch_bounds__(H8_WARPS * 32) hist8_kernel(const uint8_t* __r
   const bool aligned = (((uintptr_t)text) & 15) == 0;
   const int64_t nwarps = (int64_t)gridDim.x * H8_WARPS;
   for (int64_t t = (int64_t)blockIdx.x * H8_WARPS + wid; t < ntiles; t += nwarps) {
-    const int64_t first = t * TILE_U8;
-    const int cnt = (int)min((int64_t)TILE_U8, n - first);
+    const int64_t first = t * K8_TILE;
+    const int cnt = (int)min((int64_t)K8_TILE, n - first);
     {
       // zero this tile's words of levels 1..W-1 (the pass ORs run-edge words);
       // streamed here instead of a separate memset of the same bytes
       const int64_t w0 = first >> 6;
-      const int tw = (int)min((int64_t)(TILE_U8 / 64), nwords - w0);
+      const int tw = (int)min((int64_t)(K8_TILE / 64), nwords - w0);
 #pragma unroll
       for (int j = 1; j < W; ++j) {
         uint64_t* lw = level0 + j * nwords + w0;
         for (int i = lane; i < tw; i += 32) __stcs(reinterpret_cast<unsigned long long*>(lw + i), 0ull);
       }
     }
-    if (cnt == TILE_U8 && aligned) {
+    if (cnt == K8_TILE && aligned) {
       const uint4* v4 = reinterpret_cast<const uint4*>(text + first);
 #pragma unroll 1
-      for (int k0 = 0; k0 < TILE_U8 / 16 / 32; k0 += H8_BATCH) {
+      for (int k0 = 0; k0 < K8_TILE / 16 / 32; k0 += H8_BATCH) {
         uint4 q[H8_BATCH];
 #pragma unroll
         for (int k = 0; k < H8_BATCH; ++k) q[k] = __ldcs(v4 + (k0 + k) * 32 + lane);
@@ -446,11 +452,10 @@ __global__ void __launch_bounds__(T8_WARPS * 32) tiles8_kernel(const Pass8Args a
 #ifndef K8_Q
 #define K8_Q 4
 #endif
-constexpr int K8_TILE = 8192;
 template <int Q>
 struct K8Cfg {
   static constexpr int NT = K8_TILE / (8 * Q);
-  static constexpr int CTAS = Q == 2 ? 4 : Q == 4 ? 7 : 8;
+  static constexpr int CTAS = K8_CTAS;
 };
 
 template <int W, int Q>
@@ -720,7 +725,7 @@ inline bool k8_eligible(int sym_bytes, int w, int64_t n) {
 inline K8Layout k8_layout(int64_t n, int w) {
   K8Layout L;
   const int nb = 1 << w;
-  L.ntiles = (n + TILE_U8 - 1) / TILE_U8;
+  L.ntiles = (n + K8_TILE - 1) / K8_TILE;
   L.nchunks = (L.ntiles + S8_CHUNK - 1) / S8_CHUNK;
   size_t off = 0;
   L.off_tcnt = off;

@@ -48,7 +48,7 @@ def test_running_example():
 @pytest.mark.parametrize("sigma", SIGMA_GRID + (4, 17, 33, 100, 256, 1000, 1 << 16, 1 << 20))
 def test_tile_boundaries_vs_oracle(kind, sigma):
     rng = np.random.default_rng(sigma * 7 + (kind == "wm"))
-    for n in (1, 31, 32, 33, 63, 64, 65, 4095, 4096, 4097, 8191, 8192, 8193, 16383, 16384, 16385, 40961,
+    for n in (1, 31, 32, 33, 63, 64, 65, 4095, 4096, 4097, 8191, 8192, 8193, 16383, 16384, 16385, 32767, 32768, 32769, 40961, 49153,
               int(rng.integers(100_000, 300_000))):
         text = random_text(rng, n, sigma)
         assert wv.dump_structure(wv.build_structure(text, sigma, kind)) == ref_dump(text, sigma, kind), (n, sigma)
@@ -201,7 +201,7 @@ def test_unaligned_device_text(sigma):
     from paper_1702_07578_b200.device import DeviceBuilder
 
     rng = np.random.default_rng(sigma)
-    n = 3 * 8192 + 777
+    n = 3 * 16384 + 777
     base = random_text(rng, n + 1, sigma)
     dev = torch.from_numpy(base).cuda()[1:]  # offset by one element
     assert dev.data_ptr() % 16 != 0
