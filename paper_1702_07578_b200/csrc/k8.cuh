@@ -16,8 +16,9 @@ namespace {
 #endif
 
 // ---- K1: per-tile counts of every W-bit value (tile-major [tile][2^W]) ----
-// One warp per tile; lane-private 16-bit counters paired (p, p + 2^(W-1)) as in
-// hist_u8_kernel, zeroed after every tile so the per-tile row sums never carry.
+// One warp per tile; lane-private 16-bit counter pairs for (p, p + 2^(W-1)): the
+// low half counts both, the high half p + 2^(W-1); zeroed after every tile so
+// the per-tile row sums never carry.
 constexpr int H8_WARPS = 4;
 #ifndef K8_TILE
 #define K8_TILE 16384  // symbols per tile of every kernel of the single pass (measured: 8192 and 32768 slower)
@@ -79,9 +80,12 @@ __global__ void __launch_bounds__(H8_WARPS * 32) hist8_kernel(const uint8_t* __r
             const uint32_t lo = wd[u] & ((uint32_t)(HALF - 1) * 0x01010101u);
             const uint32_t hb = (wd[u] >> (W - 1)) & 0x01010101u;
             m16 |= ((hb * 0x01020408u) >> 24) << (4 * u);
+            // increment 0x00010001 for a value with its top bit set, else 1, straight
+            // from one PRMT: the low half counts both values of the pair, the high
+            // half the upper one
 #pragma unroll
             for (int b = 0; b < 4; ++b)
-              atomicAdd(c32w + prmt(lo, 0, 0x4440 + b) * 32, prmt(hb, 0, 0x4440 + b) * 0xFFFFu + 1u);
+              atomicAdd(c32w + prmt(lo, 0, 0x4440 + b) * 32, prmt(hb, 1u, 0x5054 + (b << 8)));
           }
           // lanes 4i..4i+3 hold 64 consecutive symbols: one level-0 word
           const uint32_t m32 = m16 | (__shfl_down_sync(FULL, m16, 1) << 16);
@@ -98,7 +102,7 @@ __global__ void __launch_bounds__(H8_WARPS * 32) hist8_kernel(const uint8_t* __r
         if (i < cnt) {
           v = text[first + i];
           vmax = max(vmax, v);
-          atomicAdd(c32w + (v & (HALF - 1)) * 32, ((v >> (W - 1)) & 1u) ? 0x10000u : 1u);
+          atomicAdd(c32w + (v & (HALF - 1)) * 32, ((v >> (W - 1)) & 1u) ? 0x10001u : 1u);
         }
         const uint32_t b = __ballot_sync(FULL, i < cnt && ((v >> (W - 1)) & 1u));
         if (lane == 0) l0[i0 >> 5] = b;
@@ -120,7 +124,7 @@ __global__ void __launch_bounds__(H8_WARPS * 32) hist8_kernel(const uint8_t* __r
         const uint4 q = row[k ^ (lane & 7)];
         s += (q.x + q.y) + (q.z + q.w);
       }
-      row_out[p] = s & 0xFFFFu;
+      row_out[p] = (s & 0xFFFFu) - (s >> 16);
       row_out[p + HALF] = s >> 16;
     }
     __syncwarp();
