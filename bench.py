@@ -65,6 +65,13 @@ def pass_plan(n: int, sym_bytes: int, sigma: int, kind: str):
         if tail and w - ell <= 8:
             out.append((ell, w - ell, 1, 0))
             break
+        in_b = sym_bytes if ell == 0 else bb(min(w - ell, vbits))
+        if ell == 0 and 8 * sym_bytes < w:
+            in_b = bb(w)  # widened text
+        if tail and 10 <= w - ell <= 16 and in_b == 2:  # k16.cuh: fused 2-byte pass, byte output
+            out.append((ell, w - ell - 8, 2, 1))
+            ell = w - 8
+            continue
         K = min(KMAX, w - ell)
         live_in = (w - ell) if kind == "wm" else w
         live_out = (w - ell - K) if kind == "wm" else w

@@ -213,7 +213,7 @@ __global__ void __launch_bounds__(256) scan8_apply_kernel(const uint32_t* __rest
 // counts per level and (optionally) the histogram.
 __global__ void __launch_bounds__(256) tables8_kernel(const int64_t* __restrict__ totals, int W, int kind,
                                                       int64_t* __restrict__ base, int64_t* __restrict__ zeros,
-                                                      int64_t* __restrict__ hist) {
+                                                      int64_t* __restrict__ hist, int64_t* __restrict__ baseW) {
   __shared__ int64_t s_tot[256];
   __shared__ int64_t s_cnt[8][256];
   const int nb = 1 << W;
@@ -229,6 +229,13 @@ __global__ void __launch_bounds__(256) tables8_kernel(const int64_t* __restrict_
     for (int e = 0; e < nb; ++e)
       if (!((e >> (W - 1 - tid)) & 1)) z += s_tot[e];
     zeros[tid] = z;
+  }
+  if (baseW && tid == 255) {  // WM level-W group starts (the 2-byte pass's output order)
+    int64_t run = 0;
+    for (int d = 0; d < nb; ++d) {
+      baseW[d] = run;
+      run += s_tot[rev_bits((unsigned)d, W)];
+    }
   }
   if (tid >= 32 && tid < 32 + W - 1) {  // thread of level j: its group sizes, then their prefix
     const int j = tid - 31;
@@ -413,6 +420,42 @@ struct Tab8 {
 };
 static_assert(sizeof(Tab8) % 16 == 0, "bulk-copy granularity");
 
+// Emission of levels 1..W-1 from a tile's level-bit arrays (NC + 4 words per
+// level, tile-local order): one destination word per task, the runs of all
+// levels flattened (consecutive tasks = consecutive words of one run, so the
+// stores of a warp coalesce); whole words stored, run-edge words OR-ed (runs of
+// neighbouring tiles share them; the levels were zeroed).
+template <int W, int NC>
+__device__ __forceinline__ void emit_levels8(const Tab8& tt, const uint32_t* bits, uint64_t* words, int64_t nwords,
+                                             int tid, int nthreads) {
+  constexpr int NR = (1 << W) - 2;
+#ifdef K8_NO_EMIT
+  const int total = 0;
+#else
+  const int total = tt.wpre[NR];
+#endif
+  for (int q = tid; q < total; q += nthreads) {
+    int r = 0;  // last run with wpre[r] <= q (empty runs share prefix values)
+#pragma unroll
+    for (int s = 128; s >= 1; s >>= 1)
+      if (r + s < NR && tt.wpre[r + s] <= q) r += s;
+    const int j = 31 - __clz(r + 2);
+    // 32-bit bit positions: the fused passes keep n < 2^32 - 64
+    const uint32_t g = tt.gs[r];
+    const uint32_t c = tt.cnt[r];
+    const uint32_t wd = (g >> 6) + (uint32_t)(q - tt.wpre[r]);
+    const uint32_t wb = wd << 6;
+    const uint32_t lo = g > wb ? g : wb;
+    const uint32_t hi = (g + c) < wb + 64 ? (g + c) : wb + 64;
+    const int len = (int)(hi - lo);
+    const uint32_t* L = bits + j * (NC + 4);
+    const uint64_t v = extract_bits(L, tt.ls[r] + (int)(lo - g), len) << (lo - wb);
+    uint64_t* dstw = words + (int64_t)j * nwords + wd;
+    if (len == 64) *dstw = v;
+    else if (v) atomicOr(reinterpret_cast<unsigned long long*>(dstw), (unsigned long long)v);
+  }
+}
+
 constexpr int T8_WARPS = 8;
 
 // One warp per tile: the tile's run tables (table8_warp) into the compact
@@ -469,7 +512,6 @@ __global__ void __launch_bounds__(K8Cfg<Q>::NT, K8Cfg<Q>::CTAS) level_pass8_kern
   constexpr int R = T / Q;  // region of run k
   constexpr int NC = T / 32;
   constexpr int NW = NT / 32;
-  constexpr int NR = (1 << W) - 2;
   constexpr int P = Q / 2;  // packed 16|16 scan values
   constexpr uint32_t B1 = 0x01010101u;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -630,35 +672,7 @@ __global__ void __launch_bounds__(K8Cfg<Q>::NT, K8Cfg<Q>::CTAS) level_pass8_kern
     bar_sync(1, NT);
   }
   bar_sync(1, NT);  // every warp's level bits are stored
-  // emission of levels 1..W-1: one destination word per task, the runs of all
-  // levels flattened (consecutive tasks = consecutive words of one run, so
-  // the stores of a warp coalesce); whole words stored, run-edge words OR-ed
-  // (runs of neighbouring tiles share them; the levels were zeroed)
-#ifdef K8_NO_EMIT
-  const int total = 0;
-#else
-  const int total = tt.wpre[NR];
-#endif
-  for (int q = tid; q < total; q += NT) {
-    int r = 0;  // last run with wpre[r] <= q (empty runs share prefix values)
-#pragma unroll
-    for (int s = 128; s >= 1; s >>= 1)
-      if (r + s < NR && tt.wpre[r + s] <= q) r += s;
-    const int j = 31 - __clz(r + 2);
-    // 32-bit bit positions: the single-pass path keeps n < 2^32 - 64
-    const uint32_t g = tt.gs[r];
-    const uint32_t c = tt.cnt[r];
-    const uint32_t wd = (g >> 6) + (uint32_t)(q - tt.wpre[r]);
-    const uint32_t wb = wd << 6;
-    const uint32_t lo = g > wb ? g : wb;
-    const uint32_t hi = (g + c) < wb + 64 ? (g + c) : wb + 64;
-    const int len = (int)(hi - lo);
-    const uint32_t* L = bits + j * (NC + 4);
-    const uint64_t v = extract_bits(L, tt.ls[r] + (int)(lo - g), len) << (lo - wb);
-    uint64_t* dstw = a.words + (int64_t)j * a.nwords + wd;
-    if (len == 64) *dstw = v;
-    else if (v) atomicOr(reinterpret_cast<unsigned long long*>(dstw), (unsigned long long)v);
-  }
+  emit_levels8<W, NC>(tt, bits, a.words, a.nwords, tid, NT);
 }
 
 // per-tile run tables, one warp per tile
@@ -797,7 +811,7 @@ int build_k8(const uint8_t* text, int64_t n, int64_t sigma, int w, int kind, uin
   e = cudaGetLastError();
   if (e != cudaSuccess) return (int)e;
   if (!tail) prof_mark(s, WVLT_STAGE_SCAN0);
-  tables8_kernel<<<1, 256, 0, s>>>(totals, w, kind, base, zeros, hist);
+  tables8_kernel<<<1, 256, 0, s>>>(totals, w, kind, base, zeros, hist, nullptr);
   ++g_launches;
   Pass8Args a;
   a.src = text;

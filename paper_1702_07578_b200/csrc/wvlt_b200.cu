@@ -569,9 +569,13 @@ struct Plan {
       off_buf0, off_buf1, off_wide;
   size_t tcnt_bytes, buf_bytes, total;
   // WM with w > 8: the last tail_w <= 8 levels (from tail_lvl) are one fused
-  // byte pass (k8.cuh) over the u8 output of the last generic pass; its
-  // workspace is the other ping-pong buffer
+  // byte pass (k8.cuh) over the u8 output of the stage before; its workspace
+  // is the other ping-pong buffer
   int tail_w, tail_lvl;
+  // WM, 2-byte input with 10..16 live bits (lean builds): the k16_w = live - 8
+  // levels from k16_lvl are one fused 2-byte pass (k16.cuh) whose byte output
+  // feeds the tail; output + its tables in the other ping-pong buffer
+  int k16_w, k16_lvl;
 };
 
 __host__ __device__ inline int64_t chain_off(int k) { return (1ll << k) - 1; }  // level-k table in a 2^(w+1)-1 array
@@ -1663,9 +1667,11 @@ int log2i(int v) {
   return r;
 }
 
-size_t k8_workspace_total(int64_t n, int w);  // k8.cuh
+size_t k8_workspace_total(int64_t n, int w);   // k8.cuh
+size_t k16_workspace_total(int64_t n, int w);  // k16.cuh
 
-bool make_plan(int64_t n, int sym_bytes, int64_t sigma, int kind, Plan* P) {
+// lean: a WM build without histogram / borders (the fused 2-byte pass needs it)
+bool make_plan(int64_t n, int sym_bytes, int64_t sigma, int kind, Plan* P, bool lean = true) {
   memset(P, 0, sizeof(*P));
   const int w = code_width_host(sigma);
   P->width = w;
@@ -1686,7 +1692,18 @@ bool make_plan(int64_t n, int sym_bytes, int64_t sigma, int kind, Plan* P) {
 #else
   const bool tail = false;
 #endif
+#ifndef WVLT_NO_K16
+  const bool k16 = tail && lean;
+#else
+  const bool k16 = false;
+#endif
   while (l < w && !(tail && w - l <= 8)) {
+    if (k16 && w - l <= 16 && w - l >= 10 && (p == 0 ? sb : bytes_for_bits(w - l)) == 2) {
+      P->k16_w = w - l - 8;
+      P->k16_lvl = l;
+      l += P->k16_w;
+      break;
+    }
     const int K = (w - l) < KMAX ? (w - l) : KMAX;
     P->lvl[p] = l;
     P->K[p] = K;
@@ -1742,6 +1759,7 @@ bool make_plan(int64_t n, int sym_bytes, int64_t sigma, int kind, Plan* P) {
   P->off_bsum = off;
   off = align_up(off + (size_t)NDIG * max_nblk * 8, 256);
   if (tail) max_buf = std::max(max_buf, k8_workspace_total(n, P->tail_w));
+  if (P->k16_w) max_buf = std::max(max_buf, align_up((size_t)n, 256) + k16_workspace_total(n, P->k16_w));
   P->buf_bytes = align_up(max_buf ? max_buf : 16, 256);
   P->off_buf0 = off;
   off += P->buf_bytes;
@@ -1954,6 +1972,7 @@ void prof_mark(cudaStream_t s, int stage_id) {
 }  // namespace
 
 #include "k8.cuh"
+#include "k16.cuh"
 
 namespace {
 int build_device_impl(const void* text, int sym_bytes, int64_t n, int64_t sigma, int kind, uint64_t* level_words,
@@ -2005,9 +2024,12 @@ int wvlt_profile_read(float* stage_ms, int* stage_ids, int max_stages) {
 size_t wvlt_workspace_bytes(int64_t n, int sym_bytes, int64_t sigma, int kind) {
   Plan P;
   if (n < 0 || !(sym_bytes == 1 || sym_bytes == 2 || sym_bytes == 4)) return 0;
-  if (!make_plan(n, sym_bytes, sigma, kind, &P)) return 0;
-  if (k8_eligible(sym_bytes, P.width, n) && !P.widen_bytes) return std::max(P.total, k8_layout(n, P.width).total);
-  return P.total;
+  if (!make_plan(n, sym_bytes, sigma, kind, &P, true)) return 0;
+  Plan P2;
+  make_plan(n, sym_bytes, sigma, kind, &P2, false);
+  const size_t total = std::max(P.total, P2.total);
+  if (k8_eligible(sym_bytes, P.width, n) && !P.widen_bytes) return std::max(total, k8_layout(n, P.width).total);
+  return total;
 }
 
 int wvlt_histogram(const void* text, int sym_bytes, int64_t n, int64_t sigma, int64_t* hist, int32_t* status,
@@ -2042,7 +2064,10 @@ int build_device_impl(const void* text, int sym_bytes, int64_t n, int64_t sigma,
   if (!(sym_bytes == 1 || sym_bytes == 2 || sym_bytes == 4) || n < 0 || sigma < 1) return WVLT_E_ARG;
   if (kind != WVLT_KIND_WT && kind != WVLT_KIND_WM) return WVLT_E_ARG;
   Plan P;
-  if (!make_plan(n, sym_bytes, sigma, kind, &P)) return WVLT_E_WIDTH;
+  // lean WM build: no histogram / borders requested -> no K1 histogram and no
+  // K2 tables; each pass's tables come from its own tile-count scan
+  const bool lean = kind == WVLT_KIND_WM && !hist && !borders;
+  if (!make_plan(n, sym_bytes, sigma, kind, &P, lean)) return WVLT_E_WIDTH;
   const int w = P.width;
   cudaStream_t s = (cudaStream_t)stream;
   cudaError_t e;
@@ -2094,14 +2119,16 @@ int build_device_impl(const void* text, int sym_bytes, int64_t n, int64_t sigma,
 
   g_prof.n = 0;
   prof_mark(s, -1);
-  // (the fused tail writes / zeroes its own levels)
-  e = cudaMemsetAsync(level_words, 0, (size_t)(P.tail_w ? P.tail_lvl : w) * nwords * 8, s);
-  if (e != cudaSuccess) return (int)e;
-  e = cudaMemsetAsync(ws + P.off_tcnt[0], 0, P.tcnt_bytes, s);
-  if (e != cudaSuccess) return (int)e;
-  // lean WM build: no histogram / borders requested -> no K1 histogram and no
-  // K2 tables; each pass's tables come from its own tile-count scan
-  const bool lean = kind == WVLT_KIND_WM && !hist && !borders;
+  // (the fused passes write / zero their own levels)
+  const int fused_lvl = P.k16_w ? P.k16_lvl : P.tail_w ? P.tail_lvl : w;
+  if (fused_lvl > 0) {
+    e = cudaMemsetAsync(level_words, 0, (size_t)fused_lvl * nwords * 8, s);
+    if (e != cudaSuccess) return (int)e;
+  }
+  if (P.npass > 0) {
+    e = cudaMemsetAsync(ws + P.off_tcnt[0], 0, P.tcnt_bytes, s);
+    if (e != cudaSuccess) return (int)e;
+  }
   unsigned long long* hw = (unsigned long long*)(chain + chain_off(w));
   if (!lean) {
     e = cudaMemsetAsync(hw, 0, ((size_t)1 << w) * 8, s);
@@ -2124,11 +2151,14 @@ int build_device_impl(const void* text, int sym_bytes, int64_t n, int64_t sigma,
     src0 = wide;
   }
   prof_mark(s, WVLT_STAGE_MEMSET);
-  g_launches += lean ? 1 : (P.in_bytes[0] == 1 && w <= 8 && P.tile[0] == TILE_U8 && (((uintptr_t)src0) & 15) == 0 ? 1 : 2);
-  if (lean) {
+  if (P.npass == 0) {
+    e = cudaSuccess;  // (lean, the fused 2-byte pass first: its digit kernel does the range check)
+  } else if (lean) {
+    ++g_launches;
     e = launch_digits_fast(src0, P.in_bytes[0], n, w, sigma, P.K[0], P.tile[0], P.ntiles[0],
                            (uint32_t*)(ws + P.off_tcnt[0]), st_flag, s);
   } else {
+    g_launches += P.in_bytes[0] == 1 && w <= 8 && P.tile[0] == TILE_U8 && (((uintptr_t)src0) & 15) == 0 ? 1 : 2;
     e = launch_hist_build(src0, P.in_bytes[0], n, w, P.K[0], P.tile[0], P.ntiles[0], hw,
                           (uint32_t*)(ws + P.off_tcnt[0]), st_flag, s);
   }
@@ -2204,11 +2234,27 @@ int build_device_impl(const void* text, int sym_bytes, int64_t n, int64_t sigma,
     if (pass_done) pass_done(ctx, P.lvl[p], P.K[p]);
     cur = pa.dst;
   }
+  int curbuf = P.npass > 0 ? ((P.npass - 1) & 1) : -1;  // bufs[] index holding cur, -1 = the text
+  int stage = P.npass;
+  if (P.k16_w) {
+    const int ob = curbuf == 0 ? 1 : 0;
+    uint8_t* out = (uint8_t*)bufs[ob];
+    const int64_t lk = P.k16_lvl;
+    const uint32_t vmax_ok = (uint32_t)std::min<int64_t>(sigma - 1, 0xFFFF);
+    const int check = curbuf < 0 && vmax_ok < 0xFFFFu ? 1 : 0;  // text input: symbols must be < sigma
+    const int rc = build_k16((const uint16_t*)cur, n, P.k16_w, level_words + lk * nwords, zeros ? zeros + lk : nullptr,
+                             out, out + align_up((size_t)n, 256), st_flag, vmax_ok, check, s, pass_done, ctx,
+                             (int)lk, stage);
+    if (rc) return rc;
+    ++stage;
+    cur = out;
+    curbuf = ob;
+  }
   if (P.tail_w) {
     const int64_t lt = P.tail_lvl;
     return build_k8((const uint8_t*)cur, n, (int64_t)1 << P.tail_w, P.tail_w, kind, level_words + lt * nwords,
-                    zeros ? zeros + lt : nullptr, nullptr, bufs[P.npass & 1], st_flag, s, pass_done, ctx,
-                    (int)lt, P.npass);
+                    zeros ? zeros + lt : nullptr, nullptr, bufs[curbuf == 0 ? 1 : 0], st_flag, s, pass_done, ctx,
+                    (int)lt, stage);
   }
   return 0;
 }
