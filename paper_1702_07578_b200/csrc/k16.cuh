@@ -1,13 +1,14 @@
 // Fused pass for the first levels of a 2-byte WM build (10..16 live bits).
 //
 // The W = live - 8 levels whose digit is the high byte come from one
-// shared-memory tile, as in the byte pass (k8.cuh), but the tile's high and low
-// bytes sit in two planes that move together: every split sorts both planes
-// of a run with the same PRMT selector and stores the two bytes at the same
-// offset of the two planes.  After the W-th split the low plane is in level-W
-// order; each digit group's bytes leave as one contiguous run of a byte text,
-// which the fused byte tail (build_k8) turns into the last 8 levels.  No
-// 2-byte intermediate order ever goes back to HBM.
+// shared-memory tile, as in the byte pass (k8.cuh): a split splits a run's
+// 2-byte elements into a high-byte and a low-byte register pair, sorts both
+// with the same PRMT selector (computed from the high bytes' flags), re-pairs
+// them and stores one 16-bit element per symbol (measured: 8% faster than two
+// byte planes).  After the W-th split the tile is in level-W order; each digit
+// group's low bytes leave as one contiguous run of a byte text, which the
+// fused byte tail (build_k8) turns into the last 8 levels.  No 2-byte
+// intermediate order ever goes back to HBM.
 // Included from wvlt_b200.cu after k8.cuh (same translation unit).
 
 namespace {
@@ -152,7 +153,7 @@ __global__ void __launch_bounds__(K16_NT, K16_CTAS) level_pass16_kernel(const Pa
   constexpr int P = Q / 2;
   constexpr uint32_t B1 = 0x01010101u;
   extern __shared__ __align__(128) unsigned char smem[];
-  // [buffer 0: staged tile, then orders 2, 4, .. as (high plane | low plane)
+  // [buffer 0: staged tile, then orders 2, 4, .. (2-byte elements)
   //  | buffer 1: orders 1, 3, .. | run table | level bits of levels 1..W-1]
   Tab8& tt = *reinterpret_cast<Tab8*>(smem + 4 * T);
   uint32_t* bits = reinterpret_cast<uint32_t*>(smem + 4 * T + sizeof(Tab8)) - (NC + 4);
@@ -217,25 +218,15 @@ __global__ void __launch_bounds__(K16_NT, K16_CTAS) level_pass16_kernel(const Pa
   for (int j = 0; j < W; ++j) {
     const int sh = W - 1 - j;
     uint32_t x[2 * Q], y[2 * Q];  // high / low bytes of the thread's runs
-    if (j == 0) {
+    {
+      const unsigned char* cur = smem + (size_t)(j & 1) * 2 * T;
 #pragma unroll
       for (int k = 0; k < Q; ++k) {
-        const uint4 qv = reinterpret_cast<const uint4*>(smem + 2 * (k * R))[tid];
+        const uint4 qv = reinterpret_cast<const uint4*>(cur + 2 * (k * R))[tid];
         x[2 * k] = prmt(qv.x, qv.y, 0x7531);
         x[2 * k + 1] = prmt(qv.z, qv.w, 0x7531);
         y[2 * k] = prmt(qv.x, qv.y, 0x6420);
         y[2 * k + 1] = prmt(qv.z, qv.w, 0x6420);
-      }
-    } else {
-      const unsigned char* cur = smem + (size_t)(j & 1) * 2 * T;
-#pragma unroll
-      for (int k = 0; k < Q; ++k) {
-        const uint2 hv = reinterpret_cast<const uint2*>(cur + k * R)[tid];
-        const uint2 lv = reinterpret_cast<const uint2*>(cur + T + k * R)[tid];
-        x[2 * k] = hv.x;
-        x[2 * k + 1] = hv.y;
-        y[2 * k] = lv.x;
-        y[2 * k + 1] = lv.y;
       }
     }
     uint32_t m[Q], ones[Q];
@@ -268,30 +259,26 @@ __global__ void __launch_bounds__(K16_NT, K16_CTAS) level_pass16_kernel(const Pa
       run_tot += (int)(tot >> 16);
     }
     const int Z = T - run_tot;
-    // order j + 1 into buffer (j + 1) & 1: high plane at +0 (not needed after
-    // the last split), low plane at +T
+    // order j + 1 into buffer (j + 1) & 1
     const uint32_t nxt = sbase + (uint32_t)((j + 1) & 1) * 2 * T;
 #pragma unroll
     for (int k = 0; k < Q; ++k) {
       const uint32_t sel = s_lut[m[k]];
-      const uint32_t sh2[2] = {prmt(x[2 * k], x[2 * k + 1], sel), prmt(x[2 * k], x[2 * k + 1], sel >> 16)};
-      const uint32_t sl2[2] = {prmt(y[2 * k], y[2 * k + 1], sel), prmt(y[2 * k], y[2 * k + 1], sel >> 16)};
+      const uint32_t h0 = prmt(x[2 * k], x[2 * k + 1], sel), h1 = prmt(x[2 * k], x[2 * k + 1], sel >> 16);
+      const uint32_t l0 = prmt(y[2 * k], y[2 * k + 1], sel), l1 = prmt(y[2 * k], y[2 * k + 1], sel >> 16);
+      const uint32_t e[4] = {prmt(l0, h0, 0x5140), prmt(l0, h0, 0x7362), prmt(l1, h1, 0x5140), prmt(l1, h1, 0x7362)};
       const int nz = 8 - (int)ones[k];
-      const uint32_t za = opaque(nxt + (uint32_t)(k * R + 8 * tid - opre[k]));
-      const uint32_t oa = opaque(nxt + (uint32_t)(Z + opre[k] - nz));
+      const uint32_t za = opaque(nxt + 2u * (uint32_t)(k * R + 8 * tid - opre[k]));
+      const uint32_t oa = opaque(nxt + 2u * (uint32_t)(Z + opre[k] - nz));
       const uint32_t F = (uint32_t)(15 - nz) << 28;
       const uint32_t dz = oa - za;
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk) {
         uint64_t t;
         asm("mad.wide.u32 %0, %1, 1, %2;" : "=l"(t) : "r"(F), "l"((uint64_t)(kk + 1) << 28));
-        const uint32_t addr = za + (uint32_t)(t >> 32) * dz + kk;
-        const uint32_t vl = sl2[kk >> 2] >> (8 * (kk & 3));
-        asm volatile("st.shared.u8 [%0+%2], %1;" ::"r"(addr), "r"(vl), "n"(T) : "memory");
-        if (j + 1 < W) {
-          const uint32_t vh = sh2[kk >> 2] >> (8 * (kk & 3));
-          asm volatile("st.shared.u8 [%0], %1;" ::"r"(addr), "r"(vh) : "memory");
-        }
+        const uint32_t addr = za + (uint32_t)(t >> 32) * dz + 2 * kk;
+        const uint32_t v = (kk & 1) ? (e[kk >> 1] >> 16) : e[kk >> 1];
+        asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
       }
     }
     bar_sync(1, NT);
@@ -299,13 +286,14 @@ __global__ void __launch_bounds__(K16_NT, K16_CTAS) level_pass16_kernel(const Pa
   // levels 1..W-1 as flattened destination-word tasks (as in the byte pass)
   emit_levels8<W, NC>(tt, bits, a.words, a.nwords, tid, NT);
   // the low bytes of each level-W group: one contiguous run of the byte text
-  const uint8_t* lo = smem + (size_t)(W & 1) * 2 * T + T;
+  const uint8_t* lo = smem + (size_t)(W & 1) * 2 * T;
+  constexpr int LS = 2;  // low byte of element p at byte 2 p
   for (int r = wid; r < NB; r += NW) {
     const int c = s_cW[r];
     if (!c) continue;
     uint8_t* dst = a.out + s_gW[r];
-    const uint8_t* sp = lo + s_lsW[r];
-    for (int i = lane; i < c; i += 32) dst[i] = sp[i];
+    const uint8_t* sp = lo + LS * s_lsW[r];
+    for (int i = lane; i < c; i += 32) dst[i] = sp[LS * i];
   }
 }
 
