@@ -212,3 +212,22 @@ def test_unaligned_device_text(sigma):
         assert np.array_equal(words, ow), kind
         if kind == "wm":
             assert zeros == oz
+
+
+@pytest.mark.parametrize("sigma", [300, 1000, 5000, 1 << 16])
+def test_byte_storage_wide_alphabet_device_text(sigma):
+    """A device text stored narrower than the code width (u8 storage, w > 8 or u16
+    storage at w = 16): the build widens it and runs the fused 2-byte pass and
+    the byte tail; output equals the oracle's."""
+    from paper_1702_07578_b200.device import DeviceBuilder
+
+    rng = np.random.default_rng(sigma + 5)
+    n = 5 * 8192 + 4321
+    hi = min(sigma, 256 if sigma <= 5000 else sigma)
+    host = rng.integers(0, hi, n).astype(np.uint8 if hi <= 256 else np.uint16)
+    dev = torch.from_numpy(host).cuda()
+    b = DeviceBuilder()
+    words, zeros, _ = b.build(dev, sigma, "wm").to_host()
+    ow, oz, _ = oracle.build(host, sigma, "wm", "pc")
+    assert np.array_equal(words, ow)
+    assert zeros == oz
