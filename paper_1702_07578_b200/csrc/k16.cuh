@@ -301,12 +301,8 @@ template <int W>
 cudaError_t launch_hist16(const uint16_t* src, int64_t n, int64_t ntiles, uint32_t vmax_ok, int check,
                           uint32_t* tcnt8, uint64_t* level0, int64_t nwords, int32_t* status, cudaStream_t s) {
   constexpr size_t sb = (size_t)H8_WARPS * (1 << (W - 1)) * 32 * 4;
-  static bool set = false;
-  if (!set) {
-    cudaError_t e = cudaFuncSetAttribute(hist16_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
-    if (e != cudaSuccess) return e;
-    set = true;
-  }
+  cudaError_t e0 = ensure_smem_attr((const void*)hist16_kernel<W>, (int)sb);
+  if (e0 != cudaSuccess) return e0;
   const int per_sm = (int)std::min<size_t>(8, (size_t)(220 * 1024) / (sb + 1024));
   const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((ntiles + H8_WARPS - 1) / H8_WARPS,
                                                                  (int64_t)sm_count() * per_sm));
@@ -320,14 +316,8 @@ cudaError_t launch_pass16(const Pass16Args& a, const Tab8* tabs, cudaStream_t s)
   constexpr int T = K16_TILE;
   const size_t smem = 4 * (size_t)T + sizeof(Tab8) + (size_t)(W - 1) * (T / 32 + 4) * 4;
   auto kern = level_pass16_kernel<W>;
-  static bool set = false;
-  if (!set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
-    if (e != cudaSuccess) return e;
-    set = true;
-  }
+  cudaError_t e0 = ensure_smem_attr((const void*)kern, (int)smem, true);
+  if (e0 != cudaSuccess) return e0;
   kern<<<(unsigned)a.ntiles, K16_NT, smem, s>>>(a, tabs);
   return cudaGetLastError();
 }

@@ -679,12 +679,8 @@ __global__ void __launch_bounds__(K8Cfg<Q>::NT, K8Cfg<Q>::CTAS) level_pass8_kern
 template <int W>
 cudaError_t launch_tiles8(const Pass8Args& a, Tab8* tabs, cudaStream_t s) {
   constexpr size_t sm = (size_t)T8_WARPS * sizeof(Tables8);
-  static bool set = false;
-  if (!set) {
-    cudaError_t e = cudaFuncSetAttribute(tiles8_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    if (e != cudaSuccess) return e;
-    set = true;
-  }
+  cudaError_t e0 = ensure_smem_attr((const void*)tiles8_kernel<W>, (int)sm);
+  if (e0 != cudaSuccess) return e0;
   const int64_t blocks = std::min<int64_t>((a.ntiles + T8_WARPS - 1) / T8_WARPS, (int64_t)sm_count() * 4);
   tiles8_kernel<W><<<(unsigned)blocks, T8_WARPS * 32, sm, s>>>(a, tabs);
   return cudaGetLastError();
@@ -696,14 +692,8 @@ cudaError_t launch_pass8(const Pass8Args& a, Tab8* tabs, cudaStream_t s) {
   // level bits of levels 1..W-1 only (level 0 comes from hist8_kernel)
   const size_t smem = 2 * (size_t)T + sizeof(Tab8) + (size_t)(W - 1) * (T / 32 + 4) * 4;
   auto kern = level_pass8_kernel<W, K8_Q>;
-  static bool set = false;
-  if (!set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
-    if (e != cudaSuccess) return e;
-    set = true;
-  }
+  cudaError_t e0 = ensure_smem_attr((const void*)kern, (int)smem, true);
+  if (e0 != cudaSuccess) return e0;
   kern<<<(unsigned)a.ntiles, K8Cfg<K8_Q>::NT, smem, s>>>(a, tabs);
   return cudaGetLastError();
 }
@@ -712,12 +702,8 @@ template <int W>
 cudaError_t launch_hist8(const uint8_t* text, int64_t n, int64_t ntiles, uint32_t vmax_ok, int check,
                          uint32_t* tcnt8, uint64_t* level0, int64_t nwords, int32_t* status, cudaStream_t s) {
   constexpr size_t sb = (size_t)H8_WARPS * (1 << (W - 1)) * 32 * 4;
-  static bool set = false;
-  if (!set) {
-    cudaError_t e = cudaFuncSetAttribute(hist8_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);
-    if (e != cudaSuccess) return e;
-    set = true;
-  }
+  cudaError_t e0 = ensure_smem_attr((const void*)hist8_kernel<W>, (int)sb);
+  if (e0 != cudaSuccess) return e0;
   const int per_sm = (int)std::min<size_t>(8, (size_t)(220 * 1024) / (sb + 1024));
   const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((ntiles + H8_WARPS - 1) / H8_WARPS,
                                                                  (int64_t)sm_count() * per_sm));

@@ -38,6 +38,8 @@
 // P = q 2^j + e.  Both tables come from the histogram alone (K2).
 
 #include <cuda_runtime.h>
+#include <mutex>
+#include <unordered_map>
 
 #include <algorithm>
 #include <stdint.h>
@@ -1771,17 +1773,37 @@ bool make_plan(int64_t n, int sym_bytes, int64_t sigma, int kind, Plan* P, bool 
   return true;
 }
 
+int sm_count();
+
+// Once per (kernel, device): the dynamic shared-memory limit above 48 KB (and
+// optionally the max-shared carveout).  Function attributes are per device, so
+// a process driving several GPUs sets them on each.
+cudaError_t ensure_smem_attr(const void* fn, int bytes, bool carveout = false) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, uint64_t> done;  // device bitmask per kernel
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  uint64_t& mask = done[fn];
+  if ((mask >> (dev & 63)) & 1) return cudaSuccess;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) return e;
+  if (carveout) {
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
+    if (e != cudaSuccess) return e;
+  }
+  mask |= 1ull << (dev & 63);
+  return cudaSuccess;
+}
+
 template <typename TIn, typename TOut, int K>
 cudaError_t launch_pass_t(const PassArgs& a, int64_t ntiles, cudaStream_t s) {
   constexpr int E = sizeof(TIn) == 4 ? 8 : E_SMALL;
   using S = PassSmem<TIn, K, E>;
   auto kern = level_pass_kernel<TIn, TOut, K, E>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::total);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  cudaError_t e = ensure_smem_attr((const void*)kern, (int)S::total);
+  if (e != cudaSuccess) return e;
   kern<<<(unsigned)ntiles, PASS_THREADS + TAB_WARP_THREADS, S::total, s>>>(a);
   return cudaGetLastError();
 }
@@ -1802,14 +1824,8 @@ template <int K>
 cudaError_t launch_pass_u8(const PassArgs& a, int64_t ntiles, cudaStream_t s) {
   using S = U8Smem<K>;
   auto kern = level_pass_u8_kernel<K>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::total);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  cudaError_t e = ensure_smem_attr((const void*)kern, (int)S::total, true);
+  if (e != cudaSuccess) return e;
   // persistent CTAs: U8_CTAS_PER_SM per SM, tiles strided by the grid
 #ifndef U8_GRID_PER_SM
 #define U8_GRID_PER_SM 0  // 0: one CTA per tile (measured faster than persistent CTAs)
@@ -1858,11 +1874,7 @@ cudaError_t launch_hist_generic(const void* text, int sym_bytes, int64_t n, int 
   const int blocks = sm_count() * per_sm;
 #define WVLT_HG(T)                                                                                          \
   do {                                                                                                      \
-    static bool set = false;                                                                                \
-    if (!set) {                                                                                             \
-      cudaFuncSetAttribute(hist_generic_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 1024); \
-      set = true;                                                                                           \
-    }                                                                                                       \
+    ensure_smem_attr((const void*)hist_generic_kernel<T>, 128 * 1024);                                      \
     hist_generic_kernel<T><<<blocks, HISTG_THREADS, sb, s>>>((const T*)text, n, w, hist, status);          \
   } while (0)
   if (sym_bytes == 1) WVLT_HG(uint8_t);
@@ -1884,11 +1896,7 @@ cudaError_t launch_hist_build(const void* text, int sym_bytes, int64_t n, int w,
     const int nd0 = 1 << K0;
 #define WVLT_H8(WW)                                                                                         \
   do {                                                                                                      \
-    static bool set = false;                                                                                \
-    if (!set) {                                                                                             \
-      cudaFuncSetAttribute(hist_u8_kernel<WW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sb);       \
-      set = true;                                                                                           \
-    }                                                                                                       \
+    ensure_smem_attr((const void*)hist_u8_kernel<WW>, (int)sb);                                             \
     hist_u8_kernel<WW><<<hb, HIST_WARPS * 32, sb, s>>>(t, n, dshift, nd0, hist, tcnt0, ntiles0, status);    \
   } while (0)
     switch (w) {
