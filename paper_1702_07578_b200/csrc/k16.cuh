@@ -32,12 +32,13 @@ __global__ void __launch_bounds__(H8_WARPS * 32) hist16_kernel(const uint16_t* _
                                                               int32_t* __restrict__ status) {
   constexpr int NB = 1 << W;
   constexpr int HALF = NB / 2;
-  constexpr int WORDS = HALF * 32;
+  constexpr int C = H8_COLS;  // counter columns per warp (lanes l and l + C share one)
+  constexpr int WORDS = HALF * C;
   constexpr uint32_t B1 = 0x01010101u;
   extern __shared__ __align__(16) uint32_t s_cols[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   uint32_t* c32 = s_cols + (size_t)wid * WORDS;
-  uint32_t* c32w = c32 + lane;
+  uint32_t* c32w = c32 + (lane & (C - 1));
   for (int i = lane; i < WORDS; i += 32) c32[i] = 0;
   __syncwarp();
   uint32_t vmax = 0;
@@ -80,7 +81,7 @@ __global__ void __launch_bounds__(H8_WARPS * 32) hist16_kernel(const uint16_t* _
             m8 |= ((hb * 0x01020408u) >> 24) << (4 * u);
 #pragma unroll
             for (int b = 0; b < 4; ++b)
-              atomicAdd(c32w + prmt(lo, 0, 0x4440 + b) * 32, prmt(hb, 1u, 0x5054 + (b << 8)));
+              atomicAdd(c32w + prmt(lo, 0, 0x4440 + b) * C, prmt(hb, 1u, 0x5054 + (b << 8)));
           }
           // lanes 8i..8i+7 hold 64 consecutive symbols: one level-l0 word
           uint32_t m32 = m8 | (__shfl_down_sync(FULL, m8, 1) << 8);
@@ -99,7 +100,7 @@ __global__ void __launch_bounds__(H8_WARPS * 32) hist16_kernel(const uint16_t* _
           v = src[first + i];
           vmax = max(vmax, v);
           const uint32_t d = v >> 8;
-          atomicAdd(c32w + (d & (HALF - 1)) * 32, ((d >> (W - 1)) & 1u) ? 0x10001u : 1u);
+          atomicAdd(c32w + (d & (HALF - 1)) * C, ((d >> (W - 1)) & 1u) ? 0x10001u : 1u);
         }
         const uint32_t b = __ballot_sync(FULL, i < cnt && (((v >> 8) >> (W - 1)) & 1u));
         if (lane == 0) l0[i0 >> 5] = b;
@@ -109,11 +110,11 @@ __global__ void __launch_bounds__(H8_WARPS * 32) hist16_kernel(const uint16_t* _
     __syncwarp();
     uint32_t* row_out = tcnt8 + t * NB;
     for (int p = lane; p < HALF; p += 32) {
-      const uint4* row = reinterpret_cast<const uint4*>(c32 + p * 32);
+      const uint4* row = reinterpret_cast<const uint4*>(c32 + p * C);
       uint32_t s = 0;
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const uint4 qq = row[k ^ (lane & 7)];
+      for (int k = 0; k < C / 4; ++k) {
+        const uint4 qq = row[k ^ (lane & (C / 4 - 1))];
         s += (qq.x + qq.y) + (qq.z + qq.w);
       }
       row_out[p] = (s & 0xFFFFu) - (s >> 16);
@@ -300,7 +301,7 @@ __global__ void __launch_bounds__(K16_NT, K16_CTAS) level_pass16_kernel(const Pa
 template <int W>
 cudaError_t launch_hist16(const uint16_t* src, int64_t n, int64_t ntiles, uint32_t vmax_ok, int check,
                           uint32_t* tcnt8, uint64_t* level0, int64_t nwords, int32_t* status, cudaStream_t s) {
-  constexpr size_t sb = (size_t)H8_WARPS * (1 << (W - 1)) * 32 * 4;
+  constexpr size_t sb = (size_t)H8_WARPS * (1 << (W - 1)) * H8_COLS * 4;
   cudaError_t e0 = ensure_smem_attr((const void*)hist16_kernel<W>, (int)sb);
   if (e0 != cudaSuccess) return e0;
   const int per_sm = (int)std::min<size_t>(8, (size_t)(220 * 1024) / (sb + 1024));

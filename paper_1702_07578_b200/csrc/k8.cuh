@@ -26,6 +26,9 @@ constexpr int H8_WARPS = 4;
 #ifndef K8_CTAS
 #define K8_CTAS (K8_TILE == 8192 ? 7 : K8_TILE == 16384 ? 4 : 2)  // pass CTAs per SM (shared memory / registers)
 #endif
+#ifndef H8_COLS
+#define H8_COLS 16  // counter columns per warp (measured: 16 < 32 < 8 ms; more warps per SM)
+#endif
 #ifndef H8_BATCH
 #define H8_BATCH 4  // 16-byte loads in flight per lane (measured: 4 < 8 < 16)
 #endif
@@ -39,11 +42,12 @@ __global__ void __launch_bounds__(H8_WARPS * 32) hist8_kernel(const uint8_t* __r
                                                              int64_t nwords, int32_t* __restrict__ status) {
   constexpr int NB = 1 << W;
   constexpr int HALF = NB / 2;
-  constexpr int WORDS = HALF * 32;
+  constexpr int C = H8_COLS;  // counter columns per warp (lanes l and l + C share one)
+  constexpr int WORDS = HALF * C;
   extern __shared__ __align__(16) uint32_t s_cols[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   uint32_t* c32 = s_cols + (size_t)wid * WORDS;
-  uint32_t* c32w = c32 + lane;
+  uint32_t* c32w = c32 + (lane & (C - 1));
   for (int i = lane; i < WORDS; i += 32) c32[i] = 0;
   __syncwarp();
   uint32_t vmax = 0;
@@ -85,7 +89,7 @@ __global__ void __launch_bounds__(H8_WARPS * 32) hist8_kernel(const uint8_t* __r
             // half the upper one
 #pragma unroll
             for (int b = 0; b < 4; ++b)
-              atomicAdd(c32w + prmt(lo, 0, 0x4440 + b) * 32, prmt(hb, 1u, 0x5054 + (b << 8)));
+              atomicAdd(c32w + prmt(lo, 0, 0x4440 + b) * C, prmt(hb, 1u, 0x5054 + (b << 8)));
           }
           // lanes 4i..4i+3 hold 64 consecutive symbols: one level-0 word
           const uint32_t m32 = m16 | (__shfl_down_sync(FULL, m16, 1) << 16);
@@ -102,7 +106,7 @@ __global__ void __launch_bounds__(H8_WARPS * 32) hist8_kernel(const uint8_t* __r
         if (i < cnt) {
           v = text[first + i];
           vmax = max(vmax, v);
-          atomicAdd(c32w + (v & (HALF - 1)) * 32, ((v >> (W - 1)) & 1u) ? 0x10001u : 1u);
+          atomicAdd(c32w + (v & (HALF - 1)) * C, ((v >> (W - 1)) & 1u) ? 0x10001u : 1u);
         }
         const uint32_t b = __ballot_sync(FULL, i < cnt && ((v >> (W - 1)) & 1u));
         if (lane == 0) l0[i0 >> 5] = b;
@@ -117,11 +121,11 @@ __global__ void __launch_bounds__(H8_WARPS * 32) hist8_kernel(const uint8_t* __r
     // lanes of a wavefront hit 8 different bank quads)
     uint32_t* row_out = tcnt8 + t * NB;
     for (int p = lane; p < HALF; p += 32) {
-      const uint4* row = reinterpret_cast<const uint4*>(c32 + p * 32);
+      const uint4* row = reinterpret_cast<const uint4*>(c32 + p * C);
       uint32_t s = 0;
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const uint4 q = row[k ^ (lane & 7)];
+      for (int k = 0; k < C / 4; ++k) {
+        const uint4 q = row[k ^ (lane & (C / 4 - 1))];
         s += (q.x + q.y) + (q.z + q.w);
       }
       row_out[p] = (s & 0xFFFFu) - (s >> 16);
@@ -701,7 +705,7 @@ cudaError_t launch_pass8(const Pass8Args& a, Tab8* tabs, cudaStream_t s) {
 template <int W>
 cudaError_t launch_hist8(const uint8_t* text, int64_t n, int64_t ntiles, uint32_t vmax_ok, int check,
                          uint32_t* tcnt8, uint64_t* level0, int64_t nwords, int32_t* status, cudaStream_t s) {
-  constexpr size_t sb = (size_t)H8_WARPS * (1 << (W - 1)) * 32 * 4;
+  constexpr size_t sb = (size_t)H8_WARPS * (1 << (W - 1)) * H8_COLS * 4;
   cudaError_t e0 = ensure_smem_attr((const void*)hist8_kernel<W>, (int)sb);
   if (e0 != cudaSuccess) return e0;
   const int per_sm = (int)std::min<size_t>(8, (size_t)(220 * 1024) / (sb + 1024));
