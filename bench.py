@@ -225,6 +225,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-wt", action="store_true")
+    ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
+                    help="N > 1: merge over peer memory (symmetric memory, one kernel) or NCCL all_to_all + merge")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -259,16 +261,26 @@ def main():
             dist.barrier()
 
     sharded = world > 1
+    transport = args.transport
     if sharded:
         from paper_1702_07578_b200.distributed import CudaOps, build_sharded
 
         ops = CudaOps(dev)
+        if transport == "p2p":
+            try:  # symmetric memory needs peer-accessible GPUs (NVLink); otherwise NCCL
+                ops.peer_buffer(1)
+            except Exception:  # noqa: BLE001
+                transport = "nccl"
+        ok = torch.tensor([1 if transport == "p2p" else 0], device=dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        transport = "p2p" if int(ok.item()) else "nccl"
 
     def one_build(kind_):
         if sharded:
-            # one WM/WT over the whole job's world * n symbols: local builds,
-            # NCCL histogram all_gather + bit-segment all_to_all, shift-merge
-            return build_sharded(text, sigma, kind_, ops=ops)
+            # one WM/WT over the whole job's world * n symbols: local builds, NCCL
+            # histogram all_gather, then the merge over peer memory (p2p) or the
+            # bit-segment all_to_all + shift-merge (nccl)
+            return build_sharded(text, sigma, kind_, ops=ops, transport=transport)
         return builder.build(text, sigma, kind_, outputs=outs, check=False)
 
     def timed(kind_, steps, warmup):
@@ -317,6 +329,18 @@ def main():
     tf = ROOT / "profiles" / f"ncu_traffic_{args.config}_{kind}.json"
     if tf.exists():
         traffic = json.loads(tf.read_text()).get(dominant)
+    # the fused pass is bound by the shared-memory pipe, not HBM: its ncu wavefront
+    # count per launch over (SMs x cycles of its CUDA-event duration at the sampled clock)
+    limiter = None
+    sf = ROOT / "profiles" / f"ncu_smem_{args.config}_{kind}.json"
+    if sf.exists() and clocks.get("sm_mhz"):
+        wf = json.loads(sf.read_text()).get(dominant)
+        if wf:
+            sms = torch.cuda.get_device_properties(dev).multi_processor_count
+            per_cycle = wf / (sms * stages[dominant] * 1e-3 * clocks["sm_mhz"] * 1e6)
+            limiter = {"resource": "shared-memory pipe", "unit": "wavefronts / SM / cycle", "achieved": per_cycle,
+                       "peak": 1.0, "frac": per_cycle, "wavefronts_per_launch": wf,
+                       "source": f"profiles/ncu_smem_{args.config}_{kind}.json (ncu --set full, one launch)"}
 
     value = world * n / (ms * 1e-3)
     mbytes = metric_bytes(n, sym_bytes, sigma)
@@ -327,10 +351,12 @@ def main():
         "config": {"workload": args.config, "description": workloads.DESCRIPTIONS[args.config], "kind": kind,
                    "n_per_gpu": n, "sigma": sigma, "levels": code_width(sigma), "passes": npass,
                    "l2": "inputs larger than L2 (text %d MiB per GPU vs 126 MB L2); no flush" % (n * sym_bytes >> 20),
-                   "parallelism": f"sharded{world} (position shards, NCCL all_gather + all_to_all)" if world > 1 else "single"},
+                   "parallelism": (f"sharded{world} (position shards; NCCL all_gather of histograms, "
+                                   + ("merge over peer memory)" if transport == "p2p" else "NCCL all_to_all + merge)")
+                                   if world > 1 else "single")},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "kernel": dominant, "kernel_ms": stages[dominant],
-                     "algorithmic_bytes": dom_bytes, "peak_source": peak_src},
+                     "algorithmic_bytes": dom_bytes, "peak_source": peak_src, "limiter": limiter},
         "metric_roofline": {"bytes_per_build": mbytes, "achieved_gbs": mbytes / (ms * 1e-3) / 1e9,
                             "frac": mbytes / (ms * 1e-3) / 1e9 / peak,
                             "definition": "SURVEY 8d: B = L (n s + n/8), text read once per level + level bits"},

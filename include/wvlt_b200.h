@@ -129,6 +129,25 @@ int wvlt_merge_bits(uint64_t* dst_words, int64_t word_lo, int64_t word_hi, int64
                     const uint64_t* src_words, void* stream);
 
 /*
+ * Multi-GPU merge over peer memory (one launch for every level): destination
+ * row l (dst_words + l * dst_row_words) receives global words [word_lo, word_hi)
+ * of level l, assembled straight from the source ranks' local levels --
+ * level_src[l * nranks + r] points at rank r's local level l words, a
+ * peer-mapped (NVLink P2P / symmetric-memory) device pointer.  Level l's tasks
+ * are t in [task_off[l], task_off[l+1]): destination bits
+ * [b[t'], b[t'+1]) with b = bounds + bounds_off[l] and t' = t - task_off[l]
+ * come from rank src_ranks[t] starting at local bit src_starts[t]; they cover
+ * the owned bit range.  bounds_off / task_off / bounds / src_* / level_src are
+ * device arrays.  Replaces the all-to-all + gather_bits pair of the
+ * domain-decomposed merge (construct.py:497-507, _kernels.py:196-232) when the
+ * ranks' memories are peer-accessible.
+ */
+int wvlt_merge_levels_peer(uint64_t* dst_words, int64_t dst_row_words, int width, int64_t word_lo, int64_t word_hi,
+                           int64_t n_bits, const int64_t* bounds, const int64_t* bounds_off, const int64_t* src_starts,
+                           const int32_t* src_ranks, const int64_t* task_off, const uint64_t* const* level_src,
+                           int nranks, void* stream);
+
+/*
  * Rank/select directories of nvec bit vectors of `length` bits stored back to
  * back (ceil(length/64) words each, the level layout above).  Replaces
  * RankSelectBitVector._build (bitvec.py:135-163), same arrays per vector:

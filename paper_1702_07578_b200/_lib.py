@@ -57,6 +57,8 @@ def load():
     L.wvlt_build_host.restype = i32
     L.wvlt_merge_bits.argtypes = [vp, i64, i64, i64, vp, vp, i64, vp, vp]
     L.wvlt_merge_bits.restype = i32
+    L.wvlt_merge_levels_peer.argtypes = [vp, i64, i32, i64, i64, i64, vp, vp, vp, vp, vp, vp, i32, vp]
+    L.wvlt_merge_levels_peer.restype = i32
     L.wvlt_last_launches.argtypes = []
     L.wvlt_last_launches.restype = i32
     L.wvlt_rank_select_workspace_bytes.argtypes = [i64, i64]

@@ -1644,6 +1644,86 @@ __global__ void __launch_bounds__(256) merge_bits_kernel(uint64_t* __restrict__ 
   }
 }
 
+// Multi-GPU merge over peer memory: every level's owned destination words are
+// assembled straight from the source ranks' local levels (P2P / symmetric-memory
+// pointers over NVLink), so the exchange and the shift-merge are one kernel.
+// Task t of level l: destination bits [bounds[t], bounds[t+1]) come from rank
+// ranks[t]'s local level l starting at bit starts[t].
+__device__ __forceinline__ uint64_t merge_word_peer(int64_t wd, int64_t nbits, const int64_t* __restrict__ bounds,
+                                                    const int64_t* __restrict__ starts,
+                                                    const int32_t* __restrict__ ranks,
+                                                    const uint64_t* const* __restrict__ srcs, int64_t t) {
+  const int64_t wb = wd << 6;
+  int64_t nb = nbits - wb;
+  if (nb > 64) nb = 64;
+  uint64_t acc = 0;
+  int filled = 0;
+  while (filled < nb) {
+    const int64_t here = wb + filled;
+    while (__ldg(bounds + t + 1) <= here) ++t;
+    int64_t take = nb - filled;
+    const int64_t avail = __ldg(bounds + t + 1) - here;
+    if (avail < take) take = avail;
+    const int64_t sp = __ldg(starts + t) + (here - __ldg(bounds + t));
+    const unsigned long long* src = reinterpret_cast<const unsigned long long*>(srcs[__ldg(ranks + t)]);
+    const int64_t wi = sp >> 6;
+    const int sh = (int)(sp & 63);
+    uint64_t chunk = src[wi] >> sh;
+    if (sh + take > 64) chunk |= src[wi + 1] << (64 - sh);
+    if (take < 64) chunk &= (1ull << take) - 1ull;
+    acc |= chunk << filled;
+    filled += (int)take;
+  }
+  return acc;
+}
+
+__global__ void __launch_bounds__(256) merge_peer_kernel(uint64_t* __restrict__ dst, int64_t dst_row, int64_t wlo,
+                                                         int64_t whi, int64_t nbits,
+                                                         const int64_t* __restrict__ bounds_all,
+                                                         const int64_t* __restrict__ bounds_off,
+                                                         const int64_t* __restrict__ starts_all,
+                                                         const int32_t* __restrict__ ranks_all,
+                                                         const int64_t* __restrict__ task_off,
+                                                         const uint64_t* const* __restrict__ level_src, int nranks) {
+  constexpr int CH = 32 * MERGE_WORDS_PER_LANE;
+  const int l = blockIdx.y;
+  const int64_t t_lo = task_off[l], ntasks = task_off[l + 1] - t_lo;
+  if (ntasks <= 0) return;
+  const int64_t* bounds = bounds_all + bounds_off[l];
+  const int64_t* starts = starts_all + t_lo;
+  const int32_t* ranks = ranks_all + t_lo;
+  const uint64_t* const* srcs = level_src + (int64_t)l * nranks;
+  uint64_t* drow = dst + (int64_t)l * dst_row - wlo;
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t w0 = wlo + ((((int64_t)blockIdx.x * blockDim.x) >> 5) + (threadIdx.x >> 5)) * CH; w0 < whi;
+       w0 += nwarps * CH) {
+    int64_t t0 = 0;
+    if (lane == 0 && (w0 << 6) < nbits) {
+      int64_t lo = 0, hi = ntasks;  // last t with bounds[t] <= bit
+      const int64_t bit = w0 << 6;
+      while (hi - lo > 1) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (__ldg(bounds + mid) <= bit) lo = mid;
+        else hi = mid;
+      }
+      t0 = lo;
+    }
+    t0 = __shfl_sync(FULL, t0, 0);
+    uint64_t v[MERGE_WORDS_PER_LANE];
+#pragma unroll
+    for (int k = 0; k < MERGE_WORDS_PER_LANE; ++k) {
+      const int64_t wd = w0 + 32 * k + lane;
+      v[k] = (wd < whi && (wd << 6) < nbits) ? merge_word_peer(wd, nbits, bounds, starts, ranks, srcs, t0) : 0ull;
+    }
+#pragma unroll
+    for (int k = 0; k < MERGE_WORDS_PER_LANE; ++k) {
+      const int64_t wd = w0 + 32 * k + lane;
+      if (wd < whi) __stcs(reinterpret_cast<unsigned long long*>(drow) + wd, v[k]);
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
@@ -2376,6 +2456,24 @@ int wvlt_merge_bits(uint64_t* dst_words, int64_t word_lo, int64_t word_hi, int64
   if (blocks > cap) blocks = cap;
   merge_bits_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(dst_words, word_lo, word_hi, n_bits, bounds,
                                                                          src_starts, ntasks, src_words);
+  return (int)cudaGetLastError();
+}
+
+int wvlt_merge_levels_peer(uint64_t* dst_words, int64_t dst_row_words, int width, int64_t word_lo, int64_t word_hi,
+                           int64_t n_bits, const int64_t* bounds, const int64_t* bounds_off, const int64_t* src_starts,
+                           const int32_t* src_ranks, const int64_t* task_off, const uint64_t* const* level_src,
+                           int nranks, void* stream) {
+  if (width < 0 || word_hi < word_lo || word_lo < 0 || n_bits < 0 || nranks < 1 || dst_row_words < word_hi - word_lo)
+    return WVLT_E_ARG;
+  if (width == 0 || word_hi == word_lo) return 0;
+  if (!dst_words || !bounds || !bounds_off || !src_starts || !src_ranks || !task_off || !level_src) return WVLT_E_ARG;
+  const int64_t nw = word_hi - word_lo;
+  int64_t blocks = (nw + 256 * MERGE_WORDS_PER_LANE - 1) / (256 * MERGE_WORDS_PER_LANE);
+  const int64_t cap = std::max<int64_t>(1, (int64_t)sm_count() * 32 / width);
+  if (blocks > cap) blocks = cap;
+  merge_peer_kernel<<<dim3((unsigned)blocks, (unsigned)width), 256, 0, (cudaStream_t)stream>>>(
+      dst_words, dst_row_words, word_lo, word_hi, n_bits, bounds, bounds_off, src_starts, src_ranks, task_off,
+      level_src, nranks);
   return (int)cudaGetLastError();
 }
 

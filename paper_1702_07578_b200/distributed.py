@@ -128,13 +128,65 @@ def exchange_plan(hists: np.ndarray, kind: str, width: int, n: int, local_ns, wo
     return ranges, levels
 
 
-def build_sharded(local_text, sigma: int, kind: str = "wm", group=None, *, ops=None, gather: bool = False):
+def peer_plan_arrays(plans, owner: int, width: int):
+    """This owner's merge tasks of every level, flattened for wvlt_merge_levels_peer:
+    (bounds, bounds_off, starts, ranks, task_off).  Level l's tasks are
+    [task_off[l], task_off[l+1]); its bounds (one more entry than tasks) start at
+    bounds_off[l]; task t takes source rank ranks[t]'s local level l from bit
+    starts[t]."""
+    bounds, starts, ranks = [], [], []
+    bounds_off, task_off = [], [0]
+    boff = 0
+    for ell in range(width):
+        pd = plans[ell][owner]
+        bounds_off.append(boff)
+        if pd is None or len(pd["lens"]) == 0:
+            task_off.append(task_off[-1])
+            continue
+        g, ln = np.asarray(pd["gstart"], dtype=np.int64), np.asarray(pd["lens"], dtype=np.int64)
+        b = np.concatenate([g, [g[-1] + ln[-1]]])
+        bounds.append(b)
+        starts.append(np.asarray(pd["local"], dtype=np.int64))
+        ranks.append(np.asarray(pd["ranks"], dtype=np.int32))
+        boff += b.size
+        task_off.append(task_off[-1] + ln.size)
+    cat = lambda xs, dt: np.concatenate(xs).astype(dt) if xs else np.zeros(1, dtype=dt)  # noqa: E731
+    return (cat(bounds, np.int64), np.asarray(bounds_off, dtype=np.int64), cat(starts, np.int64),
+            cat(ranks, np.int32), np.asarray(task_off, dtype=np.int64))
+
+
+def merge_peer_host(arrays, sources, word_lo: int, word_hi: int, n: int, width: int):
+    """Host restatement of wvlt_merge_levels_peer (test checker): ``sources[r][l]``
+    is rank r's local level l (uint64 words).  Returns uint64 [width, word_hi - word_lo]."""
+    bounds, boff, starts, ranks, toff = arrays
+    out = np.zeros((width, max(word_hi - word_lo, 0)), dtype=np.uint64)
+    for ell in range(width):
+        t0, t1 = int(toff[ell]), int(toff[ell + 1])
+        b = bounds[int(boff[ell]): int(boff[ell]) + (t1 - t0) + 1]
+        for t in range(t1 - t0):
+            lo, hi = max(int(b[t]), 64 * word_lo), min(int(b[t + 1]), 64 * word_hi, n)
+            src = sources[int(ranks[t0 + t])][ell]
+            for g in range(lo, hi):  # bit by bit: small test sizes only
+                sp = int(starts[t0 + t]) + (g - int(b[t]))
+                if (int(src[sp >> 6]) >> (sp & 63)) & 1:
+                    out[ell, (g >> 6) - word_lo] |= np.uint64(1) << np.uint64(g & 63)
+    return out
+
+
+def build_sharded(local_text, sigma: int, kind: str = "wm", group=None, *, ops=None, gather: bool = False,
+                  transport: str = "nccl"):
     """Sharded build over the ranks of ``group`` (default: the world group).
 
     Every rank passes its own contiguous shard of the text (rank order = text
     order).  Returns this rank's ShardedResult; with ``gather`` rank 0 also gets
     the full level words (attribute ``full_words``).  ``ops`` supplies the local
     build and the merge; the default uses this rank's CUDA device.
+
+    ``transport``: "nccl" moves the needed bit segments with one all_to_all and
+    shift-merges them (wvlt_merge_bits); "p2p" builds every rank's local levels in
+    symmetric (peer-mapped) memory and lets each owner assemble its words straight
+    from the peers' levels in one kernel (wvlt_merge_levels_peer) -- the exchange
+    fused into the merge, no staging copy.
     """
     import torch
     import torch.distributed as dist
@@ -157,8 +209,18 @@ def build_sharded(local_text, sigma: int, kind: str = "wm", group=None, *, ops=N
     local_ns = [int(v) for v in ns.cpu().tolist()]
     n = sum(local_ns)
 
+    if transport not in ("nccl", "p2p"):
+        raise ValueError(f"unknown transport {transport!r}")
+    peer = None
     # 1. local build (no communication)
-    words, hist, bad = ops.local_build(local_text, sigma, kind)
+    if transport == "p2p" and width > 0:
+        # local levels in symmetric memory: every rank's buffer mapped into every peer
+        lnws = [(v + 63) >> 6 for v in local_ns]
+        hdl, buf = ops.peer_buffer(width * max(lnws), group)
+        peer = (hdl, buf, lnws)
+        words, hist, bad = ops.local_build(local_text, sigma, kind, out_words=buf[: width * lnws[rank]])
+    else:
+        words, hist, bad = ops.local_build(local_text, sigma, kind)
     flag = torch.tensor([1 if bad else 0], dtype=torch.int64, device=dev)
     dist.all_reduce(flag, group=group)
     if int(flag.item()):
@@ -175,6 +237,22 @@ def build_sharded(local_text, sigma: int, kind: str = "wm", group=None, *, ops=N
     owned = torch.zeros((width, max(w1 - w0, 0)), dtype=torch.int64, device=dev)
     if width == 0 or n == 0:
         return ShardedResult(n, sigma, kind, width, w0, w1, owned, zeros, ghist)
+    if peer is not None:
+        # 3+4. one kernel per owner reads the peers' local levels directly.  The
+        # histogram all_gather above is stream-ordered after every rank's local
+        # build, so the peers' levels are complete once it has finished here.
+        hdl, buf, lnws = peer
+        arrays = peer_plan_arrays(plans, rank, width)
+        level_src = np.array([[int(hdl.buffer_ptrs[r]) + 8 * ell * lnws[r] for r in range(world)]
+                              for ell in range(width)], dtype=np.int64)
+        ops.merge_peer(owned, w0, w1, n, arrays, level_src, world)
+        # peers may reuse their buffers only after every owner has read them
+        done = torch.zeros(1, dtype=torch.int64, device=dev)
+        dist.all_reduce(done, group=group)
+        res = ShardedResult(n, sigma, kind, width, w0, w1, owned, zeros, ghist)
+        if gather:
+            res.full_words = _gather_levels(owned, ranges, width, total_words, rank, world, group, dev)
+        return res
 
     # 3. one all_to_all for every level: the send buffer is grouped by
     #    destination (levels in order inside), so the receive buffer is grouped
@@ -253,8 +331,20 @@ class CudaOps:
 
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
         self.builder = DeviceBuilder(self.device)
+        self._peer = None  # (handle, buffer) of the p2p transport, reused while large enough
 
-    def local_build(self, text, sigma: int, kind: str):
+    def peer_buffer(self, words: int, group=None):
+        """A symmetric-memory int64 buffer of at least ``words`` on every rank of
+        ``group`` (collective when it has to grow: every rank asks for the same size)."""
+        import torch.distributed as dist
+        from torch.distributed import _symmetric_memory as symm_mem
+
+        if self._peer is None or self._peer[1].numel() < words:
+            buf = symm_mem.empty(max(int(words), 1), dtype=torch_int64(), device=self.device)
+            self._peer = (symm_mem.rendezvous(buf, group if group is not None else dist.group.WORLD), buf)
+        return self._peer
+
+    def local_build(self, text, sigma: int, kind: str, out_words=None):
         import torch
 
         if not isinstance(text, torch.Tensor):
@@ -262,7 +352,11 @@ class CudaOps:
 
             text = torch.from_numpy(_device_text(np.ascontiguousarray(np.asarray(text)), sigma))
         text = text.to(self.device)
-        res = self.builder.build(text, sigma, kind, histogram=True, check=False)
+        outputs = None
+        if out_words is not None:  # levels into a caller buffer (symmetric memory for the p2p merge)
+            lw, zeros, hist, bd, status = self.builder.alloc_outputs(int(text.numel()), sigma)
+            outputs = (out_words.view(lw.shape), zeros, hist, bd, status)
+        res = self.builder.build(text, sigma, kind, histogram=True, check=False, outputs=outputs)
         bad = bool(int(res.status.item()) & 1) if res.status is not None else False
         return res.level_words, res.hist, bad
 
@@ -272,3 +366,32 @@ class CudaOps:
         b = torch.from_numpy(bounds).to(self.device)
         s = torch.from_numpy(src_starts).to(self.device)
         self.builder.merge_bits(dst_row, word_lo, word_hi, n_bits, b, s, src, dst_offset_words=word_lo)
+
+    def merge_peer(self, owned, word_lo: int, word_hi: int, n_bits: int, arrays, level_src, nranks: int):
+        """wvlt_merge_levels_peer into ``owned`` [width, word_hi - word_lo]; ``level_src``
+        int64 [width, nranks] device addresses of every rank's local levels."""
+        import torch
+
+        from . import _lib
+
+        bounds, boff, starts, ranks, toff = arrays
+        dev = self.device
+        flat = torch.from_numpy(np.concatenate([bounds, boff, starts, toff, level_src.reshape(-1)])).to(dev)
+        rk = torch.from_numpy(ranks).to(dev)
+        o1 = bounds.size
+        o2 = o1 + boff.size
+        o3 = o2 + starts.size
+        o4 = o3 + toff.size
+        base, e = flat.data_ptr(), flat.element_size()
+        width = int(owned.shape[0])
+        rc = _lib.load().wvlt_merge_levels_peer(
+            owned.data_ptr(), int(owned.shape[1]) if owned.dim() == 2 else 0, width, int(word_lo), int(word_hi),
+            int(n_bits), base, base + e * o1, base + e * o2, rk.data_ptr(), base + e * o3, base + e * o4, int(nranks),
+            torch.cuda.current_stream(dev).cuda_stream)
+        _lib.check(rc)
+
+
+def torch_int64():
+    import torch
+
+    return torch.int64

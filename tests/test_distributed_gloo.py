@@ -124,3 +124,33 @@ def test_level_plan_matches_reference_merge_order():
     assert list(gstart) == [0, 3, 4, 6, 8, 11, 15, 17]
     ranks, local, lens, gstart = level_plan(h, "wt", 3, 2)
     assert list(lens) == [3, 1, 3, 4, 2, 2, 2, 2]
+
+
+@pytest.mark.parametrize("kind", ["wt", "wm"])
+@pytest.mark.parametrize("sigma,world", [(5, 2), (256, 3), (1000, 4), (70000, 3)])
+def test_peer_merge_plan_reassembles_the_single_build(kind, sigma, world):
+    """The p2p transport's per-owner task arrays (peer_plan_arrays), applied by the
+    host restatement of wvlt_merge_levels_peer to every rank's local levels,
+    reassemble the single build (no process group needed: the plan is pure)."""
+    import oracle
+    from paper_1702_07578_b200.bitperm import code_width
+    from paper_1702_07578_b200.distributed import exchange_plan, merge_peer_host, peer_plan_arrays
+
+    rng = np.random.default_rng(sigma + world)
+    n = 3000 + 7 * world
+    text = rng.integers(0, sigma, n).astype(np.uint32 if sigma > 65536 else np.uint16 if sigma > 256 else np.uint8)
+    cuts = [0] + sorted(rng.choice(np.arange(1, n), world - 1, replace=False).tolist()) + [n]
+    width = code_width(sigma)
+    sources, hists = [], []
+    for r in range(world):
+        part = text[cuts[r]:cuts[r + 1]]
+        w, _, h = oracle.build(part, sigma, kind, "pc")
+        sources.append(np.asarray(w, dtype=np.uint64))
+        hists.append(oracle.histogram(part, sigma) if h is None else np.asarray(h, dtype=np.int64))
+    ranges, plans = exchange_plan(np.stack(hists), kind, width, n, [cuts[r + 1] - cuts[r] for r in range(world)],
+                                  world)
+    want, _, _ = oracle.build(text, sigma, kind, "pc")
+    for owner, (w0, w1) in enumerate(ranges):
+        arrays = peer_plan_arrays(plans, owner, width)
+        got = merge_peer_host(arrays, sources, w0, w1, n, width)
+        assert np.array_equal(got, np.asarray(want, dtype=np.uint64)[:, w0:w1]), owner

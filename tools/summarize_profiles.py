@@ -83,6 +83,7 @@ lines += ["", "## `--set full` capture of the top kernels (one launch each)", ""
           "| kernel | time us | DRAM read MB | DRAM write MB | DRAM %peak | SM %peak | issue % | ALU % | LSU % | smem wavefronts | bank conflicts | regs |",
           "|---|---|---|---|---|---|---|---|---|---|---|---|"]
 traffic = {}
+smem = {}
 ui = {w: units[h.index(w)] for w in want if w in h}
 pass_idx = 0
 for r in full:
@@ -96,6 +97,7 @@ for r in full:
                  f"{r['l1tex__data_pipe_lsu_wavefronts_mem_shared.sum']} | {r['l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum']} | {r['launch__registers_per_thread']} |")
     if "level_pass" in name:
         traffic[f"pass{pass_idx}"] = (rd + wr) * 1e6
+        smem[f"pass{pass_idx}"] = float(r["l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"].replace(",", ""))
         pass_idx += 1
     elif "hist" in name or "digits" in name:
         traffic["hist"] = (rd + wr) * 1e6
@@ -103,5 +105,6 @@ for r in full:
         traffic["tiles8"] = (rd + wr) * 1e6
 (out / f"{tag}_summary.md").write_text("\n".join(lines) + "\n")
 json.dump(traffic, open(out / "ncu_traffic_c2_wm.json", "w"), indent=1)
+json.dump(smem, open(out / "ncu_smem_c2_wm.json", "w"), indent=1)  # shared-memory wavefronts per launch
 print("\n".join(lines))
 print(traffic)
