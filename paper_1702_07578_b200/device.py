@@ -68,17 +68,24 @@ class DeviceBuilder:
         if not torch.cuda.is_available():
             raise RuntimeError("the wavelet construction path needs a CUDA device (no CPU fallback)")
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
-        self._ws = None
+        self._ws = {}  # stream handle -> workspace (builds on different streams never share one)
 
     # -- buffers -------------------------------------------------------------
-    def workspace(self, n: int, sym_bytes: int, sigma: int, kind: str):
+    def workspace(self, n: int, sym_bytes: int, sigma: int, kind: str, stream=None):
+        """The workspace of builds on ``stream`` (default: the current stream), grown
+        on demand.  It is allocated on that stream, so the caching allocator only
+        recycles a replaced one after the stream's queued work."""
         torch = _torch()
         need = int(self.lib.wvlt_workspace_bytes(int(n), int(sym_bytes), int(sigma), _lib.KINDS[kind]))
         if need == 0 and code_width(sigma) > _lib.MAX_WIDTH:
             raise ValueError(f"alphabet size {sigma} exceeds the supported code width {_lib.MAX_WIDTH}")
-        if self._ws is None or self._ws.numel() < need:
-            self._ws = torch.empty(max(need, 256), dtype=torch.uint8, device=self.device)
-        return self._ws, need
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        ws = self._ws.get(s.cuda_stream)
+        if ws is None or ws.numel() < need:
+            with torch.cuda.stream(s):
+                ws = torch.empty(max(need, 256), dtype=torch.uint8, device=self.device)
+            self._ws[s.cuda_stream] = ws
+        return ws, need
 
     def alloc_outputs(self, n: int, sigma: int, borders: bool = False):
         torch = _torch()
@@ -123,11 +130,12 @@ class DeviceBuilder:
         w = code_width(sigma)
         if w > _lib.MAX_WIDTH:
             raise ValueError(f"alphabet size {sigma} exceeds the supported code width {_lib.MAX_WIDTH}")
-        if outputs is None:
-            outputs = self.alloc_outputs(n, sigma, borders)
-        lw, zeros, hist, bd, status = outputs
-        ws, need = self.workspace(n, sb, sigma, kind)
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        if outputs is None:
+            with torch.cuda.stream(s):
+                outputs = self.alloc_outputs(n, sigma, borders)
+        lw, zeros, hist, bd, status = outputs
+        ws, need = self.workspace(n, sb, sigma, kind, s)
         rc = self.lib.wvlt_build_device(
             text.data_ptr() if n else None, sb, n, sigma, _lib.KINDS[kind],
             lw.data_ptr() if lw.numel() else None, zeros.data_ptr() if w else None,
@@ -157,11 +165,12 @@ class DeviceBuilder:
             out_words = np.empty((w, nwords), dtype=np.uint64)
         zeros = np.zeros(max(w, 1), dtype=np.int64)
         hist = np.zeros(1 << w, dtype=np.int64)
-        dev_text = torch.empty(max(n * sb, 16), dtype=torch.uint8, device=self.device)
-        dev_words = torch.empty(max(w * nwords, 1), dtype=torch.int64, device=self.device)
-        dev_small = torch.empty((1 << w) + w + 1, dtype=torch.int64, device=self.device)
-        ws, need = self.workspace(n, sb, sigma, kind)
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        with torch.cuda.stream(s):
+            dev_text = torch.empty(max(n * sb, 16), dtype=torch.uint8, device=self.device)
+            dev_words = torch.empty(max(w * nwords, 1), dtype=torch.int64, device=self.device)
+            dev_small = torch.empty((1 << w) + w + 1, dtype=torch.int64, device=self.device)
+        ws, need = self.workspace(n, sb, sigma, kind, s)
         rc = self.lib.wvlt_build_host(
             arr.ctypes.data if n else None, sb, n, sigma, _lib.KINDS[kind],
             out_words.ctypes.data if out_words.size else None, zeros.ctypes.data,

@@ -231,3 +231,27 @@ def test_byte_storage_wide_alphabet_device_text(sigma):
     ow, oz, _ = oracle.build(host, sigma, "wm", "pc")
     assert np.array_equal(words, ow)
     assert zeros == oz
+
+
+def test_concurrent_builds_on_two_streams():
+    """One builder, two streams in flight at once: every stream gets its own
+    workspace, so the builds do not interfere."""
+    from paper_1702_07578_b200.device import DeviceBuilder
+
+    b = DeviceBuilder()
+    g = torch.Generator(device="cuda")
+    g.manual_seed(21)
+    texts = [torch.randint(0, 256, (3_000_001,), generator=g, device="cuda", dtype=torch.int64).to(torch.uint8),
+             torch.randint(0, 1000, (2_000_003,), generator=g, device="cuda", dtype=torch.int64).to(torch.uint16)]
+    sigmas = [256, 1000]
+    want = [b.build(t, sg, "wm").level_words.clone() for t, sg in zip(texts, sigmas)]
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    for _ in range(3):
+        got = []
+        for t, sg, s in zip(texts, sigmas, streams):
+            s.wait_stream(torch.cuda.current_stream())
+            got.append(b.build(t, sg, "wm", stream=s, check=False))
+        torch.cuda.synchronize()
+        for r, w in zip(got, want):
+            assert torch.equal(r.level_words, w)
