@@ -13,11 +13,13 @@
 
 namespace {
 
-constexpr int K16_TILE = 8192;  // symbols per tile (run sizes / offsets fit 16 bits)
+#ifndef K16_TILE
+#define K16_TILE 16384  // symbols per tile (run sizes / offsets fit 16 bits; measured: 8192 slower)
+#endif
 constexpr int K16_Q = 4;        // 8-symbol runs per thread
 constexpr int K16_NT = K16_TILE / (8 * K16_Q);
 #ifndef K16_CTAS
-#define K16_CTAS 4
+#define K16_CTAS (K16_TILE == 8192 ? 4 : 2)
 #endif
 
 // ---- K1: per-tile counts of the W-bit high-byte digit, range check, level l0 ----
