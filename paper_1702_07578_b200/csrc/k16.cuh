@@ -287,7 +287,7 @@ __global__ void __launch_bounds__(K16_NT, K16_CTAS) level_pass16_kernel(const Pa
     bar_sync(1, NT);
   }
   // levels 1..W-1 as flattened destination-word tasks (as in the byte pass)
-  emit_levels8<W, NC>(tt, bits, a.words, a.nwords, tid, NT);
+  emit_levels8<W, NC>(tt, bits, a.words, a.nwords, tid, NT, smem + (size_t)((W + 1) & 1) * 2 * T);
   // the low bytes of each level-W group: one contiguous run of the byte text
   const uint8_t* lo = smem + (size_t)(W & 1) * 2 * T;
   constexpr int LS = 2;  // low byte of element p at byte 2 p

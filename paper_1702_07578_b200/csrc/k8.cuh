@@ -431,18 +431,29 @@ static_assert(sizeof(Tab8) % 16 == 0, "bulk-copy granularity");
 // neighbouring tiles share them; the levels were zeroed).
 template <int W, int NC>
 __device__ __forceinline__ void emit_levels8(const Tab8& tt, const uint32_t* bits, uint64_t* words, int64_t nwords,
-                                             int tid, int nthreads) {
+                                             int tid, int nthreads, uint8_t* coarse) {
   constexpr int NR = (1 << W) - 2;
+  constexpr int G = 16;  // tasks per coarse map entry
 #ifdef K8_NO_EMIT
   const int total = 0;
 #else
   const int total = tt.wpre[NR];
 #endif
-  for (int q = tid; q < total; q += nthreads) {
-    int r = 0;  // last run with wpre[r] <= q (empty runs share prefix values)
+  // coarse task -> run map (shared scratch): the run of every 16th task, found by
+  // one binary search each; a task then walks forward over the few runs that
+  // start after its entry (empty runs share prefix values)
+  for (int c = tid; c * G < total; c += nthreads) {
+    const int q = c * G;
+    int r = 0;
 #pragma unroll
     for (int s = 128; s >= 1; s >>= 1)
       if (r + s < NR && tt.wpre[r + s] <= q) r += s;
+    coarse[c] = (uint8_t)r;
+  }
+  bar_sync(1, nthreads);
+  for (int q = tid; q < total; q += nthreads) {
+    int r = coarse[q / G];  // last run with wpre[r] <= q
+    while (r + 1 < NR && tt.wpre[r + 1] <= q) ++r;
     const int j = 31 - __clz(r + 2);
     // 32-bit bit positions: the fused passes keep n < 2^32 - 64
     const uint32_t g = tt.gs[r];
@@ -676,7 +687,7 @@ __global__ void __launch_bounds__(K8Cfg<Q>::NT, K8Cfg<Q>::CTAS) level_pass8_kern
     bar_sync(1, NT);
   }
   bar_sync(1, NT);  // every warp's level bits are stored
-  emit_levels8<W, NC>(tt, bits, a.words, a.nwords, tid, NT);
+  emit_levels8<W, NC>(tt, bits, a.words, a.nwords, tid, NT, smem);  // ping-pong buffers are free now
 }
 
 // per-tile run tables, one warp per tile
