@@ -11,9 +11,6 @@
 
 namespace {
 
-#ifndef U8_K8_CTAS
-#define U8_K8_CTAS 4  // 16 warps per CTA, no table warp
-#endif
 
 // ---- K1: per-tile counts of every W-bit value (tile-major [tile][2^W]) ----
 // One warp per tile; lane-private 16-bit counter pairs for (p, p + 2^(W-1)): the
@@ -318,24 +315,6 @@ __device__ __forceinline__ void table8_stage(Tables8& tt, int lane, const uint32
 }
 
 template <int W>
-__device__ __forceinline__ void table8_compute(Tables8& tt, const uint32_t* s_base, int lane);
-
-template <int W>
-__device__ __forceinline__ void table8_warp(const Pass8Args& a, Tables8& tt, const uint32_t* s_base, int64_t tile,
-                                            int lane, int allt) {
-  constexpr int NB = 1 << W;
-  constexpr int NR = NB - 2;
-  uint32_t rc[8], rp[8];
-  table8_load<W>(a, tile, lane, rc, rp);
-  table8_stage<W>(tt, lane, rc, rp);
-  table8_compute<W>(tt, s_base, lane);
-  if (allt > 0) {
-    __threadfence_block();
-    bar_arrive(2, allt);
-  }
-}
-
-template <int W>
 __device__ __forceinline__ void table8_compute(Tables8& tt, const uint32_t* s_base, int lane) {
   constexpr int NB = 1 << W;
   constexpr int NR = NB - 2;
@@ -473,7 +452,7 @@ __device__ __forceinline__ void emit_levels8(const Tab8& tt, const uint32_t* bit
 
 constexpr int T8_WARPS = 8;
 
-// One warp per tile: the tile's run tables (table8_warp) into the compact
+// One warp per tile: the tile's run tables (table8_compute) into the compact
 // global layout, off the pass kernel's critical path.
 template <int W>
 __global__ void __launch_bounds__(T8_WARPS * 32) tiles8_kernel(const Pass8Args a, Tab8* __restrict__ out) {
@@ -563,11 +542,9 @@ __global__ void __launch_bounds__(K8Cfg<Q>::NT, K8Cfg<Q>::CTAS) level_pass8_kern
                    : "memory");
   }
   for (int i = tid; i < 256; i += NT) s_lut[i] = g_sort_lut.sel[i];
-#ifndef K8_LAST_SPLIT_BYTES
   // level W-1 is OR-ed bit by bit from the last split (order W-1 is never
   // materialised as bytes)
   for (int i = tid; i < NC + 4; i += NT) bits[(W - 1) * (NC + 4) + i] = 0u;
-#endif
   if (!bulk)
     for (int p = tid; p < T; p += NT) smem[p] = p < cnt ? text[base + p] : (uint8_t)0xFF;
   bar_sync(1, NT);  // mbarrier initialised, direct staging done
@@ -595,11 +572,6 @@ __global__ void __launch_bounds__(K8Cfg<Q>::NT, K8Cfg<Q>::CTAS) level_pass8_kern
       if (j > 0) bits8[j * 4 * (NC + 4) + k * (R / 8) + tid] = (uint8_t)m[k];  // level 0: hist8_kernel
     }
     if (j + 1 == W) break;
-#ifndef K8_LAST_SPLIT_BYTES
-    constexpr bool last_bits = true;
-#else
-    constexpr bool last_bits = false;
-#endif
     uint32_t pk[P], incl[P];
 #pragma unroll
     for (int p = 0; p < P; ++p) {
@@ -622,7 +594,7 @@ __global__ void __launch_bounds__(K8Cfg<Q>::NT, K8Cfg<Q>::CTAS) level_pass8_kern
       run_tot += (int)(tot >> 16);
     }
     const int Z = T - run_tot;
-    if (last_bits && j + 2 == W) {
+    if (j + 2 == W) {
       // last split: only the next level's bits are needed.  The run's flags of
       // bit sh - 1 in split order (zeros part low, ones part high) are OR-ed
       // into the level W-1 bit array at the two parts' positions.
@@ -659,7 +631,6 @@ __global__ void __launch_bounds__(K8Cfg<Q>::NT, K8Cfg<Q>::CTAS) level_pass8_kern
       // zeros of run k go to k R + 8 t - opre (its zeros before), ones to Z + opre
       const uint32_t za = opaque(nxt + (uint32_t)(k * R + 8 * tid - opre[k]));
       const uint32_t oa = opaque(nxt + (uint32_t)(Z + opre[k] - nz));
-#ifndef K8_SEL_ADDR
       // address selection mostly off the integer ALU pipe (its bound): the
       // carry of (15 - nz) 2^28 + (kk + 1) 2^28 out of 32 bits is [kk >= nz],
       // read as the high word of one mad.wide; then addr = za + flag (oa - za)
@@ -674,15 +645,6 @@ __global__ void __launch_bounds__(K8Cfg<Q>::NT, K8Cfg<Q>::CTAS) level_pass8_kern
         const uint32_t addr = za + (uint32_t)(t >> 32) * dz + kk;
         asm volatile("st.shared.u8 [%0], %1;" ::"r"(addr), "r"(vb) : "memory");
       }
-#else
-#pragma unroll
-      for (int kk = 0; kk < 8; ++kk) {
-        const uint32_t v = sv[kk >> 2];
-        const uint32_t vb = (kk & 3) == 0 ? v : (kk & 3) == 1 ? (v >> 8) : (kk & 3) == 2 ? (v >> 16) : (v >> 24);
-        const uint32_t addr = (kk < nz ? za : oa) + kk;
-        asm volatile("st.shared.u8 [%0], %1;" ::"r"(addr), "r"(vb) : "memory");
-      }
-#endif
     }
     bar_sync(1, NT);
   }
