@@ -58,10 +58,19 @@ __global__ void __launch_bounds__(H8_WARPS * 32) hist8_kernel(const uint8_t* __r
       // streamed here instead of a separate memset of the same bytes
       const int64_t w0 = first >> 6;
       const int tw = (int)min((int64_t)(K8_TILE / 64), nwords - w0);
+      if (tw == K8_TILE / 64 && !(nwords & 1)) {  // whole tile, 16-byte aligned rows
 #pragma unroll
-      for (int j = 1; j < W; ++j) {
-        uint64_t* lw = level0 + j * nwords + w0;
-        for (int i = lane; i < tw; i += 32) __stcs(reinterpret_cast<unsigned long long*>(lw + i), 0ull);
+        for (int j = 1; j < W; ++j) {
+          uint4* lw = reinterpret_cast<uint4*>(level0 + j * nwords + w0);
+#pragma unroll
+          for (int i = lane; i < K8_TILE / 128; i += 32) __stcs(lw + i, make_uint4(0, 0, 0, 0));
+        }
+      } else {
+#pragma unroll
+        for (int j = 1; j < W; ++j) {
+          uint64_t* lw = level0 + j * nwords + w0;
+          for (int i = lane; i < tw; i += 32) __stcs(reinterpret_cast<unsigned long long*>(lw + i), 0ull);
+        }
       }
     }
     if (cnt == K8_TILE && aligned) {
