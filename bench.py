@@ -225,6 +225,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-wt", action="store_true")
+    ap.add_argument("--graph", action="store_true", help="N = 1: time CUDA-graph replays of the captured build")
     ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
                     help="N > 1: merge over peer memory (symmetric memory, one kernel) or NCCL all_to_all + merge")
     args = ap.parse_args()
@@ -275,7 +276,13 @@ def main():
         dist.all_reduce(ok, op=dist.ReduceOp.MIN)
         transport = "p2p" if int(ok.item()) else "nccl"
 
+    graphs = {}
+
     def one_build(kind_):
+        if args.graph and not sharded:
+            if kind_ not in graphs:
+                graphs[kind_] = builder.capture(text, sigma, kind_)
+            return graphs[kind_].replay()
         if sharded:
             # one WM/WT over the whole job's world * n symbols: local builds, NCCL
             # histogram all_gather, then the merge over peer memory (p2p) or the
@@ -350,7 +357,10 @@ def main():
         "vs_baseline": None, "dtype": {1: "u8", 2: "u16", 4: "u32"}[sym_bytes], "data": "synthetic",
         "config": {"workload": args.config, "description": workloads.DESCRIPTIONS[args.config], "kind": kind,
                    "n_per_gpu": n, "sigma": sigma, "levels": code_width(sigma), "passes": npass,
-                   "l2": "inputs larger than L2 (text %d MiB per GPU vs 126 MB L2); no flush" % (n * sym_bytes >> 20),
+                   "l2": ("inputs larger than L2 (text %d MiB per GPU vs 126 MB L2); no flush" % (n * sym_bytes >> 20)
+                          if n * sym_bytes > (126 << 20) else
+                          "L2-resident input (text %d KiB); no flush: a launch-bound correctness config" % (n * sym_bytes >> 10)),
+                   "graph": bool(args.graph),
                    "parallelism": (f"sharded{world} (position shards; NCCL all_gather of histograms, "
                                    + ("merge over peer memory)" if transport == "p2p" else "NCCL all_to_all + merge)")
                                    if world > 1 else "single")},

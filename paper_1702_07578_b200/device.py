@@ -146,6 +146,25 @@ class DeviceBuilder:
             raise ValueError(f"symbols must lie in [0, {sigma})")
         return DeviceBuild(kind, n, sigma, w, lw, zeros, hist if histogram else None, bd, status)
 
+    def capture(self, text, sigma: int, kind: str = "wm", *, histogram: bool = False) -> "BuildGraph":
+        """Capture one build of ``text`` (a device tensor kept as the graph's input
+        buffer) into a CUDA graph: small, launch-bound builds replay it with one
+        launch.  Refill ``text`` in place and call ``replay()`` for the next build
+        of the same length / alphabet / kind."""
+        torch = _torch()
+        s = torch.cuda.Stream(self.device)
+        s.wait_stream(torch.cuda.current_stream(self.device))
+        outputs = None
+        with torch.cuda.stream(s):
+            outputs = self.alloc_outputs(int(text.numel()), sigma)
+            self.build(text, sigma, kind, histogram=histogram, outputs=outputs, stream=s, check=False)  # warm-up
+        s.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            res = self.build(text, sigma, kind, histogram=histogram, outputs=outputs,
+                             stream=torch.cuda.current_stream(self.device), check=False)
+        return BuildGraph(g, res, text)
+
     def build_host(self, arr: np.ndarray, sigma: int, kind: str, *, out_words: np.ndarray | None = None,
                    histogram: bool = False, stream=None):
         """Host buffers in and out through wvlt_build_host (H2D, build, D2H, sync).
@@ -198,6 +217,23 @@ class DeviceBuilder:
                                       src_starts.data_ptr() if ntasks > 0 else None, max(ntasks, 0),
                                       src_words.data_ptr() if src_words.numel() else None, s.cuda_stream)
         _lib.check(rc)
+
+
+class BuildGraph:
+    """A captured build (DeviceBuilder.capture): ``replay()`` reruns it on the current
+    contents of ``text``; ``result`` holds the output tensors, ``check()`` raises
+    ValueError if the last replay saw a symbol outside [0, sigma)."""
+
+    def __init__(self, graph, result: DeviceBuild, text):
+        self.graph, self.result, self.text = graph, result, text
+
+    def replay(self) -> DeviceBuild:
+        self.graph.replay()
+        return self.result
+
+    def check(self) -> None:
+        if int(self.result.status.item()) & _lib.STATUS_RANGE:
+            raise ValueError(f"symbols must lie in [0, {self.result.sigma})")
 
 
 _BUILDERS: dict = {}

@@ -255,3 +255,27 @@ def test_concurrent_builds_on_two_streams():
         torch.cuda.synchronize()
         for r, w in zip(got, want):
             assert torch.equal(r.level_words, w)
+
+
+@pytest.mark.parametrize("sigma,kind", [(256, "wt"), (5, "wm"), (1000, "wm"), (1 << 20, "wm")])
+def test_captured_build_replays(sigma, kind):
+    """DeviceBuilder.capture: one CUDA-graph replay per build of a refilled input
+    buffer gives the same words as a plain build."""
+    from paper_1702_07578_b200.device import DeviceBuilder
+
+    b = DeviceBuilder()
+    dt = torch.uint8 if sigma <= 256 else torch.uint16 if sigma <= 65536 else torch.uint32
+    n = 1 << 20
+    g = torch.Generator(device="cuda")
+    g.manual_seed(sigma)
+    buf = torch.randint(0, sigma, (n,), generator=g, device="cuda", dtype=torch.int64).to(dt)
+    cap = b.capture(buf, sigma, kind)
+    for _ in range(3):
+        buf.copy_(torch.randint(0, sigma, (n,), generator=g, device="cuda", dtype=torch.int64).to(dt))
+        res = cap.replay()
+        torch.cuda.synchronize()
+        want = b.build(buf.clone(), sigma, kind)
+        assert torch.equal(res.level_words, want.level_words)
+        if kind == "wm":
+            assert torch.equal(res.zeros, want.zeros)
+        cap.check()
