@@ -60,24 +60,28 @@ def pass_plan(n: int, sym_bytes: int, sigma: int, kind: str):
     vbits = 8 * sym_bytes
     bb = lambda b: 1 if b <= 8 else 2 if b <= 16 else 4  # noqa: E731
     out, ell = [], 0
-    tail = kind == "wm" and w > 8 and 0 < n < (1 << 32) - 64  # make_plan(): fused byte tail
+    fused = kind == "wm" and w > 8 and 0 < n < (1 << 32) - 64  # make_plan(): fused 4-/2-byte passes + byte tail
+    cur = bb(w) if 8 * sym_bytes < w else sym_bytes  # element bytes of the next stage's input (widened text)
     while ell < w:
-        if tail and w - ell <= 8:
-            out.append((ell, w - ell, 1, 0))
+        live = w - ell
+        if fused and live <= 8:
+            out.append((ell, live, 1, 0))
             break
-        in_b = sym_bytes if ell == 0 else bb(min(w - ell, vbits))
-        if ell == 0 and 8 * sym_bytes < w:
-            in_b = bb(w)  # widened text
-        if tail and 10 <= w - ell <= 16 and in_b == 2:  # k16.cuh: fused 2-byte pass, byte output
-            out.append((ell, w - ell - 8, 2, 1))
-            ell = w - 8
+        if fused and 18 <= live <= 24 and cur == 4:  # k32.cuh: fused 4-byte pass, 2-byte output
+            out.append((ell, live - 16, 4, 2))
+            ell, cur = w - 16, 2
             continue
-        K = min(KMAX, w - ell)
-        live_in = (w - ell) if kind == "wm" else w
-        live_out = (w - ell - K) if kind == "wm" else w
+        if fused and 10 <= live <= 16 and cur == 2:  # k16.cuh: fused 2-byte pass, byte output
+            out.append((ell, live - 8, 2, 1))
+            ell, cur = w - 8, 1
+            continue
+        K = min(KMAX, live)
+        live_in = live if kind == "wm" else w
+        live_out = (live - K) if kind == "wm" else w
         ib = sym_bytes if ell == 0 else bb(min(live_in, vbits))
         ob = bb(min(live_out, vbits)) if ell + K < w else 0
         out.append((ell, K, ib, min(ob, ib)))
+        cur = min(ob, ib)
         ell += K
     return out
 

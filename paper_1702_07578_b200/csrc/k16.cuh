@@ -331,10 +331,10 @@ struct K16Layout {
   int64_t ntiles, nchunks;
 };
 
-inline K16Layout k16_layout(int64_t n, int w) {
+inline K16Layout k16_layout(int64_t n, int w, int tile = K16_TILE) {
   K16Layout L;
   const int nb = 1 << w;
-  L.ntiles = (n + K16_TILE - 1) / K16_TILE;
+  L.ntiles = (n + tile - 1) / tile;
   L.nchunks = (L.ntiles + S8_CHUNK - 1) / S8_CHUNK;
   size_t off = 0;
   L.off_tcnt = off;

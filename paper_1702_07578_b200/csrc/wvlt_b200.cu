@@ -578,6 +578,10 @@ struct Plan {
   // levels from k16_lvl are one fused 2-byte pass (k16.cuh) whose byte output
   // feeds the tail; output + its tables in the other ping-pong buffer
   int k16_w, k16_lvl;
+  // WM, 4-byte input with 18..24 live bits (lean builds): the k32_w = live - 16
+  // levels from k32_lvl are one fused 4-byte pass (k32.cuh) whose 2-byte
+  // output feeds the fused 2-byte pass
+  int k32_w, k32_lvl;
 };
 
 __host__ __device__ inline int64_t chain_off(int k) { return (1ll << k) - 1; }  // level-k table in a 2^(w+1)-1 array
@@ -1751,6 +1755,7 @@ int log2i(int v) {
 
 size_t k8_workspace_total(int64_t n, int w);   // k8.cuh
 size_t k16_workspace_total(int64_t n, int w);  // k16.cuh
+size_t k32_workspace_total(int64_t n, int w);  // k32.cuh
 
 // lean: a WM build without histogram / borders (the fused 2-byte pass needs it)
 bool make_plan(int64_t n, int sym_bytes, int64_t sigma, int kind, Plan* P, bool lean = true) {
@@ -1779,13 +1784,22 @@ bool make_plan(int64_t n, int sym_bytes, int64_t sigma, int kind, Plan* P, bool 
 #else
   const bool k16 = false;
 #endif
+  int cur_bytes = sb;  // element bytes of the next stage's input
   while (l < w && !(tail && w - l <= 8)) {
-    if (k16 && w - l <= 16 && w - l >= 10 && (p == 0 ? sb : bytes_for_bits(w - l)) == 2) {
+    if (k16 && !P->k32_w && w - l <= 24 && w - l >= 18 && cur_bytes == 4) {
+      P->k32_w = w - l - 16;
+      P->k32_lvl = l;
+      l += P->k32_w;
+      cur_bytes = 2;
+      continue;
+    }
+    if (k16 && w - l <= 16 && w - l >= 10 && cur_bytes == 2) {
       P->k16_w = w - l - 8;
       P->k16_lvl = l;
       l += P->k16_w;
       break;
     }
+    if (P->k32_w) break;  // (not reached: the 4-byte pass leaves exactly 16 live bits)
     const int K = (w - l) < KMAX ? (w - l) : KMAX;
     P->lvl[p] = l;
     P->K[p] = K;
@@ -1804,6 +1818,7 @@ bool make_plan(int64_t n, int sym_bytes, int64_t sigma, int kind, Plan* P, bool 
         corr += 1ll << (l + j);
       }
     }
+    cur_bytes = P->out_bytes[p];
     l += K;
     ++p;
   }
@@ -1842,6 +1857,7 @@ bool make_plan(int64_t n, int sym_bytes, int64_t sigma, int kind, Plan* P, bool 
   off = align_up(off + (size_t)NDIG * max_nblk * 8, 256);
   if (tail) max_buf = std::max(max_buf, k8_workspace_total(n, P->tail_w));
   if (P->k16_w) max_buf = std::max(max_buf, align_up((size_t)n, 256) + k16_workspace_total(n, P->k16_w));
+  if (P->k32_w) max_buf = std::max(max_buf, align_up((size_t)n * 2, 256) + k32_workspace_total(n, P->k32_w));
   P->buf_bytes = align_up(max_buf ? max_buf : 16, 256);
   P->off_buf0 = off;
   off += P->buf_bytes;
@@ -2061,6 +2077,7 @@ void prof_mark(cudaStream_t s, int stage_id) {
 
 #include "k8.cuh"
 #include "k16.cuh"
+#include "k32.cuh"
 
 namespace {
 int build_device_impl(const void* text, int sym_bytes, int64_t n, int64_t sigma, int kind, uint64_t* level_words,
@@ -2208,7 +2225,7 @@ int build_device_impl(const void* text, int sym_bytes, int64_t n, int64_t sigma,
   g_prof.n = 0;
   prof_mark(s, -1);
   // (the fused passes write / zero their own levels)
-  const int fused_lvl = P.k16_w ? P.k16_lvl : P.tail_w ? P.tail_lvl : w;
+  const int fused_lvl = P.k32_w ? P.k32_lvl : P.k16_w ? P.k16_lvl : P.tail_w ? P.tail_lvl : w;
   if (fused_lvl > 0) {
     e = cudaMemsetAsync(level_words, 0, (size_t)fused_lvl * nwords * 8, s);
     if (e != cudaSuccess) return (int)e;
@@ -2324,6 +2341,20 @@ int build_device_impl(const void* text, int sym_bytes, int64_t n, int64_t sigma,
   }
   int curbuf = P.npass > 0 ? ((P.npass - 1) & 1) : -1;  // bufs[] index holding cur, -1 = the text
   int stage = P.npass;
+  if (P.k32_w) {
+    const int ob = curbuf == 0 ? 1 : 0;
+    uint16_t* out = (uint16_t*)bufs[ob];
+    const int64_t lk = P.k32_lvl;
+    const uint32_t vmax_ok = (uint32_t)std::min<int64_t>(sigma - 1, 0xFFFFFFFFll);
+    const int check = curbuf < 0 && vmax_ok < 0xFFFFFFFFu ? 1 : 0;  // text input: symbols must be < sigma
+    const int rc = build_k32((const uint32_t*)cur, n, P.k32_w, level_words + lk * nwords, zeros ? zeros + lk : nullptr,
+                             out, (unsigned char*)out + align_up((size_t)n * 2, 256), st_flag, vmax_ok, check, s,
+                             pass_done, ctx, (int)lk, stage);
+    if (rc) return rc;
+    ++stage;
+    cur = out;
+    curbuf = ob;
+  }
   if (P.k16_w) {
     const int ob = curbuf == 0 ? 1 : 0;
     uint8_t* out = (uint8_t*)bufs[ob];

@@ -45,7 +45,7 @@ def test_running_example():
 
 
 @pytest.mark.parametrize("kind", ["wt", "wm"])
-@pytest.mark.parametrize("sigma", SIGMA_GRID + (4, 17, 33, 100, 256, 1000, 1 << 16, 1 << 20))
+@pytest.mark.parametrize("sigma", SIGMA_GRID + (4, 17, 33, 100, 256, 1000, 1 << 16, (1 << 17) + 5, 1 << 20, 1 << 24))
 def test_tile_boundaries_vs_oracle(kind, sigma):
     rng = np.random.default_rng(sigma * 7 + (kind == "wm"))
     for n in (1, 31, 32, 33, 63, 64, 65, 4095, 4096, 4097, 8191, 8192, 8193, 16383, 16384, 16385, 32767, 32768, 32769, 40961, 49153,
