@@ -279,3 +279,23 @@ def test_captured_build_replays(sigma, kind):
         if kind == "wm":
             assert torch.equal(res.zeros, want.zeros)
         cap.check()
+
+
+@pytest.mark.parametrize("sigma,dt", [(5, torch.uint8), (200, torch.uint8), (1000, torch.uint16),
+                                      (300, torch.uint16), ((1 << 20) - 3, torch.uint32), (1 << 23, torch.uint32),
+                                      (70000, torch.uint32)])
+@pytest.mark.parametrize("kind", ["wm", "wt"])
+def test_device_range_check_every_path(sigma, dt, kind):
+    """The fused digit kernels (byte, 2-byte, 4-byte first passes) raise the status
+    bit for a symbol >= sigma anywhere in the text, including the last partial tile."""
+    from paper_1702_07578_b200.device import DeviceBuilder
+
+    b = DeviceBuilder()
+    n = 3 * 16384 + 123
+    g = torch.Generator(device="cuda")
+    g.manual_seed(sigma)
+    for pos in (0, 20_000, n - 1):
+        text = torch.randint(0, sigma, (n,), generator=g, device="cuda", dtype=torch.int64)
+        text[pos] = sigma
+        with pytest.raises(ValueError):
+            b.build(text.to(dt), sigma, kind)
