@@ -288,8 +288,8 @@ struct Tables8 {
   uint32_t gs[256];   // run starts in the global level
   uint32_t lb[256];   // symbols of earlier tiles in the run's group (scratch)
   uint16_t wpre[256]; // emission: destination words before each run (+ total)
-  uint16_t cW[256];   // level-W digit counts (scratch)
-  uint32_t lbW[256];  // level-W tile prefixes (scratch)
+  uint16_t cW[264];   // level-W digit counts (scratch, index d + d / 32)
+  uint32_t lbW[264];  // level-W tile prefixes (scratch, index d + d / 32)
 };
 
 // a tile's count / prefix row into registers (entry e = lane + 32 k)
@@ -316,8 +316,9 @@ __device__ __forceinline__ void table8_stage(Tables8& tt, int lane, const uint32
     const int e = lane + 32 * k;
     if (e < NB) {
       const int d = (int)rev_bits((unsigned)e, W);
-      tt.cW[d] = (uint16_t)rc[k];
-      tt.lbW[d] = rp[k];
+      // (bit-reversed d: the skew d + d / 32 spreads a warp's stores over the banks)
+      tt.cW[d + (d >> 5)] = (uint16_t)rc[k];
+      tt.lbW[d + (d >> 5)] = rp[k];
     }
   }
   __syncwarp();
@@ -336,8 +337,8 @@ __device__ __forceinline__ void table8_compute(Tables8& tt, const uint32_t* s_ba
       int c;
       uint32_t lb;
       if (j == W - 1) {
-        c = tt.cW[d] + tt.cW[d + mj];
-        lb = tt.lbW[d] + tt.lbW[d + mj];
+        c = tt.cW[d + (d >> 5)] + tt.cW[d + mj + ((d + mj) >> 5)];
+        lb = tt.lbW[d + (d >> 5)] + tt.lbW[d + mj + ((d + mj) >> 5)];
       } else {
         const int up = (2 << j) - 2;
         c = tt.cnt[up + d] + tt.cnt[up + d + mj];
