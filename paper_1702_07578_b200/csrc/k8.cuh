@@ -351,54 +351,44 @@ __device__ __forceinline__ void table8_compute(Tables8& tt, const uint32_t* s_ba
     }
     __syncwarp();
   }
-  // tile-local run starts: exclusive prefix of each level's run sizes
-#pragma unroll 1
-  for (int j = 1; j < W; ++j) {
-    const int mj = 1 << j, r0 = mj - 2;
-    const int per = (mj + 31) / 32;  // consecutive runs per lane
-    int loc = 0;
-    for (int k = 0; k < per; ++k) {
-      const int d = lane * per + k;
-      if (d < mj) loc += tt.cnt[r0 + d];
-    }
-    const int ex = (int)warp_incl_scan((uint32_t)loc) - loc;
-    int run = ex;
-    for (int k = 0; k < per; ++k) {
-      const int d = lane * per + k;
-      if (d < mj) {
-        tt.ls[r0 + d] = (uint16_t)run;
-        run += tt.cnt[r0 + d];
-      }
-    }
-  }
-  __syncwarp();
-  // destination words per run, flattened exclusive prefix
+  // one pass over the flattened runs (lane: PER consecutive ones): exclusive
+  // prefixes of the run sizes (P) and of the destination words (wpre); a
+  // run's tile-local start is P minus P at its level's first run
   {
-    constexpr int per = (NR + 31) / 32;
-    int nw[per];
-    int loc = 0;
+    constexpr int PER = (NR + 31) / 32;
+    uint32_t c[PER], nw[PER];
+    uint32_t sc = 0, sw = 0;
 #pragma unroll
-    for (int k = 0; k < per; ++k) {
-      const int r = lane * per + k;
+    for (int k = 0; k < PER; ++k) {
+      const int r = lane * PER + k;
+      c[k] = r < NR ? tt.cnt[r] : 0u;
       nw[k] = 0;
-      if (r < NR) {
-        const int c = tt.cnt[r];
-        if (c) {
-          const int64_t g = tt.gs[r];
-          nw[k] = (int)(((g + c - 1) >> 6) - (g >> 6) + 1);
-        }
+      if (c[k]) {
+        const uint32_t g = tt.gs[r];
+        nw[k] = ((g + c[k] - 1) >> 6) - (g >> 6) + 1;
       }
-      loc += nw[k];
+      sc += c[k];
+      sw += nw[k];
     }
-    const int ex = (int)warp_incl_scan((uint32_t)loc) - loc;
-    int run = ex;
+    uint32_t pc = warp_incl_scan(sc) - sc, pw = warp_incl_scan(sw) - sw;
+    __syncwarp();
 #pragma unroll
-    for (int k = 0; k < per; ++k) {
-      const int r = lane * per + k;
-      if (r < NR) tt.wpre[r] = (uint16_t)run;
-      run += nw[k];
+    for (int k = 0; k < PER; ++k) {
+      const int r = lane * PER + k;
+      if (r < NR) {
+        tt.lb[r] = pc;  // (lb is free once gs is set) P of run r
+        tt.wpre[r] = (uint16_t)pw;
+      }
+      pc += c[k];
+      pw += nw[k];
     }
-    if (lane == 31) tt.wpre[NR] = (uint16_t)run;
+    if (lane == 31) tt.wpre[NR] = (uint16_t)pw;
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int r = lane * PER + k;
+      if (r < NR) tt.ls[r] = (uint16_t)(tt.lb[r] - tt.lb[(1 << (31 - __clz(r + 2))) - 2]);
+    }
   }
 }
 
