@@ -196,6 +196,7 @@ int wvlt_query(int kind, int op, const uint64_t* level_words, int64_t n, int wid
 #define WVLT_STAGE_TABLES 2
 #define WVLT_STAGE_PASS0 3
 #define WVLT_STAGE_SCAN0 64
+#define WVLT_STAGE_REORDER 60 /* WT of a wide alphabet: matrix levels reordered into tree order */
 int wvlt_profile_enable(int on);
 int wvlt_profile_read(float* stage_ms, int* stage_ids, int max_stages);
 

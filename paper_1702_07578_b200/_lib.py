@@ -20,7 +20,7 @@ KINDS = {"wt": KIND_WT, "wm": KIND_WM}
 E_ARG, E_WIDTH, E_WORKSPACE, E_RANGE = -1, -2, -3, -4
 STATUS_RANGE = 1
 MAX_WIDTH = 24
-STAGE_MEMSET, STAGE_HIST, STAGE_TABLES, STAGE_PASS0, STAGE_SCAN0 = 0, 1, 2, 3, 64
+STAGE_MEMSET, STAGE_HIST, STAGE_TABLES, STAGE_PASS0, STAGE_SCAN0, STAGE_REORDER = 0, 1, 2, 3, 64, 60
 
 _lib = None
 
@@ -94,7 +94,7 @@ def profile_read(max_stages: int = 40) -> list[tuple[str, float]]:
     k = load().wvlt_profile_read(ms, ids, max_stages)
     if k < 0:
         raise WvltError(f"profile read failed ({k})")
-    names = {STAGE_MEMSET: "memset", STAGE_HIST: "hist", STAGE_TABLES: "tables"}
+    names = {STAGE_MEMSET: "memset", STAGE_HIST: "hist", STAGE_TABLES: "tables", STAGE_REORDER: "reorder"}
     def name(i):
         if i in names:
             return names[i]

@@ -2084,6 +2084,126 @@ int build_device_impl(const void* text, int sym_bytes, int64_t n, int64_t sigma,
                       int64_t* zeros, int64_t* hist, int64_t* borders, void* workspace, size_t workspace_bytes,
                       int32_t* status, void* stream, void (*pass_done)(void*, int, int), void* ctx);
 }
+// ---------------------------------------------------------------------------
+// WT of an alphabet wider than a byte: the WM levels (fused passes) reordered
+// into tree order.  Both hold level l's bits grouped by l-bit prefix, the WM
+// in bit-reversed prefix order, the WT in numeric order (structures.py:43-58,
+// 176-182; the same fact wt2wm.py:205-227 uses the other way round), so every
+// level is one gather_bits plan whose tasks are the prefix groups: destination
+// bounds = WT interval starts, sources = WM group starts -- both from the
+// histogram's fold chain.
+// ---------------------------------------------------------------------------
+namespace {
+
+__global__ void fold_level_kernel(int64_t* __restrict__ chain, int k) {  // level k from level k + 1
+  const int64_t* up = chain + chain_off(k + 1);
+  int64_t* dn = chain + chain_off(k);
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < (1ll << k);
+       q += (int64_t)gridDim.x * blockDim.x)
+    dn[q] = up[2 * q] + up[2 * q + 1];
+}
+
+// one CTA per level k >= 2 (blockIdx.x + 2): WT starts in numeric order (with
+// the end n as sentinel) and WM starts indexed by numeric prefix
+__global__ void __launch_bounds__(TAB_THREADS) level_starts_kernel(const int64_t* __restrict__ chain,
+                                                                   int64_t* __restrict__ wt_bounds,
+                                                                   int64_t* __restrict__ wm_starts, int64_t n) {
+  __shared__ int64_t s_red[33];
+  const int k = blockIdx.x + 2;
+  const int64_t* c = chain + chain_off(k);
+  int64_t* wt = wt_bounds + chain_off(k) + k;
+  int64_t* wm = wm_starts + chain_off(k);
+  block_scan_excl(
+      1ll << k, [&](int64_t i) { return c[i]; }, [&](int64_t i, int64_t v) { wt[i] = v; }, s_red);
+  block_scan_excl(
+      1ll << k, [&](int64_t r) { return c[rev_bits((unsigned)r, k)]; },
+      [&](int64_t r, int64_t v) { wm[rev_bits((unsigned)r, k)] = v; }, s_red);
+  if (threadIdx.x == 0) wt[1ll << k] = n;
+}
+
+struct WtViaWm {
+  size_t off_temp, off_zeros, off_chain, off_bounds, off_wm, off_ws, total;
+};
+
+inline bool wt_via_wm_layout(int64_t n, int sym_bytes, int64_t sigma, WtViaWm* L) {
+  Plan P;
+  if (!make_plan(n, sym_bytes, sigma, WVLT_KIND_WM, &P, true) || !P.tail_w) return false;
+  const int w = P.width;
+  const int64_t nwords = (n + 63) >> 6;
+  size_t off = 0;
+  L->off_temp = off;
+  off = align_up(off + (size_t)w * nwords * 8, 256);
+  L->off_zeros = off;
+  off = align_up(off + (size_t)w * 8, 256);
+  L->off_chain = off;
+  off = align_up(off + ((size_t)2 << w) * 8, 256);
+  L->off_bounds = off;
+  off = align_up(off + (((size_t)2 << w) + w) * 8, 256);
+  L->off_wm = off;
+  off = align_up(off + ((size_t)2 << w) * 8, 256);
+  L->off_ws = off;
+  L->total = off + P.total;
+  return true;
+}
+
+int build_wt_via_wm(const void* text, int sym_bytes, int64_t n, int64_t sigma, uint64_t* level_words, int64_t* zeros,
+                    int64_t* hist, unsigned char* ws, const WtViaWm& L, int32_t* status, cudaStream_t s,
+                    void (*pass_done)(void*, int, int), void* ctx) {
+  const int w = code_width_host(sigma);
+  const int64_t nwords = (n + 63) >> 6;
+  uint64_t* temp = (uint64_t*)(ws + L.off_temp);
+  int64_t* chain = (int64_t*)(ws + L.off_chain);
+  int64_t* bounds = (int64_t*)(ws + L.off_bounds);
+  int64_t* wmst = (int64_t*)(ws + L.off_wm);
+  // the matrix (its kernels check the symbol range; a level's zero count is the
+  // same in both layouts)
+  int rc = build_device_impl(text, sym_bytes, n, sigma, WVLT_KIND_WM, temp, zeros ? zeros : (int64_t*)(ws + L.off_zeros), nullptr,
+                             nullptr, ws + L.off_ws, L.total - L.off_ws, status, s, nullptr, nullptr);
+  if (rc) return rc;
+  // histogram -> fold chain -> per-level starts
+  unsigned long long* hw = (unsigned long long*)(chain + chain_off(w));
+  cudaError_t e = cudaMemsetAsync(hw, 0, ((size_t)1 << w) * 8, s);
+  if (e != cudaSuccess) return (int)e;
+  // (the matrix build checked the range; its zero-count scratch takes the status bits)
+  e = launch_hist_generic(text, sym_bytes, n, w, hw, status ? status : (int32_t*)(ws + L.off_zeros), s);
+  if (e != cudaSuccess) return (int)e;
+  int launches = g_launches + 1;
+  for (int k = w - 1; k >= 2; --k) {
+    const int64_t q = 1ll << k;
+    fold_level_kernel<<<(unsigned)std::min<int64_t>((q + 255) / 256, (int64_t)sm_count() * 8), 256, 0, s>>>(chain, k);
+    ++launches;
+  }
+  if (w > 2) {
+    level_starts_kernel<<<w - 2, TAB_THREADS, 0, s>>>(chain, bounds, wmst, n);
+    ++launches;
+  }
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return (int)e;
+  // levels 0 and 1 are identical; the others are reordered group by group
+  e = cudaMemcpyAsync(level_words, temp, (size_t)std::min(w, 2) * nwords * 8, cudaMemcpyDeviceToDevice, s);
+  if (e != cudaSuccess) return (int)e;
+  int64_t blocks = (nwords + 256 * MERGE_WORDS_PER_LANE - 1) / (256 * MERGE_WORDS_PER_LANE);
+  blocks = std::min<int64_t>(blocks, (int64_t)sm_count() * 32);
+  for (int k = 2; k < w; ++k) {
+    merge_bits_kernel<<<(unsigned)blocks, 256, 0, s>>>(level_words + (int64_t)k * nwords, 0, nwords, n,
+                                                        bounds + chain_off(k) + k, wmst + chain_off(k), 1ll << k,
+                                                        temp + (int64_t)k * nwords);
+    ++launches;
+  }
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return (int)e;
+  if (hist) {
+    e = cudaMemcpyAsync(hist, hw, ((size_t)1 << w) * 8, cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) return (int)e;
+  }
+  prof_mark(s, WVLT_STAGE_REORDER);
+  g_launches = launches;
+  if (pass_done) pass_done(ctx, 0, w);
+  return 0;
+}
+
+}  // namespace
+
 
 // ---------------------------------------------------------------------------
 // C ABI
@@ -2132,7 +2252,10 @@ size_t wvlt_workspace_bytes(int64_t n, int sym_bytes, int64_t sigma, int kind) {
   if (!make_plan(n, sym_bytes, sigma, kind, &P, true)) return 0;
   Plan P2;
   make_plan(n, sym_bytes, sigma, kind, &P2, false);
-  const size_t total = std::max(P.total, P2.total);
+  size_t total = std::max(P.total, P2.total);
+  WtViaWm L;
+  if (kind == WVLT_KIND_WT && P.width > 8 && n > 0 && wt_via_wm_layout(n, sym_bytes, sigma, &L))
+    total = std::max(total, L.total);
   if (k8_eligible(sym_bytes, P.width, n) && !P.widen_bytes) return std::max(total, k8_layout(n, P.width).total);
   return total;
 }
@@ -2181,6 +2304,16 @@ int build_device_impl(const void* text, int sym_bytes, int64_t n, int64_t sigma,
     if (e != cudaSuccess) return (int)e;
   }
   const int64_t nwords = (n + 63) >> 6;
+#ifndef WVLT_NO_WT_VIA_WM
+  if (kind == WVLT_KIND_WT && !borders && n > 0 && w > 8 && text && level_words && workspace) {
+    WtViaWm L;
+    if (wt_via_wm_layout(n, sym_bytes, sigma, &L)) {
+      if (workspace_bytes < L.total) return WVLT_E_WORKSPACE;
+      return build_wt_via_wm(text, sym_bytes, n, sigma, level_words, zeros, hist, (unsigned char*)workspace, L, status,
+                             s, pass_done, ctx);
+    }
+  }
+#endif
   if (n == 0 || w == 0) {
     // degenerate: no level bits to build (construct.py:457-458, bitperm.code_width)
     if (w == 0 && hist) {
