@@ -112,6 +112,27 @@ int wvlt_build_host(const void* host_text, int sym_bytes, int64_t n, int64_t sig
                     void* dev_text, uint64_t* dev_level_words, void* dev_small,
                     void* workspace, size_t workspace_bytes, void* stream);
 
+/*
+ * `count` independent builds with host buffers (same sym_bytes, sigma and kind;
+ * text i has ns[i] symbols), software-pipelined over three streams: the text of
+ * build i+1 goes host->device while build i runs on `stream` and build i-1's
+ * level words come back (pass by pass, as in wvlt_build_host).  PCIe is full
+ * duplex, so in steady state a build costs max(upload, download, compute)
+ * instead of their sum -- the serving form of wvlt_build_host for a queue of
+ * texts.  Device buffers hold two slots each: dev_text 2 x dev_text_slot_bytes,
+ * dev_level_words 2 x dev_words_slot_bytes, dev_small 2 x (2^width + width + 1)
+ * int64.  Outputs: host_level_words[i] (width x ceil(ns[i]/64) words),
+ * host_zeros + i*width (may be NULL), host_hist + i*2^width (may be NULL: the
+ * histogram-free WM build), host_status[i] (nonzero flags: build i saw a symbol
+ * out of range).  Synchronizes before returning; returns WVLT_E_RANGE if any
+ * build saw an out-of-range symbol.
+ */
+int wvlt_build_host_batch(int count, const void* const* host_texts, const int64_t* ns, int sym_bytes,
+                          int64_t sigma, int kind, uint64_t* const* host_level_words, int64_t* host_zeros,
+                          int64_t* host_hist, int32_t* host_status, void* dev_text, size_t dev_text_slot_bytes,
+                          uint64_t* dev_level_words, size_t dev_words_slot_bytes, void* dev_small,
+                          void* workspace, size_t workspace_bytes, void* stream);
+
 /* Number of this library's kernels the calling thread's last build launched. */
 int wvlt_last_launches(void);
 

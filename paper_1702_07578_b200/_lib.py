@@ -55,6 +55,8 @@ def load():
     L.wvlt_build_device.restype = i32
     L.wvlt_build_host.argtypes = [vp, i32, i64, i64, i32, vp, vp, vp, vp, vp, vp, vp, sz, vp]
     L.wvlt_build_host.restype = i32
+    L.wvlt_build_host_batch.argtypes = [i32, vp, vp, i32, i64, i32, vp, vp, vp, vp, vp, sz, vp, sz, vp, vp, sz, vp]
+    L.wvlt_build_host_batch.restype = i32
     L.wvlt_merge_bits.argtypes = [vp, i64, i64, i64, vp, vp, i64, vp, vp]
     L.wvlt_merge_bits.restype = i32
     L.wvlt_merge_levels_peer.argtypes = [vp, i64, i32, i64, i64, i64, vp, vp, vp, vp, vp, vp, i32, vp]

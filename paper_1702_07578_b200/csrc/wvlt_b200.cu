@@ -2607,6 +2607,124 @@ int wvlt_build_host(const void* host_text, int sym_bytes, int64_t n, int64_t sig
   return (hstatus & WVLT_STATUS_RANGE) ? WVLT_E_RANGE : 0;
 }
 
+// A sequence of independent builds with host buffers, software-pipelined over
+// three streams: uploads (H2D of build i+1's text), compute (`stream`: build i)
+// and downloads (D2H of build i-1's levels, which start pass by pass as in
+// wvlt_build_host).  Device text / levels / small buffers are double-buffered
+// (two slots); the workspace is used by the compute stream only.  PCIe is full
+// duplex, so in steady state a build costs max(upload, download, compute)
+// instead of their sum.
+int wvlt_build_host_batch(int count, const void* const* host_texts, const int64_t* ns, int sym_bytes, int64_t sigma,
+                          int kind, uint64_t* const* host_level_words, int64_t* host_zeros, int64_t* host_hist,
+                          int32_t* host_status, void* dev_text, size_t dev_text_slot_bytes, uint64_t* dev_level_words,
+                          size_t dev_words_slot_bytes, void* dev_small, void* workspace, size_t workspace_bytes,
+                          void* stream) {
+  if (count < 0 || !(sym_bytes == 1 || sym_bytes == 2 || sym_bytes == 4) || sigma < 1) return WVLT_E_ARG;
+  if (count == 0) return 0;
+  if (!host_texts || !ns || !host_level_words || !host_status || !dev_small) return WVLT_E_ARG;
+  const int w = code_width_host(sigma);
+  if (w > WVLT_MAX_WIDTH) return WVLT_E_WIDTH;
+  for (int i = 0; i < count; ++i) {
+    const int64_t n = ns[i];
+    if (n < 0 || (size_t)n * sym_bytes > dev_text_slot_bytes) return WVLT_E_ARG;
+    if ((size_t)w * ((n + 63) >> 6) * 8 > dev_words_slot_bytes) return WVLT_E_ARG;
+    if (n > 0 && (!host_texts[i] || !dev_text)) return WVLT_E_ARG;
+    if (w > 0 && n > 0 && (!host_level_words[i] || !dev_level_words)) return WVLT_E_ARG;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e;
+  static thread_local cudaStream_t up = nullptr, down = nullptr;
+  static thread_local cudaEvent_t ev_up[2], ev_comp[2], ev_down[2], ev_pass[2][MAXP];
+  if (!up) {
+    e = cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&down, cudaStreamNonBlocking);
+    for (int k = 0; k < 2 && e == cudaSuccess; ++k) {
+      e = cudaEventCreateWithFlags(&ev_up[k], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_comp[k], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_down[k], cudaEventDisableTiming);
+      for (int i = 0; i < MAXP && e == cudaSuccess; ++i) e = cudaEventCreateWithFlags(&ev_pass[k][i], cudaEventDisableTiming);
+    }
+    if (e != cudaSuccess) {
+      up = nullptr;
+      return (int)e;
+    }
+  }
+  const size_t small_slot = ((size_t)1 << w) + w + 1;  // int64 entries: status, zeros, hist
+  // the small outputs come back through page-locked staging (a copy into pageable
+  // memory would block this thread until the download stream reached it, and
+  // with it the enqueueing of the next upload)
+  static thread_local int64_t* stage = nullptr;
+  static thread_local size_t stage_len = 0;
+  const size_t need_stage = (size_t)count * small_slot;
+  if (stage_len < need_stage) {
+    if (stage) cudaFreeHost(stage);
+    stage = nullptr;
+    stage_len = 0;
+    if ((e = cudaHostAlloc((void**)&stage, need_stage * 8, cudaHostAllocDefault)) != cudaSuccess) return (int)e;
+    stage_len = need_stage;
+  }
+  int rc = 0;
+  for (int i = 0; i < count && !rc; ++i) {
+    const int slot = i & 1;
+    const int64_t n = ns[i];
+    const int64_t nwords = (n + 63) >> 6;
+    unsigned char* dtext = (unsigned char*)dev_text + slot * dev_text_slot_bytes;
+    uint64_t* dwords = (uint64_t*)((unsigned char*)dev_level_words + slot * dev_words_slot_bytes);
+    int64_t* small = (int64_t*)dev_small + slot * small_slot;
+    // upload: the slot's text is free once build i-2 has run
+    if (i >= 2 && (e = cudaStreamWaitEvent(up, ev_comp[slot], 0)) != cudaSuccess) return (int)e;
+    if (n > 0 && (e = cudaMemcpyAsync(dtext, host_texts[i], (size_t)n * sym_bytes, cudaMemcpyHostToDevice, up)) != cudaSuccess)
+      return (int)e;
+    if ((e = cudaEventRecord(ev_up[slot], up)) != cudaSuccess) return (int)e;
+    // compute: after the upload, and after build i-2's levels have left the slot
+    if ((e = cudaStreamWaitEvent(s, ev_up[slot], 0)) != cudaSuccess) return (int)e;
+    if (i >= 2 && (e = cudaStreamWaitEvent(s, ev_down[slot], 0)) != cudaSuccess) return (int)e;
+    HostCopy hc;
+    hc.main = s;
+    hc.copy = down;
+    for (int k = 0; k < MAXP; ++k) hc.ev[k] = ev_pass[slot][k];
+    hc.nev = 0;
+    hc.host = host_level_words[i];
+    hc.dev = dwords;
+    hc.nwords = (w > 0) ? nwords : 0;
+    hc.err = cudaSuccess;
+    int32_t* dstatus = (int32_t*)small;
+    int64_t* dzeros = small + 1;
+    int64_t* dhist = small + 1 + w;
+    int64_t* hh = host_hist ? host_hist + ((size_t)i << w) : nullptr;
+    rc = build_device_impl(dtext, sym_bytes, n, sigma, kind, dwords, dzeros, hh ? dhist : nullptr, nullptr, workspace,
+                           workspace_bytes, dstatus, s, host_copy_pass, &hc);
+    if (rc) break;
+    if (hc.err != cudaSuccess) return (int)hc.err;
+    if ((e = cudaEventRecord(ev_comp[slot], s)) != cudaSuccess) return (int)e;
+    // download: whatever the passes did not already send, then the small outputs
+    if ((e = cudaStreamWaitEvent(down, ev_comp[slot], 0)) != cudaSuccess) return (int)e;
+    if (w > 0 && nwords > 0 && hc.nev == 0 &&
+        (e = cudaMemcpyAsync(host_level_words[i], dwords, (size_t)w * nwords * 8, cudaMemcpyDeviceToHost, down)) !=
+            cudaSuccess)
+      return (int)e;
+    // status, zeros and histogram are contiguous in the slot: one small copy
+    if ((e = cudaMemcpyAsync(stage + (size_t)i * small_slot, small, (1 + w + (hh ? ((size_t)1 << w) : 0)) * 8,
+                             cudaMemcpyDeviceToHost, down)) != cudaSuccess)
+      return (int)e;
+    if ((e = cudaEventRecord(ev_down[slot], down)) != cudaSuccess) return (int)e;
+  }
+  cudaError_t e1 = cudaStreamSynchronize(up), e2 = cudaStreamSynchronize(s), e3 = cudaStreamSynchronize(down);
+  if (rc) return rc;
+  if (e1 != cudaSuccess) return (int)e1;
+  if (e2 != cudaSuccess) return (int)e2;
+  if (e3 != cudaSuccess) return (int)e3;
+  int range = 0;
+  for (int i = 0; i < count; ++i) {
+    const int64_t* st = stage + (size_t)i * small_slot;
+    host_status[i] = *(const int32_t*)st;
+    if (host_zeros && w > 0) memcpy(host_zeros + (size_t)i * w, st + 1, (size_t)w * 8);
+    if (host_hist) memcpy(host_hist + ((size_t)i << w), st + 1 + w, ((size_t)1 << w) * 8);
+    if (host_status[i] & WVLT_STATUS_RANGE) range = 1;
+  }
+  return range ? WVLT_E_RANGE : 0;
+}
+
 int wvlt_last_launches(void) { return g_launches; }
 
 int wvlt_merge_bits(uint64_t* dst_words, int64_t word_lo, int64_t word_hi, int64_t n_bits, const int64_t* bounds,

@@ -7,6 +7,7 @@ hand-written sm_100a kernels of ``csrc/wvlt_b200.cu``.
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass
 
 import numpy as np
@@ -199,6 +200,65 @@ class DeviceBuilder:
             raise ValueError(f"symbols must lie in [0, {sigma})")
         _lib.check(rc)
         return out_words, [int(z) for z in zeros[:w]], (hist if histogram else None)
+
+    def build_host_batch(self, arrs, sigma: int, kind: str, *, out_words=None, histogram: bool = False,
+                         stream=None):
+        """A queue of independent builds through wvlt_build_host_batch: the upload of
+        text i+1, the build of text i and the download of build i-1's levels overlap
+        (three streams, double-buffered device buffers).
+
+        ``arrs`` are contiguous host arrays of one dtype (page-locked for full PCIe
+        bandwidth); ``out_words[i]`` (optional) receives build i's level words.
+        Returns a list of (level_words, zeros, hist or None) per text, like
+        build_host.  Raises ValueError if any text has a symbol outside [0, sigma).
+        """
+        torch = _torch()
+        arrs = list(arrs)
+        count = len(arrs)
+        if count == 0:
+            return []
+        dt = arrs[0].dtype
+        if dt not in (np.uint8, np.uint16, np.uint32):
+            raise ValueError("host texts must be contiguous uint8/uint16/uint32 arrays")
+        for a in arrs:
+            if a.dtype != dt or not a.flags.c_contiguous or a.ndim != 1:
+                raise ValueError("host texts must be contiguous 1-D arrays of one dtype")
+        sb = dt.itemsize
+        w = code_width(sigma)
+        ns = np.array([a.size for a in arrs], dtype=np.int64)
+        nmax = int(ns.max())
+        nw = [(int(n) + 63) >> 6 for n in ns]
+        if out_words is None:
+            out_words = [np.empty((w, k), dtype=np.uint64) for k in nw]
+        for o, k in zip(out_words, nw):
+            if o.dtype != np.uint64 or not o.flags.c_contiguous or o.size < w * k:
+                raise ValueError("out_words[i] must be a contiguous uint64 array of width x ceil(n_i/64) words")
+        zeros = np.zeros((count, max(w, 1)), dtype=np.int64)
+        hist = np.zeros((count, 1 << w), dtype=np.int64) if histogram else None
+        status = np.zeros(count, dtype=np.int32)
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        text_slot = max(nmax * sb, 16)
+        text_slot = (text_slot + 255) // 256 * 256
+        words_slot = max(w * ((nmax + 63) >> 6) * 8, 8)
+        words_slot = (words_slot + 255) // 256 * 256
+        with torch.cuda.stream(s):
+            dev_text = torch.empty(2 * text_slot, dtype=torch.uint8, device=self.device)
+            dev_words = torch.empty(2 * words_slot // 8, dtype=torch.int64, device=self.device)
+            dev_small = torch.empty(2 * ((1 << w) + w + 1), dtype=torch.int64, device=self.device)
+        ws, need = self.workspace(nmax, sb, sigma, kind, s)
+        texts_p = (ctypes.c_void_p * count)(*[a.ctypes.data if a.size else None for a in arrs])
+        words_p = (ctypes.c_void_p * count)(*[o.ctypes.data if o.size else None for o in out_words])
+        rc = self.lib.wvlt_build_host_batch(
+            count, ctypes.cast(texts_p, ctypes.c_void_p), ns.ctypes.data, sb, sigma, _lib.KINDS[kind],
+            ctypes.cast(words_p, ctypes.c_void_p), zeros.ctypes.data, hist.ctypes.data if histogram else None,
+            status.ctypes.data, dev_text.data_ptr(), text_slot, dev_words.data_ptr(), words_slot,
+            dev_small.data_ptr(), ws.data_ptr(), need, s.cuda_stream)
+        if rc == _lib.E_RANGE:
+            bad = [i for i in range(count) if status[i]]
+            raise ValueError(f"symbols must lie in [0, {sigma}) (texts {bad})")
+        _lib.check(rc)
+        return [(out_words[i], [int(z) for z in zeros[i, :w]], (hist[i] if histogram else None))
+                for i in range(count)]
 
     def merge_bits(self, dst_words, word_lo: int, word_hi: int, n_bits: int, bounds, src_starts, src_words,
                    stream=None, dst_offset_words: int = 0) -> None:

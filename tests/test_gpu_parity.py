@@ -299,3 +299,34 @@ def test_device_range_check_every_path(sigma, dt, kind):
         text[pos] = sigma
         with pytest.raises(ValueError):
             b.build(text.to(dt), sigma, kind)
+
+
+@pytest.mark.parametrize("sigma,kind,hist", [(256, "wm", False), (256, "wt", True), (5, "wm", True),
+                                             (1000, "wt", True), (1 << 20, "wm", False)])
+def test_pipelined_host_batch_matches_single_builds(sigma, kind, hist):
+    """wvlt_build_host_batch (upload / build / download overlapped over three
+    streams, double-buffered slots): every build of a ragged queue of texts --
+    empty, sub-word, tile-boundary and multi-tile lengths -- equals its own
+    oracle build, zeros and histogram included."""
+    from paper_1702_07578_b200.device import DeviceBuilder, sym_dtype_for_sigma
+
+    rng = np.random.default_rng(sigma + len(kind))
+    dt = sym_dtype_for_sigma(sigma)
+    lens = [1_000_003, 0, 63, 16384, 16385, 2_000_000, 777]
+    texts = [rng.integers(0, sigma, n).astype(dt) for n in lens]
+    b = DeviceBuilder()
+    res = b.build_host_batch(texts, sigma, kind, histogram=hist)
+    assert len(res) == len(texts)
+    for t, (words, zeros, h) in zip(texts, res):
+        ww, wz, wh = oracle.build(t, sigma, kind, "pc")
+        assert np.array_equal(np.asarray(words).reshape(ww.shape), ww)
+        if kind == "wm":
+            assert list(zeros) == list(wz)
+        if hist:
+            assert np.array_equal(h, np.bincount(t, minlength=1 << (sigma - 1).bit_length()).astype(np.int64))
+    # a bad symbol in one text of the queue raises the reference's ValueError
+    bad = [texts[0].copy(), texts[5].copy()]
+    bad[1][12345] = sigma if sigma < np.iinfo(dt).max + 1 else bad[1][12345]
+    if sigma < np.iinfo(dt).max + 1:
+        with pytest.raises(ValueError):
+            b.build_host_batch(bad, sigma, kind)
