@@ -2104,7 +2104,7 @@ __global__ void fold_level_kernel(int64_t* __restrict__ chain, int k) {  // leve
 }
 
 // one CTA per level k >= 2 (blockIdx.x + 2): WT starts in numeric order (with
-// the end n as sentinel) and WM starts indexed by numeric prefix
+// the end n as sentinel) and (if wm_starts) WM starts indexed by numeric prefix
 __global__ void __launch_bounds__(TAB_THREADS) level_starts_kernel(const int64_t* __restrict__ chain,
                                                                    int64_t* __restrict__ wt_bounds,
                                                                    int64_t* __restrict__ wm_starts, int64_t n) {
@@ -2115,14 +2115,119 @@ __global__ void __launch_bounds__(TAB_THREADS) level_starts_kernel(const int64_t
   int64_t* wm = wm_starts + chain_off(k);
   block_scan_excl(
       1ll << k, [&](int64_t i) { return c[i]; }, [&](int64_t i, int64_t v) { wt[i] = v; }, s_red);
-  block_scan_excl(
-      1ll << k, [&](int64_t r) { return c[rev_bits((unsigned)r, k)]; },
-      [&](int64_t r, int64_t v) { wm[rev_bits((unsigned)r, k)] = v; }, s_red);
+  if (wm_starts)
+    block_scan_excl(
+        1ll << k, [&](int64_t r) { return c[rev_bits((unsigned)r, k)]; },
+        [&](int64_t r, int64_t v) { wm[rev_bits((unsigned)r, k)] = v; }, s_red);
   if (threadIdx.x == 0) wt[1ll << k] = n;
+}
+
+// Group sizes of the matrix levels from the matrix itself (the recurrence of
+// recover_histogram, wt2wm.py:137-156, on the WM layout): the group of prefix
+// P at level l starts at s and holds c symbols; its zero child 2P starts at
+// rank0_l(s) in level l+1 and its one child 2P+1 at Z_l + s - rank0_l(s), with
+// sizes rank0_l(s + c) - rank0_l(s) and the rest.  One rank query per group
+// and level replaces the 2^w-bin histogram of the text.
+// Rank directory: per level, per 512-bit block the ones before it inside its
+// chunk of RK_CHUNK blocks (u32), and per chunk the ones before it (i64).
+constexpr int RK_THREADS = 256;
+constexpr int RK_PER = 4;  // blocks per thread
+constexpr int RK_CHUNK = RK_THREADS * RK_PER;
+
+__global__ void __launch_bounds__(RK_THREADS) rank_blocks_kernel(const uint64_t* __restrict__ words, int64_t nwords,
+                                                                int64_t nblk, int64_t nchunk,
+                                                                uint32_t* __restrict__ blk_pre,
+                                                                int64_t* __restrict__ chunk_pre) {
+  __shared__ uint32_t s_w[RK_THREADS / 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int level = blockIdx.y;
+  const uint64_t* L = words + (int64_t)level * nwords;
+  uint32_t* bp = blk_pre + (int64_t)level * nblk;
+  uint32_t carry = 0;
+#pragma unroll 1
+  for (int i = 0; i < RK_PER; ++i) {
+    // block b = chunk * RK_CHUNK + i * RK_THREADS + thread: a warp reads 2 KB contiguous
+    const int64_t b = (int64_t)blockIdx.x * RK_CHUNK + i * RK_THREADS + threadIdx.x;
+    uint32_t c = 0;
+    if (b < nblk) {
+      const int64_t w0 = b * 8;
+      if (w0 + 8 <= nwords && !(reinterpret_cast<uintptr_t>(L + w0) & 15)) {
+        const ulonglong2* q = reinterpret_cast<const ulonglong2*>(L + w0);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const ulonglong2 v = __ldcs(q + k);
+          c += __popcll(v.x) + __popcll(v.y);
+        }
+      } else {
+        for (int64_t wd = w0; wd < min(w0 + 8, nwords); ++wd) c += __popcll(L[wd]);
+      }
+    }
+    const uint32_t incl = warp_incl_scan(c);
+    if (lane == 31) s_w[wid] = incl;
+    __syncthreads();
+    uint32_t wpre = 0, tot = 0;
+#pragma unroll
+    for (int k = 0; k < RK_THREADS / 32; ++k) {
+      const uint32_t t = s_w[k];
+      wpre += k < wid ? t : 0u;
+      tot += t;
+    }
+    if (b < nblk) bp[b] = carry + wpre + incl - c;
+    carry += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) chunk_pre[(int64_t)level * nchunk + blockIdx.x] = carry;
+}
+
+// per level (one CTA each): exclusive scan of the chunk totals in place
+__global__ void __launch_bounds__(TAB_THREADS) rank_chunks_kernel(int64_t* __restrict__ chunk_pre, int64_t nchunk) {
+  __shared__ int64_t s_red[33];
+  int64_t* c = chunk_pre + (int64_t)blockIdx.x * nchunk;
+  block_scan_excl(
+      nchunk, [&](int64_t i) { return c[i]; }, [&](int64_t i, int64_t v) { c[i] = v; }, s_red);
+}
+
+struct RankDir {
+  const uint64_t* words;
+  int64_t nwords, nblk, nchunk, n;
+  const uint32_t* blk_pre;
+  const int64_t* chunk_pre;
+};
+
+// ones of level l before position p (0 <= p <= n)
+__device__ __forceinline__ int64_t level_rank1(const RankDir& d, int l, int64_t p, int64_t ones_total) {
+  if (p >= d.n) return ones_total;
+  const int64_t b = p >> 9;
+  const uint64_t* L = d.words + (int64_t)l * d.nwords;
+  int64_t r = d.chunk_pre[(int64_t)l * d.nchunk + b / RK_CHUNK] + d.blk_pre[(int64_t)l * d.nblk + b];
+  const int64_t wp = p >> 6;
+  for (int64_t wd = b * 8; wd < wp; ++wd) r += __popcll(L[wd]);
+  if (p & 63) r += __popcll(L[wp] & ((1ull << (p & 63)) - 1ull));
+  return r;
+}
+
+// level l -> level l + 1 of the count chain (numeric prefix order) and of the
+// WM group starts (indexed by numeric prefix)
+__global__ void wm_groups_kernel(const RankDir d, int l, const int64_t* __restrict__ zeros, int64_t* __restrict__ chain,
+                                 int64_t* __restrict__ wmst) {
+  const int64_t ng = 1ll << l;
+  const int64_t z = zeros[l], ones = d.n - z;
+  for (int64_t P = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; P < ng; P += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = l ? wmst[chain_off(l) + P] : 0;
+    const int64_t c = l ? chain[chain_off(l) + P] : d.n;
+    const int64_t rs = s - level_rank1(d, l, s, ones);
+    const int64_t re = (s + c) - level_rank1(d, l, s + c, ones);
+    chain[chain_off(l + 1) + 2 * P] = re - rs;
+    chain[chain_off(l + 1) + 2 * P + 1] = c - (re - rs);
+    wmst[chain_off(l + 1) + 2 * P] = rs;
+    wmst[chain_off(l + 1) + 2 * P + 1] = z + s - rs;
+  }
 }
 
 struct WtViaWm {
   size_t off_temp, off_zeros, off_chain, off_bounds, off_wm, off_ws, total;
+  size_t off_blk, off_chunk;  // rank directory (inside the matrix build's workspace, free by then)
+  int64_t nblk, nchunk;
 };
 
 inline bool wt_via_wm_layout(int64_t n, int sym_bytes, int64_t sigma, WtViaWm* L) {
@@ -2142,7 +2247,13 @@ inline bool wt_via_wm_layout(int64_t n, int sym_bytes, int64_t sigma, WtViaWm* L
   L->off_wm = off;
   off = align_up(off + ((size_t)2 << w) * 8, 256);
   L->off_ws = off;
-  L->total = off + P.total;
+  L->nblk = (nwords + 7) / 8;
+  L->nchunk = (L->nblk + RK_CHUNK - 1) / RK_CHUNK;
+  L->off_blk = off;
+  size_t r = align_up(off + (size_t)w * L->nblk * 4, 256);
+  L->off_chunk = r;
+  r = align_up(r + (size_t)w * L->nchunk * 8, 256);
+  L->total = std::max(off + P.total, r);
   return true;
 }
 
@@ -2160,21 +2271,53 @@ int build_wt_via_wm(const void* text, int sym_bytes, int64_t n, int64_t sigma, u
   int rc = build_device_impl(text, sym_bytes, n, sigma, WVLT_KIND_WM, temp, zeros ? zeros : (int64_t*)(ws + L.off_zeros), nullptr,
                              nullptr, ws + L.off_ws, L.total - L.off_ws, status, s, nullptr, nullptr);
   if (rc) return rc;
+  int launches = g_launches;
+  cudaError_t e;
+#ifdef WVLT_WT_VIA_HIST
   // histogram -> fold chain -> per-level starts
   unsigned long long* hw = (unsigned long long*)(chain + chain_off(w));
-  cudaError_t e = cudaMemsetAsync(hw, 0, ((size_t)1 << w) * 8, s);
+  e = cudaMemsetAsync(hw, 0, ((size_t)1 << w) * 8, s);
   if (e != cudaSuccess) return (int)e;
   // (the matrix build checked the range; its zero-count scratch takes the status bits)
   e = launch_hist_generic(text, sym_bytes, n, w, hw, status ? status : (int32_t*)(ws + L.off_zeros), s);
   if (e != cudaSuccess) return (int)e;
-  int launches = g_launches + 1;
+  ++launches;
   for (int k = w - 1; k >= 2; --k) {
     const int64_t q = 1ll << k;
     fold_level_kernel<<<(unsigned)std::min<int64_t>((q + 255) / 256, (int64_t)sm_count() * 8), 256, 0, s>>>(chain, k);
     ++launches;
   }
+  int64_t* wm_scan = wmst;
+#else
+  // the count chain and the WM group starts from the matrix levels: rank
+  // directory of every level, then the group recurrence level by level
+  {
+    const int64_t* dz = zeros ? zeros : (int64_t*)(ws + L.off_zeros);
+    uint32_t* blk = (uint32_t*)(ws + L.off_blk);
+    int64_t* chk = (int64_t*)(ws + L.off_chunk);
+    rank_blocks_kernel<<<dim3((unsigned)L.nchunk, (unsigned)w), RK_THREADS, 0, s>>>(temp, nwords, L.nblk, L.nchunk,
+                                                                                  blk, chk);
+    rank_chunks_kernel<<<w, TAB_THREADS, 0, s>>>(chk, L.nchunk);
+    launches += 2;
+    RankDir d;
+    d.words = temp;
+    d.nwords = nwords;
+    d.nblk = L.nblk;
+    d.nchunk = L.nchunk;
+    d.n = n;
+    d.blk_pre = blk;
+    d.chunk_pre = chk;
+    for (int l = 0; l < w; ++l) {
+      const int64_t ng = 1ll << l;
+      wm_groups_kernel<<<(unsigned)std::min<int64_t>((ng + 255) / 256, (int64_t)sm_count() * 8), 256, 0, s>>>(
+          d, l, dz, chain, wmst);
+      ++launches;
+    }
+  }
+  int64_t* wm_scan = nullptr;  // the recurrence wrote the WM starts
+#endif
   if (w > 2) {
-    level_starts_kernel<<<w - 2, TAB_THREADS, 0, s>>>(chain, bounds, wmst, n);
+    level_starts_kernel<<<w - 2, TAB_THREADS, 0, s>>>(chain, bounds, wm_scan, n);
     ++launches;
   }
   e = cudaGetLastError();
@@ -2193,7 +2336,7 @@ int build_wt_via_wm(const void* text, int sym_bytes, int64_t n, int64_t sigma, u
   e = cudaGetLastError();
   if (e != cudaSuccess) return (int)e;
   if (hist) {
-    e = cudaMemcpyAsync(hist, hw, ((size_t)1 << w) * 8, cudaMemcpyDeviceToDevice, s);
+    e = cudaMemcpyAsync(hist, chain + chain_off(w), ((size_t)1 << w) * 8, cudaMemcpyDeviceToDevice, s);
     if (e != cudaSuccess) return (int)e;
   }
   prof_mark(s, WVLT_STAGE_REORDER);
