@@ -1608,20 +1608,22 @@ __device__ __forceinline__ uint64_t merge_word(int64_t wd, int64_t nbits, const 
   return acc;
 }
 
-constexpr int MERGE_WORDS_PER_LANE = 4;
+#ifndef MERGE_WPL
+#define MERGE_WPL 8  // measured: 8 < 4 ms (more source loads in flight)
+#endif
+constexpr int MERGE_WORDS_PER_LANE = MERGE_WPL;
 
-__global__ void __launch_bounds__(256) merge_bits_kernel(uint64_t* __restrict__ dst, int64_t wlo, int64_t whi,
-                                                         int64_t nbits, const int64_t* __restrict__ bounds,
-                                                         const int64_t* __restrict__ src_starts, int64_t ntasks,
-                                                         const uint64_t* __restrict__ src) {
+// destination words [wlo, whi) of one gather_bits plan; warp `gw` of `nwarps`
+__device__ __forceinline__ void merge_range(uint64_t* __restrict__ dst, int64_t wlo, int64_t whi, int64_t nbits,
+                                            const int64_t* __restrict__ bounds,
+                                            const int64_t* __restrict__ src_starts, int64_t ntasks,
+                                            const uint64_t* __restrict__ src, int64_t gw, int64_t nwarps) {
   // a warp owns 32 * MERGE_WORDS_PER_LANE consecutive destination words
   // (coalesced stores; within a task coalesced source loads); lane 0
   // binary-searches the task of the warp's first bit, every lane walks forward
   constexpr int CH = 32 * MERGE_WORDS_PER_LANE;
   const int lane = threadIdx.x & 31;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t w0 = wlo + ((((int64_t)blockIdx.x * blockDim.x) >> 5) + (threadIdx.x >> 5)) * CH; w0 < whi;
-       w0 += nwarps * CH) {
+  for (int64_t w0 = wlo + gw * CH; w0 < whi; w0 += nwarps * CH) {
     int64_t t0 = 0;
     if (lane == 0 && (w0 << 6) < nbits) {
       int64_t lo = 0, hi = ntasks;  // last t with bounds[t] <= bit
@@ -1635,17 +1637,71 @@ __global__ void __launch_bounds__(256) merge_bits_kernel(uint64_t* __restrict__ 
     }
     t0 = __shfl_sync(FULL, t0, 0);
     uint64_t v[MERGE_WORDS_PER_LANE];
+#ifndef MERGE_SERIAL
+    // the task of every word's first bit first (small, cached arrays), then all
+    // source loads at once (independent, in flight together), then the words
+    // that straddle a task boundary on the slow path
+    int64_t sp[MERGE_WORDS_PER_LANE];
+    uint32_t single = 0;
+    int64_t t = t0;
+#pragma unroll
+    for (int k = 0; k < MERGE_WORDS_PER_LANE; ++k) {
+      const int64_t wd = w0 + 32 * k + lane;
+      const int64_t here = wd << 6;
+      sp[k] = -1;
+      if (wd < whi && here < nbits) {
+        while (__ldg(bounds + t + 1) <= here) ++t;
+        const int64_t nb = min((int64_t)64, nbits - here);
+        if (__ldg(bounds + t + 1) >= here + nb) {
+          single |= 1u << k;
+          sp[k] = __ldg(src_starts + t) + (here - __ldg(bounds + t));
+        }
+      }
+    }
+    const unsigned long long* s64 = reinterpret_cast<const unsigned long long*>(src);
+    uint64_t lo[MERGE_WORDS_PER_LANE], hi[MERGE_WORDS_PER_LANE];
+#pragma unroll
+    for (int k = 0; k < MERGE_WORDS_PER_LANE; ++k) {
+      lo[k] = hi[k] = 0;
+      if ((single >> k) & 1u) {
+        lo[k] = __ldg(s64 + (sp[k] >> 6));
+        if (sp[k] & 63) hi[k] = __ldg(s64 + (sp[k] >> 6) + 1);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < MERGE_WORDS_PER_LANE; ++k) {
+      const int64_t wd = w0 + 32 * k + lane;
+      if ((single >> k) & 1u) {
+        const int sh = (int)(sp[k] & 63);
+        uint64_t x = sh ? ((lo[k] >> sh) | (hi[k] << (64 - sh))) : lo[k];
+        const int64_t nb = nbits - (wd << 6);
+        if (nb < 64) x &= (1ull << nb) - 1ull;
+        v[k] = x;
+      } else {
+        v[k] = (wd < whi && (wd << 6) < nbits) ? merge_word(wd, nbits, bounds, src_starts, src, t0) : 0ull;
+      }
+    }
+#else
 #pragma unroll
     for (int k = 0; k < MERGE_WORDS_PER_LANE; ++k) {
       const int64_t wd = w0 + 32 * k + lane;
       v[k] = (wd < whi && (wd << 6) < nbits) ? merge_word(wd, nbits, bounds, src_starts, src, t0) : 0ull;
     }
+#endif
 #pragma unroll
     for (int k = 0; k < MERGE_WORDS_PER_LANE; ++k) {
       const int64_t wd = w0 + 32 * k + lane;
       if (wd < whi) __stcs(reinterpret_cast<unsigned long long*>(dst) + wd, v[k]);
     }
   }
+}
+
+__global__ void __launch_bounds__(256) merge_bits_kernel(uint64_t* __restrict__ dst, int64_t wlo, int64_t whi,
+                                                         int64_t nbits, const int64_t* __restrict__ bounds,
+                                                         const int64_t* __restrict__ src_starts, int64_t ntasks,
+                                                         const uint64_t* __restrict__ src) {
+  merge_range(dst, wlo, whi, nbits, bounds, src_starts, ntasks, src,
+              (((int64_t)blockIdx.x * blockDim.x) >> 5) + (threadIdx.x >> 5), ((int64_t)gridDim.x * blockDim.x) >> 5);
 }
 
 // Multi-GPU merge over peer memory: every level's owned destination words are
@@ -2095,33 +2151,6 @@ int build_device_impl(const void* text, int sym_bytes, int64_t n, int64_t sigma,
 // ---------------------------------------------------------------------------
 namespace {
 
-__global__ void fold_level_kernel(int64_t* __restrict__ chain, int k) {  // level k from level k + 1
-  const int64_t* up = chain + chain_off(k + 1);
-  int64_t* dn = chain + chain_off(k);
-  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < (1ll << k);
-       q += (int64_t)gridDim.x * blockDim.x)
-    dn[q] = up[2 * q] + up[2 * q + 1];
-}
-
-// one CTA per level k >= 2 (blockIdx.x + 2): WT starts in numeric order (with
-// the end n as sentinel) and (if wm_starts) WM starts indexed by numeric prefix
-__global__ void __launch_bounds__(TAB_THREADS) level_starts_kernel(const int64_t* __restrict__ chain,
-                                                                   int64_t* __restrict__ wt_bounds,
-                                                                   int64_t* __restrict__ wm_starts, int64_t n) {
-  __shared__ int64_t s_red[33];
-  const int k = blockIdx.x + 2;
-  const int64_t* c = chain + chain_off(k);
-  int64_t* wt = wt_bounds + chain_off(k) + k;
-  int64_t* wm = wm_starts + chain_off(k);
-  block_scan_excl(
-      1ll << k, [&](int64_t i) { return c[i]; }, [&](int64_t i, int64_t v) { wt[i] = v; }, s_red);
-  if (wm_starts)
-    block_scan_excl(
-        1ll << k, [&](int64_t r) { return c[rev_bits((unsigned)r, k)]; },
-        [&](int64_t r, int64_t v) { wm[rev_bits((unsigned)r, k)] = v; }, s_red);
-  if (threadIdx.x == 0) wt[1ll << k] = n;
-}
-
 // Group sizes of the matrix levels from the matrix itself (the recurrence of
 // recover_histogram, wt2wm.py:137-156, on the WM layout): the group of prefix
 // P at level l starts at s and holds c symbols; its zero child 2P starts at
@@ -2206,21 +2235,28 @@ __device__ __forceinline__ int64_t level_rank1(const RankDir& d, int l, int64_t 
   return r;
 }
 
-// level l -> level l + 1 of the count chain (numeric prefix order) and of the
-// WM group starts (indexed by numeric prefix)
+// level l -> level l + 1 of the count chain (numeric prefix order), of the WM
+// group starts (indexed by numeric prefix) and of the WT interval starts
+// (wt_bounds level k at chain_off(k) + k, 2^k starts + the end n as sentinel):
+// the tree's interval of 2P starts where P's does, 2P+1 after 2P's symbols.
 __global__ void wm_groups_kernel(const RankDir d, int l, const int64_t* __restrict__ zeros, int64_t* __restrict__ chain,
-                                 int64_t* __restrict__ wmst) {
+                                 int64_t* __restrict__ wmst, int64_t* __restrict__ wt_bounds) {
   const int64_t ng = 1ll << l;
   const int64_t z = zeros[l], ones = d.n - z;
+  int64_t* wt1 = wt_bounds + chain_off(l + 1) + (l + 1);
   for (int64_t P = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; P < ng; P += (int64_t)gridDim.x * blockDim.x) {
     const int64_t s = l ? wmst[chain_off(l) + P] : 0;
     const int64_t c = l ? chain[chain_off(l) + P] : d.n;
+    const int64_t wt = l ? wt_bounds[chain_off(l) + l + P] : 0;
     const int64_t rs = s - level_rank1(d, l, s, ones);
     const int64_t re = (s + c) - level_rank1(d, l, s + c, ones);
     chain[chain_off(l + 1) + 2 * P] = re - rs;
     chain[chain_off(l + 1) + 2 * P + 1] = c - (re - rs);
     wmst[chain_off(l + 1) + 2 * P] = rs;
     wmst[chain_off(l + 1) + 2 * P + 1] = z + s - rs;
+    wt1[2 * P] = wt;
+    wt1[2 * P + 1] = wt + (re - rs);
+    if (P == 0) wt1[2 * ng] = d.n;
   }
 }
 
@@ -2273,22 +2309,6 @@ int build_wt_via_wm(const void* text, int sym_bytes, int64_t n, int64_t sigma, u
   if (rc) return rc;
   int launches = g_launches;
   cudaError_t e;
-#ifdef WVLT_WT_VIA_HIST
-  // histogram -> fold chain -> per-level starts
-  unsigned long long* hw = (unsigned long long*)(chain + chain_off(w));
-  e = cudaMemsetAsync(hw, 0, ((size_t)1 << w) * 8, s);
-  if (e != cudaSuccess) return (int)e;
-  // (the matrix build checked the range; its zero-count scratch takes the status bits)
-  e = launch_hist_generic(text, sym_bytes, n, w, hw, status ? status : (int32_t*)(ws + L.off_zeros), s);
-  if (e != cudaSuccess) return (int)e;
-  ++launches;
-  for (int k = w - 1; k >= 2; --k) {
-    const int64_t q = 1ll << k;
-    fold_level_kernel<<<(unsigned)std::min<int64_t>((q + 255) / 256, (int64_t)sm_count() * 8), 256, 0, s>>>(chain, k);
-    ++launches;
-  }
-  int64_t* wm_scan = wmst;
-#else
   // the count chain and the WM group starts from the matrix levels: rank
   // directory of every level, then the group recurrence level by level
   {
@@ -2310,21 +2330,17 @@ int build_wt_via_wm(const void* text, int sym_bytes, int64_t n, int64_t sigma, u
     for (int l = 0; l < w; ++l) {
       const int64_t ng = 1ll << l;
       wm_groups_kernel<<<(unsigned)std::min<int64_t>((ng + 255) / 256, (int64_t)sm_count() * 8), 256, 0, s>>>(
-          d, l, dz, chain, wmst);
+          d, l, dz, chain, wmst, bounds);
       ++launches;
     }
-  }
-  int64_t* wm_scan = nullptr;  // the recurrence wrote the WM starts
-#endif
-  if (w > 2) {
-    level_starts_kernel<<<w - 2, TAB_THREADS, 0, s>>>(chain, bounds, wm_scan, n);
-    ++launches;
   }
   e = cudaGetLastError();
   if (e != cudaSuccess) return (int)e;
   // levels 0 and 1 are identical; the others are reordered group by group
   e = cudaMemcpyAsync(level_words, temp, (size_t)std::min(w, 2) * nwords * 8, cudaMemcpyDeviceToDevice, s);
   if (e != cudaSuccess) return (int)e;
+  // one launch per level (measured: all levels in one 2-D grid is slower --
+  // 2 (w - 2) concurrent streams of HBM traffic instead of 2)
   int64_t blocks = (nwords + 256 * MERGE_WORDS_PER_LANE - 1) / (256 * MERGE_WORDS_PER_LANE);
   blocks = std::min<int64_t>(blocks, (int64_t)sm_count() * 32);
   for (int k = 2; k < w; ++k) {
