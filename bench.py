@@ -397,12 +397,52 @@ def main():
         hwords = [torch.empty((w, nwords), dtype=torch.int64, pin_memory=True).numpy().view(np.uint64)
                   for _ in range(4)]
         builder.build_host(harr, sigma, kind, out_words=hwords[0])  # warm-up (device buffers, workspace)
-        builder.build_host_batch([harr, harr], sigma, kind, out_words=hwords[:2])
+        if not sharded:
+            builder.build_host_batch([harr, harr], sigma, kind, out_words=hwords[:2])
         host_launches = int(builder.lib.wvlt_last_launches())
         torch.cuda.synchronize()
 
-        # latency: one build at a time through wvlt_build_host (H2D, build, D2H, sync)
         lat_steps = max(2, min(args.steps, 5))
+        if sharded:
+            # N > 1: the job is the sharded global build -- every step each rank
+            # uploads its shard, the ranks build and merge (build_sharded), and each
+            # rank downloads the level words it owns; one step at a time (the merge
+            # synchronises the ranks)
+            dev_text = torch.empty_like(text)
+
+            def e2e_step(hout=None):
+                dev_text.copy_(host, non_blocking=True)
+                res = build_sharded(dev_text, sigma, kind, ops=ops, transport=transport)
+                if hout is None:
+                    hout = torch.empty(res.level_words.shape, dtype=torch.int64, pin_memory=True)
+                hout.copy_(res.level_words, non_blocking=True)
+                torch.cuda.current_stream(dev).synchronize()
+                return hout
+
+            try:
+                hout = e2e_step()
+                barrier()
+                t0 = time.perf_counter()
+                for _ in range(e2e_steps):
+                    e2e_step(hout)
+                dt = (time.perf_counter() - t0) / e2e_steps
+            except Exception as ex:  # noqa: BLE001 - keep the device-resident line
+                print(f"e2e (sharded) failed: {ex!r}", file=sys.stderr)
+                dt = float("nan")
+            t = torch.tensor([dt], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+            hout = hout if dt == dt else torch.empty(0)
+            line["e2e"] = {"value": world * n / dt, "unit": UNIT, "ms_per_step": dt * 1e3,
+                           "h2d_bytes_per_step": n * sym_bytes, "d2h_bytes_per_step": int(hout.numel()) * 8,
+                           "steps": e2e_steps,
+                           "path": f"per rank: H2D of its {n}-symbol shard from page-locked memory, build_sharded "
+                                   f"({transport}), D2H of the level words it owns; bytes are per rank"}
+            line["gpu_launches"] += e2e_steps * host_launches
+            args.no_e2e = True  # the single-GPU queue below does not apply
+
+    if not args.no_e2e:
+        # latency: one build at a time through wvlt_build_host (H2D, build, D2H, sync)
         barrier()
         t0 = time.perf_counter()
         for _ in range(lat_steps):
