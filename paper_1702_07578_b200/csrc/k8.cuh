@@ -46,6 +46,16 @@ __global__ void __launch_bounds__(H8_WARPS * 32) hist8_kernel(const uint8_t* __r
   uint32_t* c32 = s_cols + (size_t)wid * WORDS;
   uint32_t* c32w = c32 + (lane & (C - 1));
   for (int i = lane; i < WORDS; i += 32) c32[i] = 0;
+#ifndef H8_LSU_ZERO
+  // a zero row for the bulk (TMA) stores that clear the other levels' words:
+  // they go through the async copy engine instead of the LSU pipe, the
+  // bottleneck of this kernel (one shared atomic per symbol)
+  __shared__ __align__(128) uint64_t s_zero[K8_TILE / 64];
+  for (int i = threadIdx.x; i < K8_TILE / 64; i += H8_WARPS * 32) s_zero[i] = 0;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+  const uint32_t zsrc = (uint32_t)__cvta_generic_to_shared(s_zero);
+#endif
   __syncwarp();
   uint32_t vmax = 0;
   const bool aligned = (((uintptr_t)text) & 15) == 0;
@@ -59,12 +69,23 @@ __global__ void __launch_bounds__(H8_WARPS * 32) hist8_kernel(const uint8_t* __r
       const int64_t w0 = first >> 6;
       const int tw = (int)min((int64_t)(K8_TILE / 64), nwords - w0);
       if (tw == K8_TILE / 64 && !(nwords & 1)) {  // whole tile, 16-byte aligned rows
+#ifndef H8_LSU_ZERO
+        if (lane == 0) {
+#pragma unroll
+          for (int j = 1; j < W; ++j)
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(level0 + j * nwords + w0),
+                         "r"(zsrc), "r"((uint32_t)(K8_TILE / 8))
+                         : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+#else
 #pragma unroll
         for (int j = 1; j < W; ++j) {
           uint4* lw = reinterpret_cast<uint4*>(level0 + j * nwords + w0);
 #pragma unroll
           for (int i = lane; i < K8_TILE / 128; i += 32) __stcs(lw + i, make_uint4(0, 0, 0, 0));
         }
+#endif
       } else {
 #pragma unroll
         for (int j = 1; j < W; ++j) {
@@ -145,6 +166,11 @@ __global__ void __launch_bounds__(H8_WARPS * 32) hist8_kernel(const uint8_t* __r
     vmax = max(max(vmax & 0xFFu, (vmax >> 8) & 0xFFu), max((vmax >> 16) & 0xFFu, vmax >> 24));
     if (vmax > vmax_ok) atomicOr(status, WVLT_STATUS_RANGE);
   }
+#ifndef H8_LSU_ZERO
+  // the zero row must outlive the bulk stores that read it
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  __syncthreads();
+#endif
 }
 
 // ---- S8: exclusive prefix over tiles of every column of tcnt8 ----
