@@ -42,6 +42,8 @@ __global__ void __launch_bounds__(H8_WARPS * 32) hist16_kernel(const uint16_t* _
   uint32_t* c32 = s_cols + (size_t)wid * WORDS;
   uint32_t* c32w = c32 + (lane & (C - 1));
   for (int i = lane; i < WORDS; i += 32) c32[i] = 0;
+  __shared__ __align__(128) uint64_t s_zero[K16_TILE / 64];
+  const uint32_t zsrc = zero_row_init<K16_TILE / 64>(s_zero);
   __syncwarp();
   uint32_t vmax = 0;
   const bool aligned = (((uintptr_t)src) & 15) == 0;
@@ -49,15 +51,9 @@ __global__ void __launch_bounds__(H8_WARPS * 32) hist16_kernel(const uint16_t* _
   for (int64_t t = (int64_t)blockIdx.x * H8_WARPS + wid; t < ntiles; t += nwarps) {
     const int64_t first = t * K16_TILE;
     const int cnt = (int)min((int64_t)K16_TILE, n - first);
-    {
-      const int64_t w0 = first >> 6;
-      const int tw = (int)min((int64_t)(K16_TILE / 64), nwords - w0);
-#pragma unroll
-      for (int j = 1; j < W; ++j) {
-        uint64_t* lw = level0 + j * nwords + w0;
-        for (int i = lane; i < tw; i += 32) __stcs(reinterpret_cast<unsigned long long*>(lw + i), 0ull);
-      }
-    }
+    // clear this tile's words of levels l0+1..l0+W-1 (the pass ORs run-edge words)
+    clear_level_rows<K16_TILE / 64>(level0, nwords, first >> 6, (int)min((int64_t)(K16_TILE / 64), nwords - (first >> 6)), W,
+                                    zsrc, lane);
     if (cnt == K16_TILE && aligned) {
       const uint4* v4 = reinterpret_cast<const uint4*>(src + first);  // 8 symbols per 16 bytes
 #pragma unroll 1
@@ -130,6 +126,7 @@ __global__ void __launch_bounds__(H8_WARPS * 32) hist16_kernel(const uint16_t* _
     vmax = max(vmax & 0xFFFFu, vmax >> 16);
     if (vmax > vmax_ok) atomicOr(status, WVLT_STATUS_RANGE);
   }
+  zero_row_drain(lane);  // the zero row must outlive the bulk stores that read it
 }
 
 // ---- K3: the fused 2-byte pass ----

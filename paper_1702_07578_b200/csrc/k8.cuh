@@ -30,6 +30,43 @@ constexpr int H8_WARPS = 4;
 #define H8_BATCH 4  // 16-byte loads in flight per lane (measured: 4 < 8 < 16)
 #endif
 
+// Clearing the tile's words of the levels a pass ORs into: bulk (TMA) stores
+// of a zero row in shared memory, so the clearing goes through the async copy
+// engine instead of the LSU pipe (the bottleneck of the counting kernels: one
+// shared atomic per symbol).  Rows that are not whole or not 16-byte aligned
+// fall back to LSU stores.  The kernel fills the row (zero_row_init) and waits
+// for the bulk reads before exiting (zero_row_drain).
+template <int TW>
+__device__ __forceinline__ uint32_t zero_row_init(uint64_t* s_zero) {
+  for (int i = threadIdx.x; i < TW; i += blockDim.x) s_zero[i] = 0;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+  return (uint32_t)__cvta_generic_to_shared(s_zero);
+}
+__device__ __forceinline__ void zero_row_drain(int lane) {
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  __syncthreads();
+}
+// levels 1..nlev-1 after `lvl` (row stride nwords), words [w0, w0 + tw)
+template <int TW>
+__device__ __forceinline__ void clear_level_rows(uint64_t* lvl, int64_t nwords, int64_t w0, int tw, int nlev,
+                                                 uint32_t zsrc, int lane) {
+  if (tw == TW && !(nwords & 1) && !(reinterpret_cast<uintptr_t>(lvl + w0) & 15)) {
+    if (lane == 0) {
+      for (int j = 1; j < nlev; ++j)
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(lvl + j * nwords + w0),
+                     "r"(zsrc), "r"((uint32_t)(TW * 8))
+                     : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+  } else {
+    for (int j = 1; j < nlev; ++j) {
+      uint64_t* lw = lvl + j * nwords + w0;
+      for (int i = lane; i < tw; i += 32) __stcs(reinterpret_cast<unsigned long long*>(lw + i), 0ull);
+    }
+  }
+}
+
 // It also writes level 0 (the top code bit of every symbol, already in text
 // order), so that level can leave for the host while the rest is built.
 template <int W>
@@ -46,16 +83,8 @@ __global__ void __launch_bounds__(H8_WARPS * 32) hist8_kernel(const uint8_t* __r
   uint32_t* c32 = s_cols + (size_t)wid * WORDS;
   uint32_t* c32w = c32 + (lane & (C - 1));
   for (int i = lane; i < WORDS; i += 32) c32[i] = 0;
-#ifndef H8_LSU_ZERO
-  // a zero row for the bulk (TMA) stores that clear the other levels' words:
-  // they go through the async copy engine instead of the LSU pipe, the
-  // bottleneck of this kernel (one shared atomic per symbol)
   __shared__ __align__(128) uint64_t s_zero[K8_TILE / 64];
-  for (int i = threadIdx.x; i < K8_TILE / 64; i += H8_WARPS * 32) s_zero[i] = 0;
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  __syncthreads();
-  const uint32_t zsrc = (uint32_t)__cvta_generic_to_shared(s_zero);
-#endif
+  const uint32_t zsrc = zero_row_init<K8_TILE / 64>(s_zero);
   __syncwarp();
   uint32_t vmax = 0;
   const bool aligned = (((uintptr_t)text) & 15) == 0;
@@ -63,37 +92,9 @@ __global__ void __launch_bounds__(H8_WARPS * 32) hist8_kernel(const uint8_t* __r
   for (int64_t t = (int64_t)blockIdx.x * H8_WARPS + wid; t < ntiles; t += nwarps) {
     const int64_t first = t * K8_TILE;
     const int cnt = (int)min((int64_t)K8_TILE, n - first);
-    {
-      // zero this tile's words of levels 1..W-1 (the pass ORs run-edge words);
-      // streamed here instead of a separate memset of the same bytes
-      const int64_t w0 = first >> 6;
-      const int tw = (int)min((int64_t)(K8_TILE / 64), nwords - w0);
-      if (tw == K8_TILE / 64 && !(nwords & 1)) {  // whole tile, 16-byte aligned rows
-#ifndef H8_LSU_ZERO
-        if (lane == 0) {
-#pragma unroll
-          for (int j = 1; j < W; ++j)
-            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(level0 + j * nwords + w0),
-                         "r"(zsrc), "r"((uint32_t)(K8_TILE / 8))
-                         : "memory");
-          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        }
-#else
-#pragma unroll
-        for (int j = 1; j < W; ++j) {
-          uint4* lw = reinterpret_cast<uint4*>(level0 + j * nwords + w0);
-#pragma unroll
-          for (int i = lane; i < K8_TILE / 128; i += 32) __stcs(lw + i, make_uint4(0, 0, 0, 0));
-        }
-#endif
-      } else {
-#pragma unroll
-        for (int j = 1; j < W; ++j) {
-          uint64_t* lw = level0 + j * nwords + w0;
-          for (int i = lane; i < tw; i += 32) __stcs(reinterpret_cast<unsigned long long*>(lw + i), 0ull);
-        }
-      }
-    }
+    // clear this tile's words of levels 1..W-1 (the pass ORs run-edge words)
+    clear_level_rows<K8_TILE / 64>(level0, nwords, first >> 6, (int)min((int64_t)(K8_TILE / 64), nwords - (first >> 6)),
+                                   W, zsrc, lane);
     if (cnt == K8_TILE && aligned) {
       const uint4* v4 = reinterpret_cast<const uint4*>(text + first);
 #pragma unroll 1
@@ -166,11 +167,7 @@ __global__ void __launch_bounds__(H8_WARPS * 32) hist8_kernel(const uint8_t* __r
     vmax = max(max(vmax & 0xFFu, (vmax >> 8) & 0xFFu), max((vmax >> 16) & 0xFFu, vmax >> 24));
     if (vmax > vmax_ok) atomicOr(status, WVLT_STATUS_RANGE);
   }
-#ifndef H8_LSU_ZERO
-  // the zero row must outlive the bulk stores that read it
-  if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-  __syncthreads();
-#endif
+  zero_row_drain(lane);  // the zero row must outlive the bulk stores that read it
 }
 
 // ---- S8: exclusive prefix over tiles of every column of tcnt8 ----
