@@ -26,6 +26,9 @@ constexpr int H8_WARPS = 4;
 #ifndef H8_COLS
 #define H8_COLS 16  // counter columns per warp (measured: 16 < 32 < 8 ms; more warps per SM)
 #endif
+#ifndef H8_PLANE_W
+#define H8_PLANE_W 3  // up to this width the counts come from bit planes in registers (no shared atomics)
+#endif
 #ifndef H8_BATCH
 #define H8_BATCH 4  // 16-byte loads in flight per lane (measured: 4 < 8 < 16)
 #endif
@@ -95,7 +98,14 @@ __global__ void __launch_bounds__(H8_WARPS * 32) hist8_kernel(const uint8_t* __r
     // clear this tile's words of levels 1..W-1 (the pass ORs run-edge words)
     clear_level_rows<K8_TILE / 64>(level0, nwords, first >> 6, (int)min((int64_t)(K8_TILE / 64), nwords - (first >> 6)),
                                    W, zsrc, lane);
-    if (cnt == K8_TILE && aligned) {
+    // narrow alphabets count in registers: per 16 symbols the W bit planes
+    // (bit 8 b + u = bit of byte b of word u), one POPC per value
+    constexpr bool PLANES = W <= H8_PLANE_W;
+    uint32_t acc[PLANES ? NB : 1];
+#pragma unroll
+    for (int v = 0; v < (PLANES ? NB : 1); ++v) acc[v] = 0;
+    const bool fast = cnt == K8_TILE && aligned;
+    if (fast) {
       const uint4* v4 = reinterpret_cast<const uint4*>(text + first);
 #pragma unroll 1
       for (int k0 = 0; k0 < K8_TILE / 16 / 32; k0 += H8_BATCH) {
@@ -112,12 +122,32 @@ __global__ void __launch_bounds__(H8_WARPS * 32) hist8_kernel(const uint8_t* __r
             const uint32_t lo = wd[u] & ((uint32_t)(HALF - 1) * 0x01010101u);
             const uint32_t hb = (wd[u] >> (W - 1)) & 0x01010101u;
             m16 |= ((hb * 0x01020408u) >> 24) << (4 * u);
-            // increment 0x00010001 for a value with its top bit set, else 1, straight
-            // from one PRMT: the low half counts both values of the pair, the high
-            // half the upper one
+            if (!PLANES) {
+              // increment 0x00010001 for a value with its top bit set, else 1, straight
+              // from one PRMT: the low half counts both values of the pair, the high
+              // half the upper one
 #pragma unroll
-            for (int b = 0; b < 4; ++b)
-              atomicAdd(c32w + prmt(lo, 0, 0x4440 + b) * C, prmt(hb, 1u, 0x5054 + (b << 8)));
+              for (int b = 0; b < 4; ++b)
+                atomicAdd(c32w + prmt(lo, 0, 0x4440 + b) * C, prmt(hb, 1u, 0x5054 + (b << 8)));
+            }
+          }
+          if (PLANES) {
+            uint32_t pl[PLANES ? W : 1], nl[PLANES ? W : 1];
+#pragma unroll
+            for (int b = 0; b < (PLANES ? W : 1); ++b) {
+              uint32_t x = 0;
+#pragma unroll
+              for (int u = 0; u < 4; ++u) x |= ((wd[u] >> b) & 0x01010101u) << u;
+              pl[b] = x;
+              nl[b] = x ^ 0x0F0F0F0Fu;
+            }
+#pragma unroll
+            for (int v = 0; v < (PLANES ? NB : 1); ++v) {
+              uint32_t m = (v & 1) ? pl[0] : nl[0];
+#pragma unroll
+              for (int b = 1; b < (PLANES ? W : 1); ++b) m &= ((v >> b) & 1) ? pl[b] : nl[b];
+              acc[v] += __popc(m);
+            }
           }
           // lanes 4i..4i+3 hold 64 consecutive symbols: one level-0 word
           const uint32_t m32 = m16 | (__shfl_down_sync(FULL, m16, 1) << 16);
@@ -148,6 +178,14 @@ __global__ void __launch_bounds__(H8_WARPS * 32) hist8_kernel(const uint8_t* __r
     // (16-byte reads: lane l takes chunk k ^ (l & 7) of its row, so the 8
     // lanes of a wavefront hit 8 different bank quads)
     uint32_t* row_out = tcnt8 + t * NB;
+    if (PLANES && fast) {
+#pragma unroll
+      for (int v = 0; v < (PLANES ? NB : 1); ++v) {
+        const uint32_t tot = __reduce_add_sync(FULL, acc[v]);
+        if (lane == v) row_out[v] = tot;
+      }
+      continue;  // the shared counters were not touched
+    }
     for (int p = lane; p < HALF; p += 32) {
       const uint4* row = reinterpret_cast<const uint4*>(c32 + p * C);
       uint32_t s = 0;
