@@ -74,13 +74,14 @@ def level_plan(hists: np.ndarray, kind: str, width: int, ell: int):
     hists: (R, 2^width) per-rank histograms.  Returns pieces in destination
     order: (rank, local_start, length, global_start), empty pieces dropped.
     """
+    hists = np.asarray(hists, dtype=np.int64)
     R = hists.shape[0]
     if ell == 0:
-        lens = np.array([int(h.sum()) for h in hists], dtype=np.int64)
+        lens = hists.reshape(R, -1).sum(axis=1)
         ranks = np.arange(R, dtype=np.int64)
         local = np.zeros(R, dtype=np.int64)
     else:
-        counts = np.stack([fold_to(h, width, ell) for h in hists])  # (R, 2^ell), numeric prefix
+        counts = hists.reshape(R, 1 << ell, -1).sum(axis=2)  # (R, 2^ell), numeric prefix (fold_to per rank)
         order = bit_reversal_permutation(ell) if (kind == "wm" and ell >= 2) else np.arange(1 << ell)
         ordered = counts[:, order]
         local_starts = np.cumsum(ordered, axis=1) - ordered  # (R, groups) in interval order
@@ -150,6 +151,39 @@ def peer_plan_arrays(plans, owner: int, width: int):
         ranks.append(np.asarray(pd["ranks"], dtype=np.int32))
         boff += b.size
         task_off.append(task_off[-1] + ln.size)
+    cat = lambda xs, dt: np.concatenate(xs).astype(dt) if xs else np.zeros(1, dtype=dt)  # noqa: E731
+    return (cat(bounds, np.int64), np.asarray(bounds_off, dtype=np.int64), cat(starts, np.int64),
+            cat(ranks, np.int32), np.asarray(task_off, dtype=np.int64))
+
+
+def owner_plan_arrays(hists: np.ndarray, kind: str, width: int, n: int, owner: int, world: int):
+    """peer_plan_arrays(exchange_plan(...)[1], owner, width) computed for this owner
+    alone (the p2p merge needs no per-source send ranges): per level the merge plan
+    (level_plan) cut to the pieces that intersect the owner's bit range."""
+    total_words = (n + 63) >> 6
+    w0, w1 = word_ranges(total_words, world)[owner]
+    b0, b1 = 64 * w0, min(64 * w1, n)
+    bounds, starts, ranks = [], [], []
+    bounds_off, task_off = [], [0]
+    boff = 0
+    for ell in range(width):
+        bounds_off.append(boff)
+        if b1 <= b0:
+            task_off.append(task_off[-1])
+            continue
+        pr, pl, pn, pg = level_plan(hists, kind, width, ell)
+        k0 = int(np.searchsorted(pg + pn, b0, side="right"))
+        k1 = int(np.searchsorted(pg, b1, side="left"))
+        if k1 <= k0:
+            task_off.append(task_off[-1])
+            continue
+        g, ln = pg[k0:k1], pn[k0:k1]
+        b = np.concatenate([g, [g[-1] + ln[-1]]])
+        bounds.append(b)
+        starts.append(pl[k0:k1])
+        ranks.append(pr[k0:k1].astype(np.int32))
+        boff += b.size
+        task_off.append(task_off[-1] + (k1 - k0))
     cat = lambda xs, dt: np.concatenate(xs).astype(dt) if xs else np.zeros(1, dtype=dt)  # noqa: E731
     return (cat(bounds, np.int64), np.asarray(bounds_off, dtype=np.int64), cat(starts, np.int64),
             cat(ranks, np.int32), np.asarray(task_off, dtype=np.int64))
@@ -232,9 +266,10 @@ def build_sharded(local_text, sigma: int, kind: str = "wm", group=None, *, ops=N
     ghist = hists.sum(axis=0)
     zeros = zeros_from_hist(ghist, width) if width else []
     total_words = (n + 63) >> 6
-    ranges, plans = exchange_plan(hists, kind, width, n, local_ns, world)
+    ranges = word_ranges(total_words, world)
     w0, w1 = ranges[rank]
-    owned = torch.zeros((width, max(w1 - w0, 0)), dtype=torch.int64, device=dev)
+    # the merge kernels write every owned word (padding bits included)
+    owned = torch.empty((width, max(w1 - w0, 0)), dtype=torch.int64, device=dev)
     if width == 0 or n == 0:
         return ShardedResult(n, sigma, kind, width, w0, w1, owned, zeros, ghist)
     if peer is not None:
@@ -242,7 +277,7 @@ def build_sharded(local_text, sigma: int, kind: str = "wm", group=None, *, ops=N
         # histogram all_gather above is stream-ordered after every rank's local
         # build, so the peers' levels are complete once it has finished here.
         hdl, buf, lnws = peer
-        arrays = peer_plan_arrays(plans, rank, width)
+        arrays = owner_plan_arrays(hists, kind, width, n, rank, world)
         level_src = np.array([[int(hdl.buffer_ptrs[r]) + 8 * ell * lnws[r] for r in range(world)]
                               for ell in range(width)], dtype=np.int64)
         ops.merge_peer(owned, w0, w1, n, arrays, level_src, world)
@@ -254,6 +289,7 @@ def build_sharded(local_text, sigma: int, kind: str = "wm", group=None, *, ops=N
             res.full_words = _gather_levels(owned, ranges, width, total_words, rank, world, group, dev)
         return res
 
+    plans = exchange_plan(hists, kind, width, n, local_ns, world)[1]
     # 3. one all_to_all for every level: the send buffer is grouped by
     #    destination (levels in order inside), so the receive buffer is grouped
     #    by source rank with levels in order inside

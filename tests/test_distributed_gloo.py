@@ -154,3 +154,24 @@ def test_peer_merge_plan_reassembles_the_single_build(kind, sigma, world):
         arrays = peer_plan_arrays(plans, owner, width)
         got = merge_peer_host(arrays, sources, w0, w1, n, width)
         assert np.array_equal(got, np.asarray(want, dtype=np.uint64)[:, w0:w1]), owner
+
+
+@pytest.mark.parametrize("kind", ["wt", "wm"])
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+@pytest.mark.parametrize("width", [1, 3, 8])
+def test_owner_plan_equals_full_exchange_plan(kind, world, width):
+    """owner_plan_arrays (the p2p path computes only its own merge tasks) equals
+    the owner's slice of the full exchange plan, skewed and empty groups included."""
+    from paper_1702_07578_b200.distributed import exchange_plan, owner_plan_arrays, peer_plan_arrays
+
+    rng = np.random.default_rng(world * 100 + width)
+    hists = (rng.zipf(1.3, (world, 1 << width)) % 5000).astype(np.int64)
+    hists[:, rng.integers(0, 1 << width, max(1, (1 << width) // 4))] = 0
+    local_ns = [int(h.sum()) for h in hists]
+    n = sum(local_ns)
+    _, plans = exchange_plan(hists, kind, width, n, local_ns, world)
+    for owner in range(world):
+        want = peer_plan_arrays(plans, owner, width)
+        got = owner_plan_arrays(hists, kind, width, n, owner, world)
+        for a, b in zip(want, got):
+            assert np.array_equal(a, b)
