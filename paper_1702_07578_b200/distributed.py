@@ -255,14 +255,18 @@ def build_sharded(local_text, sigma: int, kind: str = "wm", group=None, *, ops=N
         words, hist, bad = ops.local_build(local_text, sigma, kind, out_words=buf[: width * lnws[rank]])
     else:
         words, hist, bad = ops.local_build(local_text, sigma, kind)
-    flag = torch.tensor([1 if bad else 0], dtype=torch.int64, device=dev)
-    dist.all_reduce(flag, group=group)
-    if int(flag.item()):
+    # 2. histograms (+ each rank's range flag) -> plan: one all_gather, one host read
+    if torch.is_tensor(bad):
+        flag = (bad.reshape(-1)[:1].to(device=dev, dtype=torch.int64) & 1)
+    else:
+        flag = torch.tensor([1 if bad else 0], dtype=torch.int64, device=dev)
+    mine_h = torch.cat([hist.reshape(-1).to(device=dev, dtype=torch.int64), flag])
+    allh = torch.empty((world, (1 << width) + 1), dtype=torch.int64, device=dev)
+    dist.all_gather_into_tensor(allh, mine_h.reshape(1, -1), group=group)
+    gathered = allh.cpu().numpy()
+    if gathered[:, -1].any():
         raise ValueError(f"symbols must lie in [0, {sigma})")
-    # 2. histograms -> plan
-    allh = torch.empty((world, 1 << width), dtype=torch.int64, device=dev)
-    dist.all_gather_into_tensor(allh, hist.reshape(1, -1).contiguous(), group=group)
-    hists = allh.cpu().numpy()
+    hists = np.ascontiguousarray(gathered[:, :-1])
     ghist = hists.sum(axis=0)
     zeros = zeros_from_hist(ghist, width) if width else []
     total_words = (n + 63) >> 6
@@ -393,7 +397,8 @@ class CudaOps:
             lw, zeros, hist, bd, status = self.builder.alloc_outputs(int(text.numel()), sigma)
             outputs = (out_words.view(lw.shape), zeros, hist, bd, status)
         res = self.builder.build(text, sigma, kind, histogram=True, check=False, outputs=outputs)
-        bad = bool(int(res.status.item()) & 1) if res.status is not None else False
+        # the range status stays on the device (read with the histograms, no extra sync)
+        bad = res.status if res.status is not None else False
         return res.level_words, res.hist, bad
 
     def merge(self, dst_row, word_lo: int, word_hi: int, n_bits: int, bounds, src_starts, src):

@@ -83,5 +83,12 @@ def test_p2p_transport_one_rank_group():
             want = DeviceBuilder().build(text, sigma, kind)
             assert torch.equal(res.full_words, want.level_words)
             assert res.zeros == [int(z) for z in want.zeros.cpu().tolist()] or kind == "wt"
+        # an out-of-range symbol raises the reference's ValueError on every rank
+        # (the range flag travels with the histogram all_gather)
+        for transport in ("p2p", "nccl"):
+            bad = torch.full((100_000,), 3, dtype=torch.uint8, device="cuda")
+            bad[77_777] = 200
+            with pytest.raises(ValueError):
+                build_sharded(bad, 100, "wm", transport=transport)
     finally:
         dist.destroy_process_group()
