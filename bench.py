@@ -231,7 +231,10 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-wt", action="store_true")
-    ap.add_argument("--graph", action="store_true", help="N = 1: time CUDA-graph replays of the captured build")
+    ap.add_argument("--graph", dest="graph", action="store_true", default=True,
+                    help="N = 1 (default): time CUDA-graph replays of the captured build (DeviceBuilder.capture: "
+                         "the build's launches recorded once, replayed with one launch)")
+    ap.add_argument("--no-graph", dest="graph", action="store_false", help="N = 1: launch the build's kernels one by one")
     ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
                     help="N > 1: merge over peer memory (symmetric memory, one kernel) or NCCL all_to_all + merge")
     args = ap.parse_args()
@@ -366,7 +369,7 @@ def main():
                    "l2": ("inputs larger than L2 (text %d MiB per GPU vs 126 MB L2); no flush" % (n * sym_bytes >> 20)
                           if n * sym_bytes > (126 << 20) else
                           "L2-resident input (text %d KiB); no flush: a launch-bound correctness config" % (n * sym_bytes >> 10)),
-                   "graph": bool(args.graph),
+                   "graph": bool(args.graph and not sharded),
                    "parallelism": (f"sharded{world} (position shards; NCCL all_gather of histograms, "
                                    + ("merge over peer memory)" if transport == "p2p" else "NCCL all_to_all + merge)")
                                    if world > 1 else "single")},
