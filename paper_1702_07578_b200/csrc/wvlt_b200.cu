@@ -39,7 +39,9 @@
 
 #include <cuda_runtime.h>
 #include <mutex>
+#include <thread>
 #include <unordered_map>
+#include <vector>
 
 #include <algorithm>
 #include <stdint.h>
@@ -2670,6 +2672,119 @@ int build_device_impl(const void* text, int sym_bytes, int64_t n, int64_t sigma,
   return 0;
 }
 
+// Pageable host buffers (a numpy array as the reference's callers pass it):
+// copies are staged through two page-locked chunks, the host side of each
+// chunk spread over several CPU threads (one thread copies ~15 GB/s, or far
+// less when it also takes the page faults of fresh output memory; PCIe moves
+// ~55 GB/s) and overlapped with the DMA of the neighbouring chunk.
+constexpr size_t STAGE_CHUNK = (size_t)32 << 20;
+#ifndef STAGE_MAX_THREADS
+#define STAGE_MAX_THREADS 8u
+#endif
+
+struct Stager {
+  unsigned char* buf[2] = {nullptr, nullptr};
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  cudaError_t init() {
+    if (buf[0]) return cudaSuccess;
+    cudaError_t e = cudaHostAlloc((void**)&buf[0], 2 * STAGE_CHUNK, cudaHostAllocDefault);
+    if (e != cudaSuccess) {
+      buf[0] = nullptr;
+      return e;
+    }
+    buf[1] = buf[0] + STAGE_CHUNK;
+    for (int k = 0; k < 2 && e == cudaSuccess; ++k) e = cudaEventCreateWithFlags(&ev[k], cudaEventDisableTiming);
+    return e;
+  }
+};
+thread_local Stager g_stager;
+
+inline int stage_threads() {
+  const unsigned hw = std::thread::hardware_concurrency();
+  return (int)std::max(1u, std::min(STAGE_MAX_THREADS, hw));
+}
+
+void par_memcpy(void* dst, const void* src, size_t n, int nt) {
+  if (nt <= 1 || n < ((size_t)4 << 20)) {
+    memcpy(dst, src, n);
+    return;
+  }
+  const size_t per = ((n + nt - 1) / nt + 4095) & ~(size_t)4095;
+  std::vector<std::thread> th;
+  for (int t = 1; t < nt && (size_t)t * per < n; ++t)
+    th.emplace_back([=] { memcpy((char*)dst + t * per, (const char*)src + t * per, std::min(per, n - t * per)); });
+  memcpy(dst, src, std::min(per, n));
+  for (auto& x : th) x.join();
+}
+
+// Touch every page of a fresh (pageable) output buffer from nt threads, so its
+// page faults are taken in parallel while the upload and the build run rather
+// than serially inside the final copy.
+void prefault_pages(void* p, size_t n, int nt) {
+  const size_t page = 4096;
+  const size_t per = ((n + nt - 1) / nt + page - 1) & ~(page - 1);
+  std::vector<std::thread> th;
+  for (int t = 0; t < nt && (size_t)t * per < n; ++t)
+    th.emplace_back([=] {
+      volatile char* c = (volatile char*)p;
+      const size_t e = std::min(n, (size_t)(t + 1) * per);
+      for (size_t i = (size_t)t * per; i < e; i += page) c[i] = 0;  // an output buffer: contents are overwritten
+    });
+  for (auto& x : th) x.join();
+}
+
+bool host_is_pinned(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+// pageable host -> device, stream ordered on s (returns once the last chunk is queued)
+cudaError_t staged_h2d(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  Stager& g = g_stager;
+  cudaError_t e = g.init();
+  if (e != cudaSuccess) return e;
+  const int nt = stage_threads();
+  size_t off = 0;
+  for (int c = 0; off < bytes; ++c, off += STAGE_CHUNK) {
+    const int k = c & 1;
+    const size_t sz = std::min(STAGE_CHUNK, bytes - off);
+    if (c >= 2 && (e = cudaEventSynchronize(g.ev[k])) != cudaSuccess) return e;  // chunk c - 2 has left buf[k]
+    par_memcpy(g.buf[k], (const char*)src + off, sz, nt);
+    if ((e = cudaMemcpyAsync((char*)dst + off, g.buf[k], sz, cudaMemcpyHostToDevice, s)) != cudaSuccess) return e;
+    if ((e = cudaEventRecord(g.ev[k], s)) != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+// device -> pageable host after the work queued on s; returns when the data is there
+cudaError_t staged_d2h(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  Stager& g = g_stager;
+  cudaError_t e = g.init();
+  if (e != cudaSuccess) return e;
+  const int nt = stage_threads();
+  const size_t nch = (bytes + STAGE_CHUNK - 1) / STAGE_CHUNK;
+  auto issue = [&](size_t c) -> cudaError_t {
+    const int k = (int)(c & 1);
+    const size_t off = c * STAGE_CHUNK, sz = std::min(STAGE_CHUNK, bytes - off);
+    cudaError_t r = cudaMemcpyAsync(g.buf[k], (const char*)src + off, sz, cudaMemcpyDeviceToHost, s);
+    return r == cudaSuccess ? cudaEventRecord(g.ev[k], s) : r;
+  };
+  for (size_t c = 0; c < std::min<size_t>(2, nch); ++c)
+    if ((e = issue(c)) != cudaSuccess) return e;
+  for (size_t c = 0; c < nch; ++c) {
+    const int k = (int)(c & 1);
+    const size_t off = c * STAGE_CHUNK, sz = std::min(STAGE_CHUNK, bytes - off);
+    if ((e = cudaEventSynchronize(g.ev[k])) != cudaSuccess) return e;
+    par_memcpy((char*)dst + off, g.buf[k], sz, nt);
+    if (c + 2 < nch && (e = issue(c + 2)) != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
 // wvlt_build_host: the level words of a finished pass go device->host on a copy
 // stream while the next pass runs.
 struct HostCopy {
@@ -2710,13 +2825,27 @@ int wvlt_build_host(const void* host_text, int sym_bytes, int64_t n, int64_t sig
   int32_t* dstatus = (int32_t*)small;
   int64_t* dzeros = small + 1;
   int64_t* dhist = small + 1 + w;
-  if (n > 0) {
-    if (!host_text || !dev_text) return WVLT_E_ARG;
-    e = cudaMemcpyAsync(dev_text, host_text, (size_t)n * sym_bytes, cudaMemcpyHostToDevice, s);
-    if (e != cudaSuccess) return (int)e;
-  }
   const int64_t nwords = (n + 63) >> 6;
   if (w > 0 && nwords > 0 && !host_level_words) return WVLT_E_ARG;
+  // pageable level words: no per-pass streaming, one staged download at the end;
+  // their pages are faulted in by helper threads while the text goes up
+  const bool words_pinned = !(w > 0 && nwords > 0) || host_is_pinned(host_level_words);
+  std::thread prefault;
+  if (!words_pinned)
+    prefault = std::thread(prefault_pages, (void*)host_level_words, (size_t)w * nwords * 8, stage_threads());
+  struct Joiner {
+    std::thread& t;
+    ~Joiner() {
+      if (t.joinable()) t.join();
+    }
+  } joiner{prefault};
+  if (n > 0) {
+    if (!host_text || !dev_text) return WVLT_E_ARG;
+    e = host_is_pinned(host_text)
+            ? cudaMemcpyAsync(dev_text, host_text, (size_t)n * sym_bytes, cudaMemcpyHostToDevice, s)
+            : staged_h2d(dev_text, host_text, (size_t)n * sym_bytes, s);
+    if (e != cudaSuccess) return (int)e;
+  }
   // level words of each finished pass stream back while the next pass runs
   static thread_local cudaStream_t copy_stream = nullptr;
   static thread_local cudaEvent_t evs[MAXP];
@@ -2738,13 +2867,18 @@ int wvlt_build_host(const void* host_text, int sym_bytes, int64_t n, int64_t sig
   hc.nwords = (w > 0) ? nwords : 0;
   hc.err = cudaSuccess;
   int rc = build_device_impl(dev_text, sym_bytes, n, sigma, kind, dev_level_words, dzeros, host_hist ? dhist : nullptr,
-                             nullptr, workspace, workspace_bytes, dstatus, s, host_copy_pass, &hc);
+                             nullptr, workspace, workspace_bytes, dstatus, s, words_pinned ? host_copy_pass : nullptr,
+                             &hc);
   if (rc) {
     cudaStreamSynchronize(copy_stream);
     return rc;
   }
   if (hc.err != cudaSuccess) return (int)hc.err;
-  if (w > 0 && nwords > 0 && hc.nev == 0) {  // degenerate shapes: no passes ran
+  if (w > 0 && nwords > 0 && !words_pinned) {
+    if (prefault.joinable()) prefault.join();
+    e = staged_d2h(host_level_words, dev_level_words, (size_t)w * nwords * 8, s);
+    if (e != cudaSuccess) return (int)e;
+  } else if (w > 0 && nwords > 0 && hc.nev == 0) {  // degenerate shapes: no passes ran
     e = cudaMemcpyAsync(host_level_words, dev_level_words, (size_t)w * nwords * 8, cudaMemcpyDeviceToHost, s);
     if (e != cudaSuccess) return (int)e;
   }

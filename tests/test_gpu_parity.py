@@ -330,3 +330,25 @@ def test_pipelined_host_batch_matches_single_builds(sigma, kind, hist):
     if sigma < np.iinfo(dt).max + 1:
         with pytest.raises(ValueError):
             b.build_host_batch(bad, sigma, kind)
+
+
+@pytest.mark.parametrize("sigma,kind", [(256, "wm"), (1000, "wt")])
+def test_pageable_host_buffers_are_staged(sigma, kind):
+    """wvlt_build_host with pageable (plain numpy) text and output words -- the
+    reference API's case -- goes through the staged multi-chunk copies
+    (several 32 MiB chunks, odd tail) and equals the device-resident build."""
+    from paper_1702_07578_b200.device import DeviceBuilder, sym_dtype_for_sigma
+
+    rng = np.random.default_rng(sigma)
+    n = 70_000_003
+    text = rng.integers(0, sigma, n).astype(sym_dtype_for_sigma(sigma))
+    b = DeviceBuilder()
+    words, zeros, _ = b.build_host(text, sigma, kind)
+    want = b.build(torch.from_numpy(text).cuda(), sigma, kind)
+    assert np.array_equal(words, want.level_words.cpu().numpy().view(np.uint64))
+    if kind == "wm":
+        assert zeros == [int(z) for z in want.zeros.cpu().tolist()]
+    st = wv.build_structure(text[:5_000_001], sigma, kind)
+    ref_words, _, _ = oracle.build(text[:5_000_001], sigma, kind, "pc")
+    for ell, lv in enumerate(st.levels):
+        assert np.array_equal(lv.words, ref_words[ell])
