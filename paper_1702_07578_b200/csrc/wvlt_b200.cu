@@ -2956,8 +2956,11 @@ int wvlt_build_host_batch(int count, const void* const* host_texts, const int64_
     if ((e = cudaHostAlloc((void**)&stage, need_stage * 8, cudaHostAllocDefault)) != cudaSuccess) return (int)e;
     stage_len = need_stage;
   }
-  int rc = 0;
-  for (int i = 0; i < count && !rc; ++i) {
+  // enqueue build i on the three streams; an error stops the queue, and every
+  // stream is drained below before returning (no copy into caller memory may
+  // still be in flight)
+  auto enqueue = [&](int i) -> int {
+    cudaError_t e;
     const int slot = i & 1;
     const int64_t n = ns[i];
     const int64_t nwords = (n + 63) >> 6;
@@ -2985,9 +2988,9 @@ int wvlt_build_host_batch(int count, const void* const* host_texts, const int64_
     int64_t* dzeros = small + 1;
     int64_t* dhist = small + 1 + w;
     int64_t* hh = host_hist ? host_hist + ((size_t)i << w) : nullptr;
-    rc = build_device_impl(dtext, sym_bytes, n, sigma, kind, dwords, dzeros, hh ? dhist : nullptr, nullptr, workspace,
-                           workspace_bytes, dstatus, s, host_copy_pass, &hc);
-    if (rc) break;
+    const int brc = build_device_impl(dtext, sym_bytes, n, sigma, kind, dwords, dzeros, hh ? dhist : nullptr, nullptr,
+                                      workspace, workspace_bytes, dstatus, s, host_copy_pass, &hc);
+    if (brc) return brc;
     if (hc.err != cudaSuccess) return (int)hc.err;
     if ((e = cudaEventRecord(ev_comp[slot], s)) != cudaSuccess) return (int)e;
     // download: whatever the passes did not already send, then the small outputs
@@ -3001,7 +3004,10 @@ int wvlt_build_host_batch(int count, const void* const* host_texts, const int64_
                              cudaMemcpyDeviceToHost, down)) != cudaSuccess)
       return (int)e;
     if ((e = cudaEventRecord(ev_down[slot], down)) != cudaSuccess) return (int)e;
-  }
+    return 0;
+  };
+  int rc = 0;
+  for (int i = 0; i < count && !rc; ++i) rc = enqueue(i);
   cudaError_t e1 = cudaStreamSynchronize(up), e2 = cudaStreamSynchronize(s), e3 = cudaStreamSynchronize(down);
   if (rc) return rc;
   if (e1 != cudaSuccess) return (int)e1;
