@@ -102,7 +102,9 @@ int wvlt_build_device(const void* text, int sym_bytes, int64_t n, int64_t sigma,
  * builds, copies level words / zeros / histogram device->host and synchronizes
  * `stream`.  Device buffers are caller-provided (dev_text: n*sym_bytes bytes,
  * dev_level_words: width*ceil(n/64)*8 bytes, dev_small: (2^width + width + 1)*8 bytes).
- * Host buffers should be page-locked for full copy bandwidth.  host_zeros and
+ * Page-locked host buffers get direct DMA; pageable ones are staged through
+ * page-locked chunks by several host threads (the output pages are faulted in
+ * while the text goes up).  host_zeros and
  * host_hist may be NULL (host_hist == NULL selects the histogram-free WM build).  Returns WVLT_E_RANGE when a symbol is out of range.
  * This is the call a reference-side binding (ctypes / cgo / JNI) would make
  * in place of construct.build_structure (construct.py:150-164).
@@ -125,7 +127,8 @@ int wvlt_build_host(const void* host_text, int sym_bytes, int64_t n, int64_t sig
  * host_zeros + i*width (may be NULL), host_hist + i*2^width (may be NULL: the
  * histogram-free WM build), host_status[i] (nonzero flags: build i saw a symbol
  * out of range).  Synchronizes before returning; returns WVLT_E_RANGE if any
- * build saw an out-of-range symbol.
+ * build saw an out-of-range symbol.  The overlap needs page-locked texts and
+ * level-word buffers; pageable ones are accepted (the copies then serialise).
  */
 int wvlt_build_host_batch(int count, const void* const* host_texts, const int64_t* ns, int sym_bytes,
                           int64_t sigma, int kind, uint64_t* const* host_level_words, int64_t* host_zeros,
