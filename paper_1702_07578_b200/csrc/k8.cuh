@@ -282,52 +282,80 @@ __global__ void __launch_bounds__(256) scan8_apply_kernel(const uint32_t* __rest
 // starts in level j (WM: exclusive prefix of the group sizes in LSD-digit
 // order; WT: interval start of the numeric prefix rev(d)).  Also the zero
 // counts per level and (optionally) the histogram.
+// exclusive scan of get(i), i < cnt <= 256, by one warp (8 entries per lane), written through put
+template <typename Get, typename Put>
+__device__ __forceinline__ void warp_scan_excl64(int cnt, int lane, Get get, Put put) {
+  int64_t v[8], sum = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int i = lane * 8 + k;
+    v[k] = i < cnt ? get(i) : 0;
+    sum += v[k];
+  }
+  int64_t incl = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t t = __shfl_up_sync(FULL, incl, o);
+    if (lane >= o) incl += t;
+  }
+  int64_t run = incl - sum;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int i = lane * 8 + k;
+    if (i < cnt) put(i, run);
+    run += v[k];
+  }
+}
+
+// One CTA (the fused passes keep n < 2^32, so every count fits 32 bits):
+// group sizes of every level folded from the digit totals level by level
+// (thread = group), zero counts by warp reductions, then one warp per level
+// scans the sizes into group starts (warp 7: the WM level-W starts).
 __global__ void __launch_bounds__(256) tables8_kernel(const int64_t* __restrict__ totals, int W, int kind,
                                                       int64_t* __restrict__ base, int64_t* __restrict__ zeros,
                                                       int64_t* __restrict__ hist, int64_t* __restrict__ baseW) {
-  __shared__ int64_t s_tot[256];
-  __shared__ int64_t s_cnt[8][256];
+  __shared__ uint32_t s_tot[256];
+  __shared__ uint32_t s_cnt[9][256];  // level j: WM by LSD digit, WT by numeric prefix
+  __shared__ uint32_t s_z[8][8];      // [warp][level] partial zero counts
   const int nb = 1 << W;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  uint32_t tot = 0;
   if (tid < nb) {
-    s_tot[tid] = totals[tid];
-    if (hist) hist[tid] = totals[tid];
+    const int64_t t64 = totals[tid];
+    tot = (uint32_t)t64;
+    s_tot[tid] = tot;
+    if (hist) hist[tid] = t64;
+    s_cnt[W][kind == WVLT_KIND_WM ? (int)rev_bits((unsigned)tid, W) : tid] = tot;
   }
-  for (int i = tid; i < 8 * 256; i += 256) s_cnt[i >> 8][i & 255] = 0;
+  for (int l = 0; l < W; ++l) {  // symbols whose level-l bit is 0
+    const uint32_t z = __reduce_add_sync(FULL, ((tid >> (W - 1 - l)) & 1) ? 0u : tot);
+    if (lane == 0) s_z[wid][l] = z;
+  }
   __syncthreads();
-  if (tid < W && zeros) {  // thread l: symbols whose level-l bit is 0
+  for (int j = W - 1; j >= 1; --j) {
+    const int mj = 1 << j;
+    if (tid < mj)  // WM: LSD digits d, d + 2^j of level j+1; WT: prefixes 2P, 2P+1
+      s_cnt[j][tid] = kind == WVLT_KIND_WM ? s_cnt[j + 1][tid] + s_cnt[j + 1][tid + mj]
+                                           : s_cnt[j + 1][2 * tid] + s_cnt[j + 1][2 * tid + 1];
+    __syncthreads();
+  }
+  if (zeros && tid < W) {
     int64_t z = 0;
-    for (int e = 0; e < nb; ++e)
-      if (!((e >> (W - 1 - tid)) & 1)) z += s_tot[e];
+    for (int w = 0; w < 8; ++w) z += w * 32 < nb ? s_z[w][tid] : 0u;
     zeros[tid] = z;
   }
-  if (baseW && tid == 255) {  // WM level-W group starts (the 2-byte pass's output order)
-    int64_t run = 0;
-    for (int d = 0; d < nb; ++d) {
-      baseW[d] = run;
-      run += s_tot[rev_bits((unsigned)d, W)];
-    }
-  }
-  if (tid >= 32 && tid < 32 + W - 1) {  // thread of level j: its group sizes, then their prefix
-    const int j = tid - 31;
-    const int mj = 1 << j;
-    int64_t* c = s_cnt[j];
-    for (int e = 0; e < nb; ++e) {
-      if (kind == WVLT_KIND_WM) c[rev_bits((unsigned)e, W) & (mj - 1)] += s_tot[e];
-      else c[e >> (W - j)] += s_tot[e];  // numeric j-bit prefix
-    }
-    int64_t run = 0;
-    if (kind == WVLT_KIND_WM) {
-      for (int d = 0; d < mj; ++d) {
-        base[j * 256 + d] = run;
-        run += c[d];
-      }
-    } else {
-      for (int P = 0; P < mj; ++P) {
-        base[j * 256 + rev_bits((unsigned)P, j)] = run;
-        run += c[P];
-      }
-    }
+  const int j = wid + 1;  // warp j - 1: level j
+  if (j < W) {
+    const uint32_t* c = s_cnt[j];
+    if (kind == WVLT_KIND_WM)
+      warp_scan_excl64(1 << j, lane, [&](int d) { return (int64_t)c[d]; },
+                       [&](int d, int64_t v) { base[j * 256 + d] = v; });
+    else
+      warp_scan_excl64(1 << j, lane, [&](int P) { return (int64_t)c[P]; },
+                       [&](int P, int64_t v) { base[j * 256 + rev_bits((unsigned)P, j)] = v; });
+  } else if (wid == 7 && baseW) {  // WM level-W group starts (the 2-byte pass's output order)
+    warp_scan_excl64(nb, lane, [&](int d) { return (int64_t)s_tot[rev_bits((unsigned)d, W)]; },
+                     [&](int d, int64_t v) { baseW[d] = v; });
   }
 }
 
