@@ -29,8 +29,11 @@ constexpr int H8_WARPS = 4;
 #ifndef H8_PLANE_W
 #define H8_PLANE_W 3  // up to this width the counts come from bit planes in registers (no shared atomics)
 #endif
+#ifndef H8_ATOMIC_BATCH
+#define H8_ATOMIC_BATCH 2  // hist8: 16-byte loads per pipelined batch when counting by shared atomics
+#endif
 #ifndef H8_BATCH
-#define H8_BATCH 4  // 16-byte loads in flight per lane (measured: 4 < 8 < 16)
+#define H8_BATCH 4  // hist16 / hist32: 16-byte loads in flight per lane (measured: 4 < 8 < 16)
 #endif
 
 // Clearing the tile's words of the levels a pass ORs into: bulk (TMA) stores
@@ -107,13 +110,24 @@ __global__ void __launch_bounds__(H8_WARPS * 32) hist8_kernel(const uint8_t* __r
     const bool fast = cnt == K8_TILE && aligned;
     if (fast) {
       const uint4* v4 = reinterpret_cast<const uint4*>(text + first);
+      // software-pipelined: the next batch's loads are in flight while this one
+      // is counted (measured: batches of 4 for the register-plane widths, 2 for
+      // the shared-atomic ones)
+      constexpr int NBAT = PLANES ? 4 : H8_ATOMIC_BATCH;
+      uint4 qn[NBAT];
+#pragma unroll
+      for (int k = 0; k < NBAT; ++k) qn[k] = __ldcs(v4 + k * 32 + lane);
 #pragma unroll 1
-      for (int k0 = 0; k0 < K8_TILE / 16 / 32; k0 += H8_BATCH) {
-        uint4 q[H8_BATCH];
+      for (int k0 = 0; k0 < K8_TILE / 16 / 32; k0 += NBAT) {
+        uint4 q[NBAT];
 #pragma unroll
-        for (int k = 0; k < H8_BATCH; ++k) q[k] = __ldcs(v4 + (k0 + k) * 32 + lane);
+        for (int k = 0; k < NBAT; ++k) q[k] = qn[k];
+        if (k0 + NBAT < K8_TILE / 16 / 32) {
 #pragma unroll
-        for (int k = 0; k < H8_BATCH; ++k) {
+          for (int k = 0; k < NBAT; ++k) qn[k] = __ldcs(v4 + (k0 + NBAT + k) * 32 + lane);
+        }
+#pragma unroll
+        for (int k = 0; k < NBAT; ++k) {
           const uint32_t wd[4] = {q[k].x, q[k].y, q[k].z, q[k].w};
           uint32_t m16 = 0;  // level-0 bits of this lane's 16 symbols
 #pragma unroll
