@@ -26,6 +26,9 @@ constexpr int K16_NT = K16_TILE / (8 * K16_Q);
 // One warp per tile, the byte kernel's counter pairs; the level-l0 bits are
 // the top digit bit of every symbol; the tile's words of levels l0+1..l0+W-1
 // are zeroed here (the pass ORs their run-edge words).
+#ifndef H16_PIPE_BATCH
+#define H16_PIPE_BATCH 2  // 16-byte loads per pipelined batch of the counting kernel (measured: 2 <= 4)
+#endif
 template <int W>
 __global__ void __launch_bounds__(H8_WARPS * 32) hist16_kernel(const uint16_t* __restrict__ src, int64_t n,
                                                               int64_t ntiles, uint32_t vmax_ok, int check,
@@ -56,13 +59,22 @@ __global__ void __launch_bounds__(H8_WARPS * 32) hist16_kernel(const uint16_t* _
                                     zsrc, lane);
     if (cnt == K16_TILE && aligned) {
       const uint4* v4 = reinterpret_cast<const uint4*>(src + first);  // 8 symbols per 16 bytes
+      // software-pipelined: the next batch's loads are in flight while this one is counted
+      constexpr int NBAT = H16_PIPE_BATCH;
+      uint4 qn[NBAT];
+#pragma unroll
+      for (int k = 0; k < NBAT; ++k) qn[k] = __ldcs(v4 + k * 32 + lane);
 #pragma unroll 1
-      for (int k0 = 0; k0 < K16_TILE / 8 / 32; k0 += H8_BATCH) {
-        uint4 q[H8_BATCH];
+      for (int k0 = 0; k0 < K16_TILE / 8 / 32; k0 += NBAT) {
+        uint4 q[NBAT];
 #pragma unroll
-        for (int k = 0; k < H8_BATCH; ++k) q[k] = __ldcs(v4 + (k0 + k) * 32 + lane);
+        for (int k = 0; k < NBAT; ++k) q[k] = qn[k];
+        if (k0 + NBAT < K16_TILE / 8 / 32) {
 #pragma unroll
-        for (int k = 0; k < H8_BATCH; ++k) {
+          for (int k = 0; k < NBAT; ++k) qn[k] = __ldcs(v4 + (k0 + NBAT + k) * 32 + lane);
+        }
+#pragma unroll
+        for (int k = 0; k < NBAT; ++k) {
           if (check) {
             vmax = __vmaxu2(vmax, q[k].x);
             vmax = __vmaxu2(vmax, q[k].y);

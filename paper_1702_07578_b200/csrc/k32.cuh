@@ -21,6 +21,9 @@ constexpr int K32_NT = K32_TILE / (8 * K32_Q);
 #endif
 
 // ---- K1: per-tile counts of the W-bit digit (byte 2), range check, level l0 ----
+#ifndef H32_PIPE_BATCH
+#define H32_PIPE_BATCH 2  // 16-byte loads per pipelined batch of the counting kernel (measured: 2 < 4)
+#endif
 template <int W>
 __global__ void __launch_bounds__(H8_WARPS * 32) hist32_kernel(const uint32_t* __restrict__ src, int64_t n,
                                                               int64_t ntiles, uint32_t vmax_ok, int check,
@@ -51,13 +54,22 @@ __global__ void __launch_bounds__(H8_WARPS * 32) hist32_kernel(const uint32_t* _
                                     zsrc, lane);
     if (cnt == K32_TILE && aligned) {
       const uint4* v4 = reinterpret_cast<const uint4*>(src + first);  // 4 symbols per 16 bytes
+      // software-pipelined: the next batch's loads are in flight while this one is counted
+      constexpr int NBAT = H32_PIPE_BATCH;
+      uint4 qn[NBAT];
+#pragma unroll
+      for (int k = 0; k < NBAT; ++k) qn[k] = __ldcs(v4 + k * 32 + lane);
 #pragma unroll 1
-      for (int k0 = 0; k0 < K32_TILE / 4 / 32; k0 += H8_BATCH) {
-        uint4 q[H8_BATCH];
+      for (int k0 = 0; k0 < K32_TILE / 4 / 32; k0 += NBAT) {
+        uint4 q[NBAT];
 #pragma unroll
-        for (int k = 0; k < H8_BATCH; ++k) q[k] = __ldcs(v4 + (k0 + k) * 32 + lane);
+        for (int k = 0; k < NBAT; ++k) q[k] = qn[k];
+        if (k0 + NBAT < K32_TILE / 4 / 32) {
 #pragma unroll
-        for (int k = 0; k < H8_BATCH; ++k) {
+          for (int k = 0; k < NBAT; ++k) qn[k] = __ldcs(v4 + (k0 + NBAT + k) * 32 + lane);
+        }
+#pragma unroll
+        for (int k = 0; k < NBAT; ++k) {
           if (check) vmax = max(max(vmax, max(q[k].x, q[k].y)), max(q[k].z, q[k].w));
           // byte 2 (the digit) of the four symbols
           const uint32_t d4 = prmt(prmt(q[k].x, q[k].y, 0x0062), prmt(q[k].z, q[k].w, 0x0062), 0x5410);
