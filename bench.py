@@ -457,11 +457,19 @@ def main():
         # levels overlap (PCIe is full duplex); every build still moves its whole
         # text host->device and all its level words device->host inside the timed
         # region
-        barrier()
-        t0 = time.perf_counter()
-        builder.build_host_batch([harr] * e2e_steps, sigma, kind,
-                                 out_words=[hwords[i % len(hwords)] for i in range(e2e_steps)])
-        dt = (time.perf_counter() - t0) / e2e_steps
+        # three timed queues, the median reported (host-side hiccups of the copy
+        # path -- an occasional one-off stall of a whole queue was seen -- do not
+        # decide the figure)
+        queue = [harr] * e2e_steps
+        outs_q = [hwords[i % len(hwords)] for i in range(e2e_steps)]
+        builder.build_host_batch(queue, sigma, kind, out_words=outs_q)  # warm-up at the timed queue length
+        reps = []
+        for _ in range(3):
+            barrier()
+            t0 = time.perf_counter()
+            builder.build_host_batch(queue, sigma, kind, out_words=outs_q)
+            reps.append((time.perf_counter() - t0) / e2e_steps)
+        dt = statistics.median(reps)
         if world > 1:
             t = torch.tensor([dt, lat], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -470,6 +478,7 @@ def main():
                        "h2d_bytes_per_step": n * sym_bytes,
                        "d2h_bytes_per_step": w * nwords * 8 + w * 8 + 4,
                        "steps": e2e_steps, "latency_ms": lat * 1e3,
+                       "queues_ms_per_step": [round(r * 1e3, 3) for r in reps],
                        "path": "wvlt_build_host_batch (C ABI) over a queue of K builds with page-locked host "
                                "buffers: upload of text i+1, build i and download of build i-1's levels overlap "
                                "on three streams; latency_ms = one build at a time through wvlt_build_host"}

@@ -2948,7 +2948,7 @@ int wvlt_build_host_batch(int count, const void* const* host_texts, const int64_
   // with it the enqueueing of the next upload)
   static thread_local int64_t* stage = nullptr;
   static thread_local size_t stage_len = 0;
-  const size_t need_stage = (size_t)count * small_slot;
+  const size_t need_stage = (size_t)std::max(count, 64) * small_slot;  // (grown rarely: cudaFreeHost syncs)
   if (stage_len < need_stage) {
     if (stage) cudaFreeHost(stage);
     stage = nullptr;
