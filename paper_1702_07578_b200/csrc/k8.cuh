@@ -515,7 +515,10 @@ template <int W, int NC>
 __device__ __forceinline__ void emit_levels8(const Tab8& tt, const uint32_t* bits, uint64_t* words, int64_t nwords,
                                              int tid, int nthreads, uint8_t* coarse) {
   constexpr int NR = (1 << W) - 2;
-  constexpr int G = 16;  // tasks per coarse map entry
+#ifndef K8_EMIT_G
+#define K8_EMIT_G 8  // measured: 8 < 16 < 4 < 32
+#endif
+  constexpr int G = K8_EMIT_G;  // tasks per coarse map entry
 #ifdef K8_NO_EMIT
   const int total = 0;
 #else
