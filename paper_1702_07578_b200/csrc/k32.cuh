@@ -148,7 +148,7 @@ __device__ __forceinline__ void planes4(uint32_t e0, uint32_t e1, uint32_t e2, u
 
 template <int W>
 __global__ void __launch_bounds__(K32_NT, K32_CTAS) level_pass32_kernel(const Pass32Args a,
-                                                                        const Tab8* __restrict__ tabs) {
+                                                                        const TabW<W>* __restrict__ tabs) {
   constexpr int T = K32_TILE;
   constexpr int NT = K32_NT;
   constexpr int Q = K32_Q;
@@ -161,8 +161,8 @@ __global__ void __launch_bounds__(K32_NT, K32_CTAS) level_pass32_kernel(const Pa
   extern __shared__ __align__(128) unsigned char smem[];
   // [buffer 0: staged tile, then orders 2, 4, .. (4-byte elements; the last
   //  order 2-byte payloads) | buffer 1: orders 1, 3, .. | run table | level bits]
-  Tab8& tt = *reinterpret_cast<Tab8*>(smem + 8 * T);
-  uint32_t* bits = reinterpret_cast<uint32_t*>(smem + 8 * T + sizeof(Tab8)) - (NC + 4);
+  TabW<W>& tt = *reinterpret_cast<TabW<W>*>(smem + 8 * T);
+  uint32_t* bits = reinterpret_cast<uint32_t*>(smem + 8 * T + sizeof(TabW<W>)) - (NC + 4);
   __shared__ __align__(16) uint32_t s_wtot[2][P][NW];
   __shared__ uint32_t s_tmp[NW];
   __shared__ uint32_t s_lut[256];
@@ -181,11 +181,11 @@ __global__ void __launch_bounds__(K32_NT, K32_CTAS) level_pass32_kernel(const Pa
     mbar_init(mbar, 1);
     fence_mbar_init();
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar),
-                 "r"((uint32_t)(sizeof(Tab8) + (bulk ? 4 * T : 0)))
+                 "r"((uint32_t)(sizeof(TabW<W>) + (bulk ? 4 * T : 0)))
                  : "memory");
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                      sbase + 8 * T),
-                 "l"(tabs + tile), "r"((uint32_t)sizeof(Tab8)), "r"(mbar)
+                 "l"(tabs + tile), "r"((uint32_t)sizeof(TabW<W>)), "r"(mbar)
                  : "memory");
     if (bulk)
       asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -330,13 +330,13 @@ cudaError_t launch_hist32(const uint32_t* src, int64_t n, int64_t ntiles, uint32
 }
 
 template <int W>
-cudaError_t launch_pass32(const Pass32Args& a, const Tab8* tabs, cudaStream_t s) {
+cudaError_t launch_pass32(const Pass32Args& a, const void* tabs, cudaStream_t s) {
   constexpr int T = K32_TILE;
-  const size_t smem = 8 * (size_t)T + sizeof(Tab8) + (size_t)(W - 1) * (T / 32 + 4) * 4;
+  const size_t smem = 8 * (size_t)T + sizeof(TabW<W>) + (size_t)(W - 1) * (T / 32 + 4) * 4;
   auto kern = level_pass32_kernel<W>;
   cudaError_t e0 = ensure_smem_attr((const void*)kern, (int)smem, true);
   if (e0 != cudaSuccess) return e0;
-  kern<<<(unsigned)a.ntiles, K32_NT, smem, s>>>(a, tabs);
+  kern<<<(unsigned)a.ntiles, K32_NT, smem, s>>>(a, (const TabW<W>*)tabs);
   return cudaGetLastError();
 }
 
@@ -354,7 +354,7 @@ int build_k32(const uint32_t* src, int64_t n, int W, uint64_t* level_words, int6
   int64_t* totals = (int64_t*)(ws + L.off_totals);
   int64_t* base = (int64_t*)(ws + L.off_base);
   int64_t* baseW = (int64_t*)(ws + L.off_baseW);
-  Tab8* tabs = (Tab8*)(ws + L.off_tabs);
+  void* tabs = ws + L.off_tabs;  // TabW<W> per tile
   const int64_t nwords = (n + 63) >> 6;
   cudaError_t e;
   switch (W) {

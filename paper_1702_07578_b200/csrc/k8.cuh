@@ -498,13 +498,19 @@ __device__ __forceinline__ void table8_compute(Tables8& tt, const uint32_t* s_ba
 // Compact per-tile run table written by tiles8_kernel and bulk-copied into
 // the pass kernel's shared memory with the tile: positions fit 32 bits (the
 // single-pass path needs n < 2^32), sizes and offsets inside a tile 16 bits.
-struct Tab8 {
-  uint32_t gs[256];   // run starts in the global level
-  uint16_t cnt[256];  // run sizes
-  uint16_t ls[256];   // run starts in the tile-local order of the level
-  uint16_t wpre[256]; // destination words before each run; wpre[NR] = total
+// Sized by the width: 2^W - 2 runs plus the emission total, rounded so the
+// table stays a multiple of 16 bytes (W = 8: 256 entries, 2560 bytes; W = 4:
+// 16 entries, 160 bytes).
+template <int W>
+struct TabW {
+  static constexpr int NRP = (((1 << W) - 1) + 7) & ~7;
+  uint32_t gs[NRP];   // run starts in the global level
+  uint16_t cnt[NRP];  // run sizes
+  uint16_t ls[NRP];   // run starts in the tile-local order of the level
+  uint16_t wpre[NRP]; // destination words before each run; wpre[NR] = total
 };
-static_assert(sizeof(Tab8) % 16 == 0, "bulk-copy granularity");
+using Tab8 = TabW<8>;  // the largest (workspace sizing)
+static_assert(sizeof(Tab8) == 2560 && sizeof(TabW<2>) % 16 == 0 && sizeof(TabW<5>) % 16 == 0, "bulk-copy granularity");
 
 // Emission of levels 1..W-1 from a tile's level-bit arrays (NC + 4 words per
 // level, tile-local order): one destination word per task, the runs of all
@@ -512,7 +518,7 @@ static_assert(sizeof(Tab8) % 16 == 0, "bulk-copy granularity");
 // stores of a warp coalesce); whole words stored, run-edge words OR-ed (runs of
 // neighbouring tiles share them; the levels were zeroed).
 template <int W, int NC>
-__device__ __forceinline__ void emit_levels8(const Tab8& tt, const uint32_t* bits, uint64_t* words, int64_t nwords,
+__device__ __forceinline__ void emit_levels8(const TabW<W>& tt, const uint32_t* bits, uint64_t* words, int64_t nwords,
                                              int tid, int nthreads, uint8_t* coarse) {
   constexpr int NR = (1 << W) - 2;
 #ifndef K8_EMIT_G
@@ -561,7 +567,7 @@ constexpr int T8_WARPS = 8;
 // One warp per tile: the tile's run tables (table8_compute) into the compact
 // global layout, off the pass kernel's critical path.
 template <int W>
-__global__ void __launch_bounds__(T8_WARPS * 32) tiles8_kernel(const Pass8Args a, Tab8* __restrict__ out) {
+__global__ void __launch_bounds__(T8_WARPS * 32) tiles8_kernel(const Pass8Args a, TabW<W>* __restrict__ out) {
   constexpr int NR = (1 << W) - 2;
   extern __shared__ __align__(16) unsigned char t8_smem[];
   __shared__ uint32_t s_base[256];  // global group starts of every run
@@ -582,8 +588,8 @@ __global__ void __launch_bounds__(T8_WARPS * 32) tiles8_kernel(const Pass8Args a
     if (tile + nw < a.ntiles) table8_load<W>(a, tile + nw, lane, rc, rp);  // next row in flight
     table8_compute<W>(tt, s_base, lane);
     __syncwarp();
-    Tab8* o = out + tile;
-    for (int r = lane; r < 256; r += 32) {
+    TabW<W>* o = out + tile;
+    for (int r = lane; r < TabW<W>::NRP; r += 32) {
       o->gs[r] = tt.gs[r];
       o->cnt[r] = tt.cnt[r];
       o->ls[r] = tt.ls[r];
@@ -606,7 +612,7 @@ struct K8Cfg {
 };
 
 template <int W, int Q>
-__global__ void __launch_bounds__(K8Cfg<Q>::NT, K8Cfg<Q>::CTAS) level_pass8_kernel(const Pass8Args a, const Tab8* __restrict__ tabs) {
+__global__ void __launch_bounds__(K8Cfg<Q>::NT, K8Cfg<Q>::CTAS) level_pass8_kernel(const Pass8Args a, const TabW<W>* __restrict__ tabs) {
   constexpr int T = K8_TILE;
   constexpr int NT = K8Cfg<Q>::NT;
   constexpr int R = T / Q;  // region of run k
@@ -616,8 +622,8 @@ __global__ void __launch_bounds__(K8Cfg<Q>::NT, K8Cfg<Q>::CTAS) level_pass8_kern
   constexpr uint32_t B1 = 0x01010101u;
   extern __shared__ __align__(128) unsigned char smem[];
   // [stage | ping-pong order buffer | run table | level bits of levels 1..W-1]
-  Tab8& tt = *reinterpret_cast<Tab8*>(smem + 2 * T);
-  uint32_t* bits = reinterpret_cast<uint32_t*>(smem + 2 * T + sizeof(Tab8)) - (NC + 4);  // level j at j (NC+4)
+  TabW<W>& tt = *reinterpret_cast<TabW<W>*>(smem + 2 * T);
+  uint32_t* bits = reinterpret_cast<uint32_t*>(smem + 2 * T + sizeof(TabW<W>)) - (NC + 4);  // level j at j (NC+4)
   __shared__ __align__(16) uint32_t s_wtot[2][P][NW];
   __shared__ uint32_t s_lut[256];
   __shared__ __align__(8) uint64_t s_mbar;
@@ -635,11 +641,11 @@ __global__ void __launch_bounds__(K8Cfg<Q>::NT, K8Cfg<Q>::CTAS) level_pass8_kern
     fence_mbar_init();
     // the run table always comes by bulk copy, the tile when it is whole and aligned
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar),
-                 "r"((uint32_t)(sizeof(Tab8) + (bulk ? T : 0)))
+                 "r"((uint32_t)(sizeof(TabW<W>) + (bulk ? T : 0)))
                  : "memory");
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                      sbase + 2 * T),
-                 "l"(tabs + tile), "r"((uint32_t)sizeof(Tab8)), "r"(mbar)
+                 "l"(tabs + tile), "r"((uint32_t)sizeof(TabW<W>)), "r"(mbar)
                  : "memory");
     if (bulk)
       asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -760,24 +766,24 @@ __global__ void __launch_bounds__(K8Cfg<Q>::NT, K8Cfg<Q>::CTAS) level_pass8_kern
 
 // per-tile run tables, one warp per tile
 template <int W>
-cudaError_t launch_tiles8(const Pass8Args& a, Tab8* tabs, cudaStream_t s) {
+cudaError_t launch_tiles8(const Pass8Args& a, void* tabs, cudaStream_t s) {
   constexpr size_t sm = (size_t)T8_WARPS * sizeof(Tables8);
   cudaError_t e0 = ensure_smem_attr((const void*)tiles8_kernel<W>, (int)sm);
   if (e0 != cudaSuccess) return e0;
   const int64_t blocks = std::min<int64_t>((a.ntiles + T8_WARPS - 1) / T8_WARPS, (int64_t)sm_count() * 4);
-  tiles8_kernel<W><<<(unsigned)blocks, T8_WARPS * 32, sm, s>>>(a, tabs);
+  tiles8_kernel<W><<<(unsigned)blocks, T8_WARPS * 32, sm, s>>>(a, (TabW<W>*)tabs);
   return cudaGetLastError();
 }
 
 template <int W>
-cudaError_t launch_pass8(const Pass8Args& a, Tab8* tabs, cudaStream_t s) {
+cudaError_t launch_pass8(const Pass8Args& a, void* tabs, cudaStream_t s) {
   constexpr int T = K8_TILE;
   // level bits of levels 1..W-1 only (level 0 comes from hist8_kernel)
-  const size_t smem = 2 * (size_t)T + sizeof(Tab8) + (size_t)(W - 1) * (T / 32 + 4) * 4;
+  const size_t smem = 2 * (size_t)T + sizeof(TabW<W>) + (size_t)(W - 1) * (T / 32 + 4) * 4;
   auto kern = level_pass8_kernel<W, K8_Q>;
   cudaError_t e0 = ensure_smem_attr((const void*)kern, (int)smem, true);
   if (e0 != cudaSuccess) return e0;
-  kern<<<(unsigned)a.ntiles, K8Cfg<K8_Q>::NT, smem, s>>>(a, tabs);
+  kern<<<(unsigned)a.ntiles, K8Cfg<K8_Q>::NT, smem, s>>>(a, (const TabW<W>*)tabs);
   return cudaGetLastError();
 }
 
@@ -891,7 +897,7 @@ int build_k8(const uint8_t* text, int64_t n, int64_t sigma, int w, int kind, uin
   a.tcnt8 = tcnt8;
   a.tpre8 = tpre8;
   a.base = base;
-  Tab8* tabs = (Tab8*)(ws + L.off_tabs);
+  void* tabs = ws + L.off_tabs;  // TabW<w> per tile
   switch (w) {
     case 2: e = launch_tiles8<2>(a, tabs, s); break;
     case 3: e = launch_tiles8<3>(a, tabs, s); break;
