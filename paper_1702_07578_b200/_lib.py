@@ -39,7 +39,25 @@ def load():
             f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
             "(nvcc, sm_100a); the wavelet construction path has no CPU fallback"
         )
-    L = ctypes.CDLL(str(LIB_PATH))
+    _lib = _bind(ctypes.CDLL(str(LIB_PATH)))
+    return _lib
+
+
+def load_variant(path) -> ctypes.CDLL:
+    """Experiments only (tools/variant_bench.py): bind a tuning variant built by
+    ``_build.build_variant`` in place of the product library for this process.
+    Must be called before anything else loads the library."""
+    global _lib
+    path = Path(path).resolve()
+    if path.parent != (_PKG.parent / "tools" / "variants").resolve():
+        raise ValueError("variants live in tools/variants/")
+    if _lib is not None:
+        raise RuntimeError("the product library is already loaded in this process")
+    _lib = _bind(ctypes.CDLL(str(path)))
+    return _lib
+
+
+def _bind(L):
     i64, i32, vp, sz = ctypes.c_int64, ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t
     L.wvlt_abi_version.argtypes = []
     L.wvlt_abi_version.restype = i32
@@ -75,7 +93,6 @@ def load():
     L.wvlt_profile_read.restype = i32
     if L.wvlt_abi_version() != 1:
         raise ImportError("wvlt_b200 ABI version mismatch")
-    _lib = L
     return L
 
 

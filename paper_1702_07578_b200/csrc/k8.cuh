@@ -525,11 +525,7 @@ __device__ __forceinline__ void emit_levels8(const TabW<W>& tt, const uint32_t* 
 #define K8_EMIT_G 8  // measured: 8 < 16 < 4 < 32
 #endif
   constexpr int G = K8_EMIT_G;  // tasks per coarse map entry
-#ifdef K8_NO_EMIT
-  const int total = 0;
-#else
   const int total = tt.wpre[NR];
-#endif
   // coarse task -> run map (shared scratch): the run of every 16th task, found by
   // one binary search each; a task then walks forward over the few runs that
   // start after its entry (empty runs share prefix values)
@@ -808,11 +804,7 @@ struct K8Layout {
 };
 
 inline bool k8_eligible(int sym_bytes, int w, int64_t n) {
-#ifdef WVLT_NO_K8
-  return false;
-#else
   return sym_bytes == 1 && w >= 2 && w <= 8 && n > 0 && n < (1ll << 32) - 64;
-#endif
 }
 
 inline K8Layout k8_layout(int64_t n, int w) {

@@ -168,14 +168,6 @@ __device__ __forceinline__ uint32_t shr_mul(uint32_t v) {
 // Inclusive warp scan (sum): shfl.up's in-range predicate guards the add, two
 // instructions per step.
 __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v) {
-#ifdef U8_PLAIN_SCAN
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t t = __shfl_up_sync(FULL, v, o);
-    if ((threadIdx.x & 31) >= o) v += t;
-  }
-  return v;
-#else
   asm("{\n\t.reg .u32 t;\n\t.reg .pred p;\n\t"
       "shfl.sync.up.b32 t|p, %0, 1, 0, -1;\n\t@p add.u32 %0, %0, t;\n\t"
       "shfl.sync.up.b32 t|p, %0, 2, 0, -1;\n\t@p add.u32 %0, %0, t;\n\t"
@@ -184,7 +176,6 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v) {
       "shfl.sync.up.b32 t|p, %0, 16, 0, -1;\n\t@p add.u32 %0, %0, t;\n\t}"
       : "+r"(v));
   return v;
-#endif
 }
 
 // mbarrier + bulk async copy (global -> shared), completion by transaction bytes
@@ -350,9 +341,14 @@ __global__ void __launch_bounds__(HIST_WARPS * 32) hist_u8_kernel(const uint8_t*
 // Generic histogram for wide symbols / wide alphabets.  Bins [0, 2^min(w,16))
 // live in shared memory as 16-bit counters packed two per word (128 KB at
 // most); an increment that wraps a counter is detected from the atomic's
-// returned old value and carried into the global histogram exactly (low half:
-// the carry that leaked into the high half is taken back).  Bins at or above
-// 2^16 (code widths 17..24) go to global atomics.
+// returned old value and carried into the global histogram exactly.  All the
+// accounting comes from that single atomic's old value (no second shared
+// atomic, so no interleaving can observe a half-corrected word): a low-half
+// wrap leaks its carry into the high half, which then over-reports the high
+// bin by one — the global high bin is debited 1 — and if that leaked carry in
+// turn wrapped the high half (old high == 0xFFFF), it is credited 65536, the
+// same as a high increment that wraps.  Bins at or above 2^16 (code widths
+// 17..24) go to global atomics.
 constexpr int HISTG_THREADS = 1024;
 template <typename TIn>
 __global__ void __launch_bounds__(HISTG_THREADS) hist_generic_kernel(const TIn* __restrict__ text, int64_t n, int w,
@@ -374,10 +370,18 @@ __global__ void __launch_bounds__(HISTG_THREADS) hist_generic_kernel(const TIn* 
     if ((v >> sw) == 0) {
       const uint32_t hi = v & 1u;
       const uint32_t old = atomicAdd(&s_pairs[v >> 1], hi ? 0x10000u : 1u);
-      const uint32_t half = hi ? (old >> 16) : (old & 0xFFFFu);
-      if (half == 0xFFFFu) {  // wrapped: carry 2^16 to the global bin
-        if (!hi) atomicSub(&s_pairs[v >> 1], 0x10000u);  // the carry leaked into the high half
-        if (hist) atomicAdd(&hist[v], 65536ull);
+      if (hist) {
+        if (hi) {
+          if ((old >> 16) == 0xFFFFu) atomicAdd(&hist[v], 65536ull);  // high half wrapped out of the word
+        } else if ((old & 0xFFFFu) == 0xFFFFu) {                     // low half wrapped
+          atomicAdd(&hist[v], 65536ull);
+          if (v + 1 < (1u << sw)) {
+            // The carry landed in the high half: debit it, and credit the
+            // high half's own wrap if the carry caused one.
+            const unsigned long long adj = (old >> 16) == 0xFFFFu ? 65535ull : ~0ull;
+            atomicAdd(&hist[v + 1], adj);
+          }
+        }
       }
     } else if (hist) {
       atomicAdd(&hist[v], 1ull);
@@ -1453,14 +1457,9 @@ __global__ void __launch_bounds__(U8_THREADS + U8_TABW, U8_CTAS_PER_SM) level_pa
 #pragma unroll
       for (int k = 0; k < 4; ++k) b[k] = (x[k] >> sh) & B1;
       // this thread's level bits: byte t (first half) and byte T/16 + t (second half)
-#ifdef U8_NEW_M
-      const uint32_t m0 = ((b[1] * 16u + b[0]) * 0x01020408u) >> 24;
-      const uint32_t m1 = ((b[3] * 16u + b[2]) * 0x01020408u) >> 24;
-#else
       // one multiply gathers a half's 8 flags (bits at 8i and 8i + 4 -> 24 + i, 28 + i)
       const uint32_t m0 = ((b[1] * 16u + b[0]) * 0x01020408u) >> 24;
       const uint32_t m1 = ((b[3] * 16u + b[2]) * 0x01020408u) >> 24;
-#endif
       const uint32_t ones0 = __popc(m0), ones1 = __popc(m1);
       if (j == 0) {
         // level l0 is in global order already: byte stores (32 lanes = 32 consecutive bytes)
@@ -1639,11 +1638,11 @@ __device__ __forceinline__ void merge_range(uint64_t* __restrict__ dst, int64_t 
     }
     t0 = __shfl_sync(FULL, t0, 0);
     uint64_t v[MERGE_WORDS_PER_LANE];
-#ifndef MERGE_SERIAL
     // the task of every word's first bit first (small, cached arrays), then all
     // source loads at once (independent, in flight together), then the words
     // that straddle a task boundary on the slow path
     int64_t sp[MERGE_WORDS_PER_LANE];
+    int nbk[MERGE_WORDS_PER_LANE];
     uint32_t single = 0;
     int64_t t = t0;
 #pragma unroll
@@ -1651,12 +1650,14 @@ __device__ __forceinline__ void merge_range(uint64_t* __restrict__ dst, int64_t 
       const int64_t wd = w0 + 32 * k + lane;
       const int64_t here = wd << 6;
       sp[k] = -1;
+      nbk[k] = 0;
       if (wd < whi && here < nbits) {
         while (__ldg(bounds + t + 1) <= here) ++t;
         const int64_t nb = min((int64_t)64, nbits - here);
         if (__ldg(bounds + t + 1) >= here + nb) {
           single |= 1u << k;
           sp[k] = __ldg(src_starts + t) + (here - __ldg(bounds + t));
+          nbk[k] = (int)nb;
         }
       }
     }
@@ -1667,7 +1668,8 @@ __device__ __forceinline__ void merge_range(uint64_t* __restrict__ dst, int64_t 
       lo[k] = hi[k] = 0;
       if ((single >> k) & 1u) {
         lo[k] = __ldg(s64 + (sp[k] >> 6));
-        if (sp[k] & 63) hi[k] = __ldg(s64 + (sp[k] >> 6) + 1);
+        // the next source word only when the bits run into it (never past the source's end)
+        if ((int)(sp[k] & 63) + nbk[k] > 64) hi[k] = __ldg(s64 + (sp[k] >> 6) + 1);
       }
     }
 #pragma unroll
@@ -1676,20 +1678,12 @@ __device__ __forceinline__ void merge_range(uint64_t* __restrict__ dst, int64_t 
       if ((single >> k) & 1u) {
         const int sh = (int)(sp[k] & 63);
         uint64_t x = sh ? ((lo[k] >> sh) | (hi[k] << (64 - sh))) : lo[k];
-        const int64_t nb = nbits - (wd << 6);
-        if (nb < 64) x &= (1ull << nb) - 1ull;
+        if (nbk[k] < 64) x &= (1ull << nbk[k]) - 1ull;
         v[k] = x;
       } else {
         v[k] = (wd < whi && (wd << 6) < nbits) ? merge_word(wd, nbits, bounds, src_starts, src, t0) : 0ull;
       }
     }
-#else
-#pragma unroll
-    for (int k = 0; k < MERGE_WORDS_PER_LANE; ++k) {
-      const int64_t wd = w0 + 32 * k + lane;
-      v[k] = (wd < whi && (wd << 6) < nbits) ? merge_word(wd, nbits, bounds, src_starts, src, t0) : 0ull;
-    }
-#endif
 #pragma unroll
     for (int k = 0; k < MERGE_WORDS_PER_LANE; ++k) {
       const int64_t wd = w0 + 32 * k + lane;
@@ -1832,16 +1826,8 @@ bool make_plan(int64_t n, int sym_bytes, int64_t sigma, int kind, Plan* P, bool 
   int l = 0, p = 0;
   int64_t corr = 0;
   size_t max_buf = 0;
-#ifndef WVLT_NO_K8_TAIL
   const bool tail = kind == WVLT_KIND_WM && w > 8 && n > 0 && n < (1ll << 32) - 64;
-#else
-  const bool tail = false;
-#endif
-#ifndef WVLT_NO_K16
   const bool k16 = tail && lean;
-#else
-  const bool k16 = false;
-#endif
   int cur_bytes = sb;  // element bytes of the next stage's input
   while (l < w && !(tail && w - l <= 8)) {
     if (k16 && !P->k32_w && w - l <= 24 && w - l >= 18 && cur_bytes == 4) {
@@ -2465,7 +2451,6 @@ int build_device_impl(const void* text, int sym_bytes, int64_t n, int64_t sigma,
     if (e != cudaSuccess) return (int)e;
   }
   const int64_t nwords = (n + 63) >> 6;
-#ifndef WVLT_NO_WT_VIA_WM
   if (kind == WVLT_KIND_WT && !borders && n > 0 && w > 8 && text && level_words && workspace) {
     WtViaWm L;
     if (wt_via_wm_layout(n, sym_bytes, sigma, &L)) {
@@ -2474,7 +2459,6 @@ int build_device_impl(const void* text, int sym_bytes, int64_t n, int64_t sigma,
                              s, pass_done, ctx);
     }
   }
-#endif
   if (n == 0 || w == 0) {
     // degenerate: no level bits to build (construct.py:457-458, bitperm.code_width)
     if (w == 0 && hist) {

@@ -72,14 +72,18 @@ class DeviceBuilder:
         self._ws = {}  # stream handle -> workspace (builds on different streams never share one)
 
     # -- buffers -------------------------------------------------------------
+    def workspace_bytes(self, n: int, sym_bytes: int, sigma: int, kind: str) -> int:
+        need = int(self.lib.wvlt_workspace_bytes(int(n), int(sym_bytes), int(sigma), _lib.KINDS[kind]))
+        if need == 0 and code_width(sigma) > _lib.MAX_WIDTH:
+            raise ValueError(f"alphabet size {sigma} exceeds the supported code width {_lib.MAX_WIDTH}")
+        return need
+
     def workspace(self, n: int, sym_bytes: int, sigma: int, kind: str, stream=None):
         """The workspace of builds on ``stream`` (default: the current stream), grown
         on demand.  It is allocated on that stream, so the caching allocator only
         recycles a replaced one after the stream's queued work."""
         torch = _torch()
-        need = int(self.lib.wvlt_workspace_bytes(int(n), int(sym_bytes), int(sigma), _lib.KINDS[kind]))
-        if need == 0 and code_width(sigma) > _lib.MAX_WIDTH:
-            raise ValueError(f"alphabet size {sigma} exceeds the supported code width {_lib.MAX_WIDTH}")
+        need = self.workspace_bytes(n, sym_bytes, sigma, kind)
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
         ws = self._ws.get(s.cuda_stream)
         if ws is None or ws.numel() < need:
@@ -101,7 +105,7 @@ class DeviceBuilder:
 
     # -- builds --------------------------------------------------------------
     def build(self, text, sigma: int, kind: str = "wm", *, borders: bool = False, histogram: bool = False,
-              outputs=None, stream=None, check: bool = True) -> DeviceBuild:
+              outputs=None, stream=None, check: bool = True, workspace=None) -> DeviceBuild:
         """Build from a device tensor of uint8/uint16/uint32 symbols in [0, sigma).
 
         ``outputs`` may pass preallocated (level_words, zeros, hist, borders, status)
@@ -111,6 +115,8 @@ class DeviceBuilder:
         come from the per-pass tile counts).
         With ``check`` the range status is read back (one device->host sync) and
         a bad symbol raises ValueError like construct._validated (construct.py:183-187).
+        ``workspace`` passes a private uint8 device buffer instead of the per-stream
+        shared one (a captured graph owns its own, see ``capture``).
         """
         torch = _torch()
         if kind not in _lib.KINDS:
@@ -136,7 +142,12 @@ class DeviceBuilder:
             with torch.cuda.stream(s):
                 outputs = self.alloc_outputs(n, sigma, borders)
         lw, zeros, hist, bd, status = outputs
-        ws, need = self.workspace(n, sb, sigma, kind, s)
+        if workspace is None:
+            ws, need = self.workspace(n, sb, sigma, kind, s)
+        else:
+            ws, need = workspace, self.workspace_bytes(n, sb, sigma, kind)
+            if ws.numel() < need:
+                raise ValueError(f"workspace holds {ws.numel()} bytes, the build needs {need}")
         rc = self.lib.wvlt_build_device(
             text.data_ptr() if n else None, sb, n, sigma, _lib.KINDS[kind],
             lw.data_ptr() if lw.numel() else None, zeros.data_ptr() if w else None,
@@ -151,20 +162,27 @@ class DeviceBuilder:
         """Capture one build of ``text`` (a device tensor kept as the graph's input
         buffer) into a CUDA graph: small, launch-bound builds replay it with one
         launch.  Refill ``text`` in place and call ``replay()`` for the next build
-        of the same length / alphabet / kind."""
+        of the same length / alphabet / kind.
+
+        The graph bakes in the workspace address, so it gets a private workspace
+        that the returned BuildGraph keeps alive (never the per-stream shared one,
+        which a later build could replace and free under the graph)."""
         torch = _torch()
         s = torch.cuda.Stream(self.device)
         s.wait_stream(torch.cuda.current_stream(self.device))
-        outputs = None
+        n = int(text.numel())
+        need = self.workspace_bytes(n, text.element_size(), sigma, kind)
         with torch.cuda.stream(s):
-            outputs = self.alloc_outputs(int(text.numel()), sigma)
-            self.build(text, sigma, kind, histogram=histogram, outputs=outputs, stream=s, check=False)  # warm-up
+            outputs = self.alloc_outputs(n, sigma)
+            ws = torch.empty(max(need, 256), dtype=torch.uint8, device=self.device)
+            self.build(text, sigma, kind, histogram=histogram, outputs=outputs, stream=s, check=False,
+                       workspace=ws)  # warm-up
         s.synchronize()
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=s):
             res = self.build(text, sigma, kind, histogram=histogram, outputs=outputs,
-                             stream=torch.cuda.current_stream(self.device), check=False)
-        return BuildGraph(g, res, text)
+                             stream=torch.cuda.current_stream(self.device), check=False, workspace=ws)
+        return BuildGraph(g, res, text, ws)
 
     def build_host(self, arr: np.ndarray, sigma: int, kind: str, *, out_words: np.ndarray | None = None,
                    histogram: bool = False, stream=None):
@@ -284,8 +302,9 @@ class BuildGraph:
     contents of ``text``; ``result`` holds the output tensors, ``check()`` raises
     ValueError if the last replay saw a symbol outside [0, sigma)."""
 
-    def __init__(self, graph, result: DeviceBuild, text):
+    def __init__(self, graph, result: DeviceBuild, text, workspace):
         self.graph, self.result, self.text = graph, result, text
+        self.workspace = workspace  # the address the graph writes into: owned here
 
     def replay(self) -> DeviceBuild:
         self.graph.replay()

@@ -6,7 +6,8 @@ generated on the GPU with torch's seeded Philox generator, in chunks.
 
   c1  n=2^20  u8  sigma=256  uniform
   c2  n=2^30  u8  sigma=256  Zipf(s=1.1) ranks -> byte values via a seeded permutation
-  c3  n=2^30  u8  sigma=4 order-3 Markov chain, Dirichlet(0.5) transitions;
+  c3  n=2^30  u8  sigma=4: one order-3 Markov chain, Dirichlet(0.5) transitions
+      (generated in parallel segments, exactly; see _markov3_chain);
       variant sigma=5 replaces 1% of positions by the rare symbol 4
   c4  n=2^29  u16 sigma=2^16: 50% Zipf(s=1.0) over all values, 50% uniform over a
       random 4096-value subset
@@ -29,8 +30,8 @@ CONFIGS = {
 DESCRIPTIONS = {
     "c1": "WT n=2^20 u8 sigma=256 uniform",
     "c2": "WM n=2^30 u8 sigma=256 Zipf(1.1) ranks via seeded permutation",
-    "c3": "WM n=2^30 u8 sigma=5 order-3 Markov (Dirichlet 0.5) + 1% rare symbol",
-    "c3s4": "WM n=2^30 u8 sigma=4 order-3 Markov (Dirichlet 0.5)",
+    "c3": "WM n=2^30 u8 sigma=5 one order-3 Markov chain (Dirichlet 0.5 rows, uniform head) + 1% rare symbol",
+    "c3s4": "WM n=2^30 u8 sigma=4 one order-3 Markov chain (Dirichlet 0.5 rows, uniform head)",
     "c4": "WM n=2^29 u16 sigma=2^16 50% Zipf(1.0) + 50% uniform over 4096-subset",
     "c5": "WM n=2^31 u32 sigma=2^20 log-uniform",
 }
@@ -46,6 +47,48 @@ def _zipf_ranks(g, n, k, s, device):
     cdf[-1] = 1.0
     u = torch.rand(n, generator=g, dtype=torch.float64, device=device)
     return torch.searchsorted(cdf, u).clamp_(max=k - 1)
+
+
+def _markov3_chain(g, n, device):
+    """ONE order-3 Markov chain over {0..3} of n steps: 64 contexts x Dirichlet(0.5)
+    transition rows, a uniform initial context (the first 3 symbols), step t
+    consuming one uniform draw.
+
+    The chain is computed in 2^14-step segments advanced in lock step.  Pass 1
+    runs every segment from all 64 possible entry contexts at once (same draws)
+    to get each segment's exit context as a function of its entry; the entry
+    context of every segment then follows sequentially from the chain's head
+    (one table lookup per segment); pass 2 replays the same draws from those
+    entries and emits the symbols.  The output is exactly the sequential chain.
+    """
+    alpha = torch.full((64, 4), 0.5, dtype=torch.float64, device=device)
+    gam = torch._standard_gamma(alpha, generator=g)
+    table = torch.cumsum(gam / gam.sum(1, keepdim=True), 1)
+    table[:, -1] = 1.0
+    seg = 1 << 14
+    nseg = max((n + seg - 1) // seg, 1)
+    head = int(torch.randint(0, 64, (1,), generator=g, device=device).item())
+    state = g.get_state()
+    ctx = torch.arange(64, device=device).repeat(nseg, 1)  # [segment, entry context]
+    for _ in range(seg):
+        u = torch.rand(nseg, generator=g, dtype=torch.float64, device=device)
+        sym = (u[:, None, None] > table[ctx]).sum(2).clamp_(max=3)
+        ctx = ((ctx << 2) | sym) & 63
+    exit_of = ctx.cpu().numpy()
+    entries = [0] * nseg
+    c = head
+    for k in range(nseg):
+        entries[k] = c
+        c = int(exit_of[k, c])
+    g.set_state(state)
+    ctx = torch.tensor(entries, device=device)
+    buf = torch.empty((nseg, seg), dtype=torch.uint8, device=device)
+    for t in range(seg):
+        u = torch.rand(nseg, generator=g, dtype=torch.float64, device=device)
+        sym = (u[:, None] > table[ctx]).sum(1).clamp_(max=3)
+        buf[:, t] = sym.to(torch.uint8)
+        ctx = ((ctx << 2) | sym) & 63
+    return buf.view(-1)[:n]
 
 
 def generate(name: str, device="cuda", n: int | None = None, seed: int | None = None) -> torch.Tensor:
@@ -66,22 +109,7 @@ def generate(name: str, device="cuda", n: int | None = None, seed: int | None = 
             m = min(CHUNK, n - i)
             out[i : i + m] = perm[_zipf_ranks(g, m, 256, 1.1, device)].to(torch.uint8)
     elif name in ("c3", "c3s4"):
-        # 64 contexts x Dirichlet(0.5) rows; independent chain segments of 2^14
-        # steps advanced in lock step (segment heads drawn uniformly)
-        alpha = torch.full((64, 4), 0.5, dtype=torch.float64, device=device)
-        gam = torch._standard_gamma(alpha, generator=g)
-        table = torch.cumsum(gam / gam.sum(1, keepdim=True), 1)
-        table[:, -1] = 1.0
-        seg = 1 << 14
-        nseg = (n + seg - 1) // seg
-        ctx = torch.randint(0, 64, (nseg,), generator=g, device=device)
-        buf = torch.empty((nseg, seg), dtype=torch.uint8, device=device)
-        for t in range(seg):
-            u = torch.rand(nseg, generator=g, dtype=torch.float64, device=device)
-            sym = (u.unsqueeze(1) > table[ctx]).sum(1).clamp_(max=3)
-            buf[:, t] = sym.to(torch.uint8)
-            ctx = ((ctx << 2) | sym) & 63
-        out.copy_(buf.view(-1)[:n])
+        out.copy_(_markov3_chain(g, n, device))
         if name == "c3":
             for i in range(0, n, CHUNK):
                 m = min(CHUNK, n - i)
