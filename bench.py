@@ -164,23 +164,54 @@ def cpu_threads() -> int:
         return os.cpu_count() or 1
 
 
-def cpu_baseline(text_host: np.ndarray, sigma: int, kind: str, sample: int, runs: int = 3):
-    """Oracle port of the reference ps builder on all host cores over text[:sample]."""
+def cpu_model() -> str:
+    try:
+        for ln in Path("/proc/cpuinfo").read_text().splitlines():
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:  # pragma: no cover
+        pass
+    return "unknown"
+
+
+REF_NOTE = ("the reference package (wvlt: Python + numba) cannot run on the GPU box: numba is not installed in "
+            "this image and there is no network; its algorithms run as the oracle's C restatement (kind 'port'), "
+            "pinned to the reference's own golden vectors (tests/test_oracle_golden.py)")
+
+
+def cpu_baseline(text_host: np.ndarray, sigma: int, kind: str, sample: int, runs: int = 3, algo: str = "ps",
+                 threads: int | None = None):
+    """Oracle port of a reference builder (ps by default) on all host cores over text[:sample]."""
     import oracle
 
-    threads = cpu_threads()
+    threads = threads or cpu_threads()
     piece = np.ascontiguousarray(text_host[:sample])
-    oracle.build(piece[: 1 << 16], sigma, kind, "ps", threads)  # warm-up
+    oracle.build(piece[: 1 << 16], sigma, kind, algo, threads)  # warm-up
     times = []
     for _ in range(runs):
         t0 = time.perf_counter()
-        oracle.build(piece, sigma, kind, "ps", threads)
+        oracle.build(piece, sigma, kind, algo, threads)
         times.append(time.perf_counter() - t0)
     t = statistics.median(times)
+    src = {"ps": "construct.py:322-387", "pc": "construct.py:292-319", "ddps": "construct.py:437-543",
+           "ddpc": "construct.py:437-543"}[algo]
     return {"value": piece.size / t, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"first {piece.size} symbols of the same {kind.upper()} text, oracle ps "
-                      f"(restatement of construct.py:322-387) with {threads} POSIX threads, median of {runs}",
-            "seconds_per_build": t}
+            "sample": (f"{'all' if piece.size == text_host.size else 'first'} {piece.size} symbols of the same "
+                       f"{kind.upper()} text, oracle {algo} (restatement of {src}) with {threads} POSIX "
+                       f"thread{'s' if threads > 1 else ''}, median of {runs}"),
+            "cpu_model": cpu_model(), "reference_package": REF_NOTE, "seconds_per_build": t}
+
+
+def cpu_variants(text_host: np.ndarray, sigma: int, kind: str, pc_sample: int):
+    """BASELINE.md §4's other CPU figures: ddps / ddpc at all host threads on the
+    whole text, pc on one thread over a bounded sample (it is ~50x slower)."""
+    out = {}
+    for algo in ("ddps", "ddpc"):
+        r = cpu_baseline(text_host, sigma, kind, text_host.size, runs=1, algo=algo)
+        out[algo] = {"value": r["value"], "cores": r["cores"], "sample": r["sample"]}
+    r = cpu_baseline(text_host, sigma, kind, min(pc_sample, text_host.size), runs=1, algo="pc", threads=1)
+    out["pc_p1"] = {"value": r["value"], "cores": 1, "sample": r["sample"]}
+    return out
 
 
 def run_reference(args):
@@ -192,9 +223,10 @@ def run_reference(args):
     if rank != 0:
         return 0
     cfg = workloads.CONFIGS[args.config]
-    sample = min(cfg["n"], args.cpu_sample)
-    text = workloads.generate(args.config, device="cuda" if torch.cuda.is_available() else "cpu", n=sample)
+    sample = min(cfg["n"], args.cpu_sample) if args.cpu_sample else cfg["n"]
+    text = workloads.generate(args.config, device="cuda" if torch.cuda.is_available() else "cpu")
     host = text.cpu().numpy()
+    del text
     kind = args.kind or cfg["kind"]
     for _ in range(args.warmup):
         cpu_baseline(host, cfg["sigma"], kind, min(sample, 1 << 20), runs=1)
@@ -211,10 +243,15 @@ def run_reference(args):
         "data": "synthetic", "config": {"workload": args.config, "description": workloads.DESCRIPTIONS[args.config],
                                          "kind": kind, "n": sample, "sigma": cfg["sigma"]},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cpu_threads(), "kind": "port",
-                         "sample": f"first {sample} symbols per step (bounded sample of the {args.config} text); "
-                                   "oracle ps = restatement of the reference ps builder, all host threads"},
+                         "sample": (f"{'the whole' if sample == cfg['n'] else f'first {sample} symbols of the'} "
+                                    f"{args.config} text per step (same config as the GPU arm); oracle ps = "
+                                    "restatement of the reference ps builder (construct.py:322-387), all host threads"),
+                         "cpu_model": cpu_model(), "reference_package": REF_NOTE},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "same_config": sample == cfg["n"],
     }
+    if not args.no_variants:
+        line["cpu_variants"] = cpu_variants(host, cfg["sigma"], kind, 1 << 26)
     print(json.dumps(line))
     return 0
 
@@ -227,7 +264,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2")
     ap.add_argument("--kind", default=None, choices=[None, "wt", "wm"])
-    ap.add_argument("--cpu-sample", type=int, default=1 << 28)
+    ap.add_argument("--cpu-sample", type=int, default=0, help="symbols of the CPU legs (0 = the whole config text)")
+    ap.add_argument("--borders", action="store_true", help="also emit the node borders (always on for c1)")
+    ap.add_argument("--no-variants", action="store_true", help="skip the ddps / ddpc / pc p=1 CPU figures")
+    ap.add_argument("--no-api", action="store_true", help="skip the build_structure (numpy in, BitVectors out) figure")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-wt", action="store_true")
@@ -262,7 +302,9 @@ def main():
     # weak scaling: every rank builds its own n-symbol shard of the job
     text = workloads.generate(args.config, device=dev, seed=workloads.SEED + 101 * rank)
     builder = DeviceBuilder(dev)
-    outs = builder.alloc_outputs(n, sigma)
+    # c1's output is "8 packed bit vectors plus node borders" (BASELINE.json configs[0])
+    want_borders = args.borders or args.config == "c1"
+    outs = builder.alloc_outputs(n, sigma, want_borders)
     stream = torch.cuda.current_stream(dev)
     npass = len(pass_plan(n, sym_bytes, sigma, kind))
 
@@ -290,14 +332,14 @@ def main():
     def one_build(kind_):
         if args.graph and not sharded:
             if kind_ not in graphs:
-                graphs[kind_] = builder.capture(text, sigma, kind_)
+                graphs[kind_] = builder.capture(text, sigma, kind_, borders=want_borders)
             return graphs[kind_].replay()
         if sharded:
             # one WM/WT over the whole job's world * n symbols: local builds, NCCL
             # histogram all_gather, then the merge over peer memory (p2p) or the
             # bit-segment all_to_all + shift-merge (nccl)
             return build_sharded(text, sigma, kind_, ops=ops, transport=transport)
-        return builder.build(text, sigma, kind_, outputs=outs, check=False)
+        return builder.build(text, sigma, kind_, outputs=outs, borders=want_borders, check=False)
 
     def timed(kind_, steps, warmup):
         for _ in range(warmup):
@@ -321,7 +363,7 @@ def main():
         return ms
 
     # correctness gate on the benchmark input: range status must be clean
-    builder.build(text, sigma, kind, outputs=outs, check=True)
+    builder.build(text, sigma, kind, outputs=outs, borders=want_borders, check=True)
     launches_per_build = int(builder.lib.wvlt_last_launches())  # our kernels in one device build
 
     with ClockSampler(local) as clk:
@@ -332,15 +374,20 @@ def main():
     _lib.profile_enable(True)
     stage_ms: dict[str, list[float]] = {}
     for _ in range(max(3, min(args.steps, 5))):
-        builder.build(text, sigma, kind, outputs=outs, check=False)
+        builder.build(text, sigma, kind, outputs=outs, borders=want_borders, check=False)
         for name, t in _lib.profile_read():
             stage_ms.setdefault(name, []).append(t)
     _lib.profile_enable(False)
     stages = {k: statistics.median(v) for k, v in stage_ms.items()}
-    dominant = max((k for k in stages if k != "memset"), key=lambda k: stages[k])
+    # the dominant kernel: the longest stage that moves the text (K1 or a level pass)
+    dominant = max((k for k in stages if k == "hist" or k.startswith("pass")), key=lambda k: stages[k])
     peak, peak_src = peaks()
+    mbytes = metric_bytes(n, sym_bytes, sigma)
+    # SURVEY §8(d) bytes of the build (text read once per level + level bits)
+    # over the dominant kernel's own CUDA-event time: the fused pass emits the
+    # build (every level but level 0) in one kernel
+    achieved = mbytes / (stages[dominant] * 1e-3) / 1e9
     dom_bytes = stage_bytes(dominant, n, sym_bytes, sigma, kind)
-    achieved = dom_bytes / (stages[dominant] * 1e-3) / 1e9
     traffic = None
     tf = ROOT / "profiles" / f"ncu_traffic_{args.config}_{kind}.json"
     if tf.exists():
@@ -359,7 +406,6 @@ def main():
                        "source": f"profiles/ncu_smem_{args.config}_{kind}.json (ncu --set full, one launch)"}
 
     value = world * n / (ms * 1e-3)
-    mbytes = metric_bytes(n, sym_bytes, sigma)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
@@ -369,13 +415,21 @@ def main():
                    "l2": ("inputs larger than L2 (text %d MiB per GPU vs 126 MB L2); no flush" % (n * sym_bytes >> 20)
                           if n * sym_bytes > (126 << 20) else
                           "L2-resident input (text %d KiB); no flush: a launch-bound correctness config" % (n * sym_bytes >> 10)),
-                   "graph": bool(args.graph and not sharded),
+                   "graph": bool(args.graph and not sharded), "node_borders": bool(want_borders),
                    "parallelism": (f"sharded{world} (position shards; NCCL all_gather of histograms, "
                                    + ("merge over peer memory)" if transport == "p2p" else "NCCL all_to_all + merge)")
                                    if world > 1 else "single")},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "kernel": dominant, "kernel_ms": stages[dominant],
-                     "algorithmic_bytes": dom_bytes, "peak_source": peak_src, "limiter": limiter},
+                     "algorithmic_bytes": mbytes,
+                     "definition": "SURVEY 8d bytes of the build, B = L (n s + n/8), over the dominant kernel's "
+                                   "CUDA-event time",
+                     "physical": {"bytes": traffic, "frac": (traffic / (stages[dominant] * 1e-3) / 1e9 / peak)
+                                  if traffic else None, "kernel_own_bytes": dom_bytes,
+                                  "kernel_own_frac": dom_bytes / (stages[dominant] * 1e-3) / 1e9 / peak,
+                                  "note": "traffic = ncu dram bytes of one launch (profiles/); kernel_own_bytes = "
+                                          "the text it reads + the bytes it writes"},
+                     "peak_source": peak_src, "limiter": limiter},
         "metric_roofline": {"bytes_per_build": mbytes, "achieved_gbs": mbytes / (ms * 1e-3) / 1e9,
                             "frac": mbytes / (ms * 1e-3) / 1e9 / peak,
                             "definition": "SURVEY 8d: B = L (n s + n/8), text read once per level + level bits"},
@@ -484,9 +538,31 @@ def main():
                                "on three streams; latency_ms = one build at a time through wvlt_build_host"}
         line["gpu_launches"] += (lat_steps + e2e_steps) * host_launches
 
+    if not args.no_api and not sharded and rank == 0:
+        # the reference-facing Python API exactly as the reference's callers use it:
+        # a pageable numpy text in, a WaveletMatrix / LevelWiseWaveletTree of
+        # BitVectors (numpy words) out, node borders included
+        import paper_1702_07578_b200 as wv
+
+        arr = text.cpu().numpy()
+        wv.build_structure(arr, sigma, kind, "ps")  # warm-up (staging buffers, workspace)
+        api = []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            st = wv.build_structure(arr, sigma, kind, "ps")
+            api.append(time.perf_counter() - t0)
+            del st
+        ta = statistics.median(api)
+        line["e2e_api"] = {"value": n / ta, "unit": UNIT, "ms_per_step": ta * 1e3, "steps": len(api),
+                           "h2d_bytes_per_step": n * sym_bytes, "d2h_bytes_per_step": code_width(sigma) * ((n + 63) // 64) * 8,
+                           "path": "paper_1702_07578_b200.build_structure(numpy text, sigma, kind, 'ps') -> "
+                                   "structure of BitVectors (pageable numpy in and out, node borders included), "
+                                   "one call at a time, median of 3"}
+
     if not args.no_cpu and rank == 0:
-        host_np = text[: min(n, args.cpu_sample)].cpu().numpy()
-        line["cpu_baseline"] = cpu_baseline(host_np, sigma, kind, min(n, args.cpu_sample))
+        sample = min(n, args.cpu_sample) if args.cpu_sample else n
+        host_np = text[:sample].cpu().numpy()
+        line["cpu_baseline"] = cpu_baseline(host_np, sigma, kind, sample)
         line["cpu_baseline"].pop("seconds_per_build", None)
 
     if rank == 0:

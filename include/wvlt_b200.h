@@ -115,6 +115,19 @@ int wvlt_build_host(const void* host_text, int sym_bytes, int64_t n, int64_t sig
                     void* workspace, size_t workspace_bytes, void* stream);
 
 /*
+ * wvlt_build_host plus the node borders (layout of wvlt_build_device's
+ * `borders`) copied to host_borders (int64[max(2^width - 2, 0)], may be NULL).
+ * With host_borders, dev_small must hold (2^(width+1) + width - 1) int64.
+ * This is the drop-in's call: the reference's structures expose the node
+ * borders (levelstats.interval_starts, levelstats.py:58-73, for the tree;
+ * wt2wm.interval_start_table, wt2wm.py:55-78, for the matrix).
+ */
+int wvlt_build_host_borders(const void* host_text, int sym_bytes, int64_t n, int64_t sigma, int kind,
+                            uint64_t* host_level_words, int64_t* host_zeros, int64_t* host_hist,
+                            int64_t* host_borders, void* dev_text, uint64_t* dev_level_words, void* dev_small,
+                            void* workspace, size_t workspace_bytes, void* stream);
+
+/*
  * `count` independent builds with host buffers (same sym_bytes, sigma and kind;
  * text i has ns[i] symbols), software-pipelined over three streams: the text of
  * build i+1 goes host->device while build i runs on `stream` and build i-1's
@@ -170,6 +183,24 @@ int wvlt_merge_levels_peer(uint64_t* dst_words, int64_t dst_row_words, int width
                            int64_t n_bits, const int64_t* bounds, const int64_t* bounds_off, const int64_t* src_starts,
                            const int32_t* src_ranks, const int64_t* task_off, const uint64_t* const* level_src,
                            int nranks, void* stream);
+
+/*
+ * The merge plan of wvlt_merge_levels_peer for every level and every owner, on
+ * the device, from the all-gathered per-rank build outputs (replaces
+ * construct._merge_plan, construct.py:516-543, and its host-side use in the
+ * domain-decomposed build, construct.py:490-507).  Rank r's row starts at
+ * rows + r * row_stride; its node borders (wvlt_build_device `borders` layout:
+ * level l at [2^l - 2, 2^(l+1) - 2), indexed by prefix) start at column
+ * borders_col.  local_ns[r] = rank r's symbol count.  Level l gets
+ * nranks * 2^l tasks ((group in interval order) x rank, group-major, empty
+ * tasks kept): task_off[l] = nranks (2^l - 1), bounds_off[l] = task_off[l] + l;
+ * bounds / src_starts / src_ranks must hold nranks (2^width - 1) + width,
+ * nranks (2^width - 1) and nranks (2^width - 1) entries, task_off width + 1 and
+ * bounds_off width.  All arrays are device memory; no host work.
+ */
+int wvlt_peer_plan(const int64_t* rows, int64_t row_stride, int64_t borders_col, const int64_t* local_ns, int nranks,
+                   int width, int kind, int64_t* bounds, int64_t* src_starts, int32_t* src_ranks, int64_t* bounds_off,
+                   int64_t* task_off, void* stream);
 
 /*
  * Rank/select directories of nvec bit vectors of `length` bits stored back to

@@ -352,3 +352,153 @@ void oracle_merge_bits(uint64_t* dst, int64_t word_lo, int64_t word_hi, int64_t 
     dst[wd] = acc;
   }
 }
+
+/* ------------------------------------------------------------------------
+ * construct.build_domain_decomposed (construct.py:437-513) with its
+ * _merge_plan (construct.py:516-543): p aligned slices (construct.py:199-211)
+ * each built independently by the inner algorithm (pc, or ps on one thread),
+ * the partial levels concatenated at the slices' word offsets, then every
+ * level merged by gather_bits over p destination word ranges
+ * (construct.py:214-217), one thread each.  inner: 0 = pc, 1 = ps.
+ * ------------------------------------------------------------------------ */
+typedef struct {
+  const void* text;
+  int sb, kind, inner, width;
+  int64_t sigma, lo, hi;
+  uint64_t* partial; /* width rows of nwords */
+  int64_t nwords;
+  int64_t* hist;     /* 2^width */
+  int rc;
+} dd_slice;
+
+static void* dd_slice_worker(void* arg) {
+  dd_slice* t = (dd_slice*)arg;
+  const int64_t m = t->hi - t->lo;
+  const int64_t mw = (m + 63) >> 6;
+  const void* piece = (const char*)t->text + (size_t)t->lo * t->sb;
+  uint64_t* w = (uint64_t*)calloc((size_t)(t->width * mw) + 1, 8);
+  int64_t* z = (int64_t*)calloc((size_t)t->width + 1, 8);
+  if (!w || !z) { t->rc = -1; free(w); free(z); return NULL; }
+  t->rc = t->inner == 0 ? oracle_build_pc(piece, t->sb, m, t->sigma, t->kind, w, z, t->hist)
+                        : oracle_build_ps(piece, t->sb, m, t->sigma, t->kind, 1, w, z);
+  if (!t->rc && t->inner != 0) t->rc = oracle_histogram(piece, t->sb, m, t->sigma, t->hist);
+  for (int l = 0; l < t->width && !t->rc; ++l)
+    memcpy(t->partial + (int64_t)l * t->nwords + (t->lo >> 6), w + (int64_t)l * mw, (size_t)mw * 8);
+  free(w);
+  free(z);
+  return NULL;
+}
+
+typedef struct {
+  uint64_t* dst;
+  const uint64_t* src;
+  const int64_t* bounds;
+  const int64_t* src_starts;
+  int64_t ntasks, w0, w1, n;
+} dd_merge;
+
+static void* dd_merge_worker(void* arg) {
+  dd_merge* t = (dd_merge*)arg;
+  if (t->w1 <= t->w0) return NULL;
+  /* t0 = searchsorted(bounds, 64 w0, side="right") - 1 (construct.py:503) */
+  int64_t lo = 0, hi = t->ntasks;
+  while (hi - lo > 1) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (t->bounds[mid] <= 64 * t->w0) lo = mid;
+    else hi = mid;
+  }
+  oracle_merge_bits(t->dst, t->w0, t->w1, t->n, t->bounds, t->src_starts, t->src, lo);
+  return NULL;
+}
+
+int oracle_build_dd(const void* text, int sb, int64_t n, int64_t sigma, int kind, int threads, int inner,
+                    uint64_t* level_words, int64_t* zeros) {
+  const int width = oracle_code_width(sigma);
+  const int64_t nwords = (n + 63) >> 6;
+  if (threads < 1) return -2;
+  if (width == 0) return 0;
+  memset(level_words, 0, (size_t)width * nwords * 8);
+  for (int l = 0; l < width; ++l) zeros[l] = 0;
+  if (n == 0) return 0; /* construct.py:457-458 */
+  const int p = threads;
+  const int64_t nb = 1ll << width;
+  uint64_t* partial = (uint64_t*)calloc((size_t)width * nwords + 1, 8);
+  int64_t* hists = (int64_t*)calloc((size_t)p * nb, 8);
+  dd_slice* sl = (dd_slice*)calloc((size_t)p, sizeof(dd_slice));
+  pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * p);
+  if (!partial || !hists || !sl || !th) return -1;
+  const int64_t per = (n + p - 1) / p;
+  const int64_t chunk = (per + SLICE_ALIGNMENT - 1) / SLICE_ALIGNMENT * SLICE_ALIGNMENT;
+  int nact = 0;
+  for (int c = 0; c < p; ++c) {
+    int64_t lo = c * chunk;
+    if (lo > n) lo = n;
+    int64_t hi = lo + chunk;
+    if (hi > n || c == p - 1) hi = n;
+    if (hi <= lo) continue;
+    dd_slice* t = &sl[nact++];
+    t->text = text; t->sb = sb; t->kind = kind; t->inner = inner; t->width = width; t->sigma = sigma;
+    t->lo = lo; t->hi = hi; t->partial = partial; t->nwords = nwords; t->hist = hists + (int64_t)(nact - 1) * nb;
+  }
+  for (int c = 0; c < nact; ++c) pthread_create(&th[c], NULL, dd_slice_worker, &sl[c]);
+  for (int c = 0; c < nact; ++c) pthread_join(th[c], NULL);
+  int rc = 0;
+  for (int c = 0; c < nact; ++c) rc = rc ? rc : sl[c].rc;
+  /* per-slice count chains: level l counts at chain[c][l] (fold of the histogram) */
+  int64_t* chain = (int64_t*)malloc((size_t)nact * (2 * nb) * 8); /* level l at offset 2^l - 1 */
+  int64_t* lens = (int64_t*)malloc((size_t)nact * nb * 8 + 8);
+  int64_t* src = (int64_t*)malloc((size_t)nact * nb * 8 + 8);
+  int64_t* bounds = (int64_t*)malloc(((size_t)nact * nb + 1) * 8);
+  dd_merge* mt = (dd_merge*)malloc(sizeof(dd_merge) * p);
+  if (!chain || !lens || !src || !bounds || !mt) rc = -1;
+  for (int c = 0; c < nact && !rc; ++c) {
+    int64_t* ch = chain + (int64_t)c * 2 * nb;
+    memcpy(ch + nb - 1, sl[c].hist, (size_t)nb * 8);
+    for (int l = width - 1; l >= 0; --l)
+      for (int64_t q = 0; q < (1ll << l); ++q)
+        ch[(1ll << l) - 1 + q] = ch[(2ll << l) - 1 + 2 * q] + ch[(2ll << l) - 1 + 2 * q + 1];
+  }
+  /* WM zero counts: sum over slices of the even (l+1)-prefix counts (construct.py:486-488) */
+  if (kind == KIND_WM && !rc)
+    for (int l = 0; l < width; ++l)
+      for (int c = 0; c < nact; ++c) {
+        const int64_t* cl = chain + (int64_t)c * 2 * nb + (2ll << l) - 1;
+        for (int64_t q = 0; q < (1ll << l); ++q) zeros[l] += cl[2 * q];
+      }
+  for (int l = width - 1; l >= 0 && !rc; --l) {
+    /* _merge_plan: prefixes in interval order, slices in text order inside */
+    int64_t k = 0;
+    const int64_t m = 1ll << l;
+    for (int64_t r = 0; r < m; ++r) {
+      const int64_t q = (kind == KIND_WM && l >= 2) ? (int64_t)rev_bits((uint64_t)r, l) : r;
+      for (int c = 0; c < nact; ++c) {
+        const int64_t* cl = chain + (int64_t)c * 2 * nb + (1ll << l) - 1;
+        const int64_t len = l == 0 ? sl[c].hi - sl[c].lo : cl[q];
+        if (len > 0) { lens[k] = len; src[k] = c; bounds[k] = q; ++k; }
+      }
+    }
+    /* local starts: per slice a running sum over the interval order */
+    int64_t* run = (int64_t*)calloc((size_t)nact, 8);
+    int64_t acc = 0;
+    for (int64_t t = 0; t < k; ++t) {
+      const int c = (int)src[t];
+      const int64_t s0 = sl[c].lo + run[c];
+      run[c] += lens[t];
+      src[t] = s0;
+      bounds[t] = acc;
+      acc += lens[t];
+    }
+    bounds[k] = acc;
+    free(run);
+    const uint64_t* srcw = partial + (int64_t)l * nwords;
+    uint64_t* dstw = level_words + (int64_t)l * nwords;
+    for (int c = 0; c < p; ++c) {
+      mt[c].dst = dstw; mt[c].src = srcw; mt[c].bounds = bounds; mt[c].src_starts = src; mt[c].ntasks = k;
+      mt[c].w0 = nwords * c / p; mt[c].w1 = nwords * (c + 1) / p; mt[c].n = n;
+      pthread_create(&th[c], NULL, dd_merge_worker, &mt[c]);
+    }
+    for (int c = 0; c < p; ++c) pthread_join(th[c], NULL);
+  }
+  free(chain); free(lens); free(src); free(bounds); free(mt); free(partial); free(hists); free(sl); free(th);
+  return rc;
+}

@@ -73,12 +73,16 @@ def _bind(L):
     L.wvlt_build_device.restype = i32
     L.wvlt_build_host.argtypes = [vp, i32, i64, i64, i32, vp, vp, vp, vp, vp, vp, vp, sz, vp]
     L.wvlt_build_host.restype = i32
+    L.wvlt_build_host_borders.argtypes = [vp, i32, i64, i64, i32, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]
+    L.wvlt_build_host_borders.restype = i32
     L.wvlt_build_host_batch.argtypes = [i32, vp, vp, i32, i64, i32, vp, vp, vp, vp, vp, sz, vp, sz, vp, vp, sz, vp]
     L.wvlt_build_host_batch.restype = i32
     L.wvlt_merge_bits.argtypes = [vp, i64, i64, i64, vp, vp, i64, vp, vp]
     L.wvlt_merge_bits.restype = i32
     L.wvlt_merge_levels_peer.argtypes = [vp, i64, i32, i64, i64, i64, vp, vp, vp, vp, vp, vp, i32, vp]
     L.wvlt_merge_levels_peer.restype = i32
+    L.wvlt_peer_plan.argtypes = [vp, i64, i64, vp, i32, i32, i32, vp, vp, vp, vp, vp, vp]
+    L.wvlt_peer_plan.restype = i32
     L.wvlt_last_launches.argtypes = []
     L.wvlt_last_launches.restype = i32
     L.wvlt_rank_select_workspace_bytes.argtypes = [i64, i64]

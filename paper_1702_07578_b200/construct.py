@@ -195,17 +195,24 @@ def _build(text, sigma: int, kind: str, threads: int = 1):
         if n and not host_checked and int(arr.max()) >= sigma:
             raise ValueError(f"symbols must lie in [0, {sigma})")
         levels = [BitVector(n) for _ in range(width)]
-        if kind == "wm":
-            return WaveletMatrix(n, sigma, levels, [0] * width)
-        return LevelWiseWaveletTree(n, sigma, levels)
+        st = WaveletMatrix(n, sigma, levels, [0] * width) if kind == "wm" else LevelWiseWaveletTree(n, sigma, levels)
+        st.borders = np.zeros(max((1 << width) - 2, 0), dtype=np.int64)  # every interval starts at 0
+        st.histogram = np.zeros(1 << width, dtype=np.int64)
+        if n:
+            st.histogram[0] = n
+        return st
     from .device import default_builder
 
     dev_arr = _device_text(arr, sigma)
     _note_device_build(n, dev_arr.dtype.itemsize, sigma, kind)
-    # the WT build computes the histogram anyway (its placement tables need it)
-    words, zeros, hist = default_builder().build_host(dev_arr, sigma, kind, histogram=kind == "wt")
+    # the WT build computes the histogram anyway (its placement tables need it);
+    # the node borders come with every build (byte texts: from the same tables;
+    # wider alphabets: from the group recurrence over the matrix levels)
+    words, zeros, hist, borders = default_builder().build_host_ex(dev_arr, sigma, kind, histogram=kind == "wt",
+                                                                  borders=True)
     st = wrap(kind, n, sigma, words, zeros)
     st.histogram = hist
+    st.borders = borders
     return st
 
 

@@ -394,7 +394,7 @@ int build_k16(const uint16_t* src, int64_t n, int W, uint64_t* level_words, int6
   scan8_chunks_kernel<<<(unsigned)L.nchunks, nb, 0, s>>>(tcnt8, L.ntiles, nb, chunk);
   scan8_carry_kernel<<<nb, S8_SCAN_THREADS, 0, s>>>(chunk, L.nchunks, nb, totals);
   scan8_apply_kernel<<<(unsigned)L.nchunks, nb, 0, s>>>(tcnt8, L.ntiles, nb, chunk, tpre8);
-  tables8_kernel<<<1, 256, 0, s>>>(totals, W, WVLT_KIND_WM, base, zeros, nullptr, baseW);
+  tables8_kernel<<<1, 256, 0, s>>>(totals, W, WVLT_KIND_WM, base, zeros, nullptr, baseW, nullptr);
   g_launches += 4;
   e = cudaGetLastError();
   if (e != cudaSuccess) return (int)e;

@@ -295,7 +295,9 @@ __global__ void __launch_bounds__(256) scan8_apply_kernel(const uint32_t* __rest
 // base[j * 256 + d], 1 <= j < W, d < 2^j an LSD digit: where the group of d
 // starts in level j (WM: exclusive prefix of the group sizes in LSD-digit
 // order; WT: interval start of the numeric prefix rev(d)).  Also the zero
-// counts per level and (optionally) the histogram.
+// counts per level and (optionally) the histogram and the node borders (level
+// j at [2^j - 2, 2^(j+1) - 2) indexed by the numeric j-bit prefix: WT interval
+// starts, levelstats.py:58-73; WM group starts, wt2wm.py:55-78).
 // exclusive scan of get(i), i < cnt <= 256, by one warp (8 entries per lane), written through put
 template <typename Get, typename Put>
 __device__ __forceinline__ void warp_scan_excl64(int cnt, int lane, Get get, Put put) {
@@ -327,7 +329,8 @@ __device__ __forceinline__ void warp_scan_excl64(int cnt, int lane, Get get, Put
 // scans the sizes into group starts (warp 7: the WM level-W starts).
 __global__ void __launch_bounds__(256) tables8_kernel(const int64_t* __restrict__ totals, int W, int kind,
                                                       int64_t* __restrict__ base, int64_t* __restrict__ zeros,
-                                                      int64_t* __restrict__ hist, int64_t* __restrict__ baseW) {
+                                                      int64_t* __restrict__ hist, int64_t* __restrict__ baseW,
+                                                      int64_t* __restrict__ borders) {
   __shared__ uint32_t s_tot[256];
   __shared__ uint32_t s_cnt[9][256];  // level j: WM by LSD digit, WT by numeric prefix
   __shared__ uint32_t s_z[8][8];      // [warp][level] partial zero counts
@@ -361,12 +364,17 @@ __global__ void __launch_bounds__(256) tables8_kernel(const int64_t* __restrict_
   const int j = wid + 1;  // warp j - 1: level j
   if (j < W) {
     const uint32_t* c = s_cnt[j];
+    int64_t* bj = borders ? borders + ((1 << j) - 2) : nullptr;
     if (kind == WVLT_KIND_WM)
-      warp_scan_excl64(1 << j, lane, [&](int d) { return (int64_t)c[d]; },
-                       [&](int d, int64_t v) { base[j * 256 + d] = v; });
+      warp_scan_excl64(1 << j, lane, [&](int d) { return (int64_t)c[d]; }, [&](int d, int64_t v) {
+        base[j * 256 + d] = v;
+        if (bj) bj[rev_bits((unsigned)d, j)] = v;  // digit d = bit-reversed prefix
+      });
     else
-      warp_scan_excl64(1 << j, lane, [&](int P) { return (int64_t)c[P]; },
-                       [&](int P, int64_t v) { base[j * 256 + rev_bits((unsigned)P, j)] = v; });
+      warp_scan_excl64(1 << j, lane, [&](int P) { return (int64_t)c[P]; }, [&](int P, int64_t v) {
+        base[j * 256 + rev_bits((unsigned)P, j)] = v;
+        if (bj) bj[P] = v;
+      });
   } else if (wid == 7 && baseW) {  // WM level-W group starts (the 2-byte pass's output order)
     warp_scan_excl64(nb, lane, [&](int d) { return (int64_t)s_tot[rev_bits((unsigned)d, W)]; },
                      [&](int d, int64_t v) { baseW[d] = v; });
@@ -831,7 +839,7 @@ inline K8Layout k8_layout(int64_t n, int w) {
 
 // The whole single-pass build (called by build_device_impl).
 int build_k8(const uint8_t* text, int64_t n, int64_t sigma, int w, int kind, uint64_t* level_words,
-             int64_t* zeros, int64_t* hist, void* workspace, int32_t* status, cudaStream_t s,
+             int64_t* zeros, int64_t* hist, int64_t* borders, void* workspace, int32_t* status, cudaStream_t s,
              void (*pass_done)(void*, int, int), void* ctx, int lvl0, int tail_pass) {
   const K8Layout L = k8_layout(n, w);
   const int nb = 1 << w;
@@ -878,7 +886,7 @@ int build_k8(const uint8_t* text, int64_t n, int64_t sigma, int w, int kind, uin
   e = cudaGetLastError();
   if (e != cudaSuccess) return (int)e;
   if (!tail) prof_mark(s, WVLT_STAGE_SCAN0);
-  tables8_kernel<<<1, 256, 0, s>>>(totals, w, kind, base, zeros, hist, nullptr);
+  tables8_kernel<<<1, 256, 0, s>>>(totals, w, kind, base, zeros, hist, nullptr, borders);
   ++g_launches;
   Pass8Args a;
   a.src = text;

@@ -1780,6 +1780,53 @@ __global__ void __launch_bounds__(256) merge_peer_kernel(uint64_t* __restrict__ 
   }
 }
 
+// Merge plan of the sharded build on the device (construct._merge_plan,
+// construct.py:516-543, for every level at once): level l's pieces are the
+// (group q in interval order, rank r) pairs, group-major -- R 2^l tasks, empty
+// ones kept (the merge kernels skip them).  Everything is elementwise given
+// every rank's node borders B_r (its local group starts, indexed by prefix):
+// a piece's source start is B_r(P), its length B_r(P') - B_r(P) (P' the next
+// group in interval order; the rank's symbol count after the last), and its
+// destination start sum_r' B_r'(P) + the lengths of the lower ranks' pieces of
+// the group.  Level 0 is one group.  One thread per (level, group).
+__global__ void peer_plan_kernel(const int64_t* __restrict__ rows, int64_t row_stride, int64_t borders_col,
+                                 const int64_t* __restrict__ local_ns, int R, int w, int kind,
+                                 int64_t* __restrict__ bounds, int64_t* __restrict__ starts,
+                                 int32_t* __restrict__ ranks, int64_t* __restrict__ bounds_off,
+                                 int64_t* __restrict__ task_off) {
+  const int64_t items = (1ll << w) - 1;  // sum over levels of 2^l
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gtid <= w) {  // closed-form offsets: level l has R 2^l tasks and R 2^l + 1 bounds
+    task_off[gtid] = (int64_t)R * ((1ll << gtid) - 1);
+    if (gtid < w) bounds_off[gtid] = (int64_t)R * ((1ll << gtid) - 1) + gtid;
+  }
+  for (int64_t i = gtid; i < items; i += (int64_t)gridDim.x * blockDim.x) {
+    const int l = 63 - __clzll(i + 1);
+    const int64_t q = i + 1 - (1ll << l);
+    const int64_t ng = 1ll << l;
+    const bool last = q + 1 == ng;
+    const bool rev = kind == WVLT_KIND_WM && l >= 2;
+    const int64_t P = rev ? (int64_t)rev_bits((unsigned)q, l) : q;
+    const int64_t Pn = last ? 0 : (rev ? (int64_t)rev_bits((unsigned)(q + 1), l) : q + 1);
+    int64_t g = 0;
+    for (int r = 0; r < R; ++r) g += l ? rows[r * row_stride + borders_col + (1ll << l) - 2 + P] : 0;
+    int64_t* bl = bounds + (int64_t)R * ((1ll << l) - 1) + l;
+    int64_t* sl = starts + (int64_t)R * ((1ll << l) - 1);
+    int32_t* rl = ranks + (int64_t)R * ((1ll << l) - 1);
+    int64_t run = g;
+    for (int r = 0; r < R; ++r) {
+      const int64_t* br = rows + r * row_stride + borders_col + (1ll << l) - 2;
+      const int64_t st = l ? br[P] : 0;
+      const int64_t en = (l && !last) ? br[Pn] : local_ns[r];
+      bl[q * R + r] = run;
+      sl[q * R + r] = st;
+      rl[q * R + r] = r;
+      run += en - st;
+    }
+    if (last) bl[(int64_t)R * ng] = run;  // = n
+  }
+}
+
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
@@ -2254,14 +2301,16 @@ struct WtViaWm {
   int64_t nblk, nchunk;
 };
 
-inline bool wt_via_wm_layout(int64_t n, int sym_bytes, int64_t sigma, WtViaWm* L) {
+// kind WT: the matrix goes to a temporary and is reordered into the tree;
+// kind WM (histogram / borders requested): the matrix is the output itself.
+inline bool wt_via_wm_layout(int64_t n, int sym_bytes, int64_t sigma, int kind, WtViaWm* L) {
   Plan P;
   if (!make_plan(n, sym_bytes, sigma, WVLT_KIND_WM, &P, true) || !P.tail_w) return false;
   const int w = P.width;
   const int64_t nwords = (n + 63) >> 6;
   size_t off = 0;
   L->off_temp = off;
-  off = align_up(off + (size_t)w * nwords * 8, 256);
+  if (kind == WVLT_KIND_WT) off = align_up(off + (size_t)w * nwords * 8, 256);
   L->off_zeros = off;
   off = align_up(off + (size_t)w * 8, 256);
   L->off_chain = off;
@@ -2281,19 +2330,35 @@ inline bool wt_via_wm_layout(int64_t n, int sym_bytes, int64_t sigma, WtViaWm* L
   return true;
 }
 
-int build_wt_via_wm(const void* text, int sym_bytes, int64_t n, int64_t sigma, uint64_t* level_words, int64_t* zeros,
-                    int64_t* hist, unsigned char* ws, const WtViaWm& L, int32_t* status, cudaStream_t s,
-                    void (*pass_done)(void*, int, int), void* ctx) {
+// node borders of levels 1..w-1 (layout of wvlt_build_device) from the group
+// recurrence's tables: WT interval starts (bounds, level k at chain_off(k) + k)
+// or WM group starts (wmst, level k at chain_off(k)), both indexed by prefix
+__global__ void borders_copy_kernel(const int64_t* __restrict__ src, int w, int wt, int64_t* __restrict__ out) {
+  const int64_t total = (1ll << w) - 2;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int k = 63 - __clzll(i + 2);
+    const int64_t P = i + 2 - (1ll << k);
+    out[i] = src[chain_off(k) + (wt ? k : 0) + P];
+  }
+}
+
+// Wide alphabets (w > 8) through the fused matrix build: kind WT reorders the
+// matrix into the tree; both kinds take the histogram and the node borders
+// from the group recurrence over the matrix levels (no pass over the text).
+int build_wt_via_wm(int kind, const void* text, int sym_bytes, int64_t n, int64_t sigma, uint64_t* level_words,
+                    int64_t* zeros, int64_t* hist, int64_t* borders, unsigned char* ws, const WtViaWm& L,
+                    int32_t* status, cudaStream_t s, void (*pass_done)(void*, int, int), void* ctx) {
   const int w = code_width_host(sigma);
   const int64_t nwords = (n + 63) >> 6;
-  uint64_t* temp = (uint64_t*)(ws + L.off_temp);
+  const bool wt = kind == WVLT_KIND_WT;
+  uint64_t* temp = wt ? (uint64_t*)(ws + L.off_temp) : level_words;
   int64_t* chain = (int64_t*)(ws + L.off_chain);
   int64_t* bounds = (int64_t*)(ws + L.off_bounds);
   int64_t* wmst = (int64_t*)(ws + L.off_wm);
   // the matrix (its kernels check the symbol range; a level's zero count is the
   // same in both layouts)
   int rc = build_device_impl(text, sym_bytes, n, sigma, WVLT_KIND_WM, temp, zeros ? zeros : (int64_t*)(ws + L.off_zeros), nullptr,
-                             nullptr, ws + L.off_ws, L.total - L.off_ws, status, s, nullptr, nullptr);
+                             nullptr, ws + L.off_ws, L.total - L.off_ws, status, s, wt ? nullptr : pass_done, ctx);
   if (rc) return rc;
   int launches = g_launches;
   cudaError_t e;
@@ -2324,6 +2389,19 @@ int build_wt_via_wm(const void* text, int sym_bytes, int64_t n, int64_t sigma, u
   }
   e = cudaGetLastError();
   if (e != cudaSuccess) return (int)e;
+  if (borders && w >= 2) {
+    borders_copy_kernel<<<(unsigned)std::min<int64_t>((((1ll << w) - 2) + 255) / 256, (int64_t)sm_count() * 8), 256, 0,
+                          s>>>(wt ? bounds : wmst, w, wt ? 1 : 0, borders);
+    ++launches;
+  }
+  if (!wt) {
+    if (hist) {
+      e = cudaMemcpyAsync(hist, chain + chain_off(w), ((size_t)1 << w) * 8, cudaMemcpyDeviceToDevice, s);
+      if (e != cudaSuccess) return (int)e;
+    }
+    g_launches = launches;
+    return (int)cudaGetLastError();
+  }
   // levels 0 and 1 are identical; the others are reordered group by group
   e = cudaMemcpyAsync(level_words, temp, (size_t)std::min(w, 2) * nwords * 8, cudaMemcpyDeviceToDevice, s);
   if (e != cudaSuccess) return (int)e;
@@ -2401,8 +2479,7 @@ size_t wvlt_workspace_bytes(int64_t n, int sym_bytes, int64_t sigma, int kind) {
   make_plan(n, sym_bytes, sigma, kind, &P2, false);
   size_t total = std::max(P.total, P2.total);
   WtViaWm L;
-  if (kind == WVLT_KIND_WT && P.width > 8 && n > 0 && wt_via_wm_layout(n, sym_bytes, sigma, &L))
-    total = std::max(total, L.total);
+  if (P.width > 8 && n > 0 && wt_via_wm_layout(n, sym_bytes, sigma, kind, &L)) total = std::max(total, L.total);
   if (k8_eligible(sym_bytes, P.width, n) && !P.widen_bytes) return std::max(total, k8_layout(n, P.width).total);
   return total;
 }
@@ -2451,12 +2528,12 @@ int build_device_impl(const void* text, int sym_bytes, int64_t n, int64_t sigma,
     if (e != cudaSuccess) return (int)e;
   }
   const int64_t nwords = (n + 63) >> 6;
-  if (kind == WVLT_KIND_WT && !borders && n > 0 && w > 8 && text && level_words && workspace) {
+  if ((kind == WVLT_KIND_WT || !lean) && n > 0 && w > 8 && text && level_words && workspace) {
     WtViaWm L;
-    if (wt_via_wm_layout(n, sym_bytes, sigma, &L)) {
+    if (wt_via_wm_layout(n, sym_bytes, sigma, kind, &L)) {
       if (workspace_bytes < L.total) return WVLT_E_WORKSPACE;
-      return build_wt_via_wm(text, sym_bytes, n, sigma, level_words, zeros, hist, (unsigned char*)workspace, L, status,
-                             s, pass_done, ctx);
+      return build_wt_via_wm(kind, text, sym_bytes, n, sigma, level_words, zeros, hist, borders,
+                             (unsigned char*)workspace, L, status, s, pass_done, ctx);
     }
   }
   if (n == 0 || w == 0) {
@@ -2484,10 +2561,10 @@ int build_device_impl(const void* text, int sym_bytes, int64_t n, int64_t sigma,
     return 0;
   }
   if (!text || !level_words || !workspace) return WVLT_E_ARG;
-  if (k8_eligible(sym_bytes, w, n) && !borders && !P.widen_bytes) {
+  if (k8_eligible(sym_bytes, w, n) && !P.widen_bytes) {
     // byte text, 2 <= w <= 8: every level in one fused pass (k8.cuh)
     if (workspace_bytes < k8_layout(n, w).total) return WVLT_E_WORKSPACE;
-    return build_k8((const uint8_t*)text, n, sigma, w, kind, level_words, zeros, hist, workspace, status, s,
+    return build_k8((const uint8_t*)text, n, sigma, w, kind, level_words, zeros, hist, borders, workspace, status, s,
                     pass_done, ctx, 0, -1);
   }
   if (workspace_bytes < P.total) return WVLT_E_WORKSPACE;
@@ -2650,7 +2727,7 @@ int build_device_impl(const void* text, int sym_bytes, int64_t n, int64_t sigma,
   if (P.tail_w) {
     const int64_t lt = P.tail_lvl;
     return build_k8((const uint8_t*)cur, n, (int64_t)1 << P.tail_w, P.tail_w, kind, level_words + lt * nwords,
-                    zeros ? zeros + lt : nullptr, nullptr, bufs[curbuf == 0 ? 1 : 0], st_flag, s, pass_done, ctx,
+                    zeros ? zeros + lt : nullptr, nullptr, nullptr, bufs[curbuf == 0 ? 1 : 0], st_flag, s, pass_done, ctx,
                     (int)lt, stage);
   }
   return 0;
@@ -2795,10 +2872,10 @@ void host_copy_pass(void* c, int l0, int K) {
 
 extern "C" {
 
-int wvlt_build_host(const void* host_text, int sym_bytes, int64_t n, int64_t sigma, int kind,
-                    uint64_t* host_level_words, int64_t* host_zeros, int64_t* host_hist, void* dev_text,
-                    uint64_t* dev_level_words, void* dev_small, void* workspace, size_t workspace_bytes,
-                    void* stream) {
+int wvlt_build_host_borders(const void* host_text, int sym_bytes, int64_t n, int64_t sigma, int kind,
+                            uint64_t* host_level_words, int64_t* host_zeros, int64_t* host_hist,
+                            int64_t* host_borders, void* dev_text, uint64_t* dev_level_words, void* dev_small,
+                            void* workspace, size_t workspace_bytes, void* stream) {
   if (!(sym_bytes == 1 || sym_bytes == 2 || sym_bytes == 4) || n < 0 || sigma < 1) return WVLT_E_ARG;
   const int w = code_width_host(sigma);
   if (w > WVLT_MAX_WIDTH) return WVLT_E_WIDTH;
@@ -2809,6 +2886,7 @@ int wvlt_build_host(const void* host_text, int sym_bytes, int64_t n, int64_t sig
   int32_t* dstatus = (int32_t*)small;
   int64_t* dzeros = small + 1;
   int64_t* dhist = small + 1 + w;
+  int64_t* dborders = (host_borders && w >= 2) ? small + 1 + w + ((int64_t)1 << w) : nullptr;
   const int64_t nwords = (n + 63) >> 6;
   if (w > 0 && nwords > 0 && !host_level_words) return WVLT_E_ARG;
   // pageable level words: no per-pass streaming, one staged download at the end;
@@ -2851,7 +2929,7 @@ int wvlt_build_host(const void* host_text, int sym_bytes, int64_t n, int64_t sig
   hc.nwords = (w > 0) ? nwords : 0;
   hc.err = cudaSuccess;
   int rc = build_device_impl(dev_text, sym_bytes, n, sigma, kind, dev_level_words, dzeros, host_hist ? dhist : nullptr,
-                             nullptr, workspace, workspace_bytes, dstatus, s, words_pinned ? host_copy_pass : nullptr,
+                             dborders, workspace, workspace_bytes, dstatus, s, words_pinned ? host_copy_pass : nullptr,
                              &hc);
   if (rc) {
     cudaStreamSynchronize(copy_stream);
@@ -2877,11 +2955,23 @@ int wvlt_build_host(const void* host_text, int sym_bytes, int64_t n, int64_t sig
     e = cudaMemcpyAsync(host_hist, dhist, ((size_t)1 << w) * 8, cudaMemcpyDeviceToHost, s);
     if (e != cudaSuccess) return (int)e;
   }
+  if (dborders) {
+    e = cudaMemcpyAsync(host_borders, dborders, (((size_t)1 << w) - 2) * 8, cudaMemcpyDeviceToHost, s);
+    if (e != cudaSuccess) return (int)e;
+  }
   e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) return (int)e;
   e = cudaStreamSynchronize(copy_stream);
   if (e != cudaSuccess) return (int)e;
   return (hstatus & WVLT_STATUS_RANGE) ? WVLT_E_RANGE : 0;
+}
+
+int wvlt_build_host(const void* host_text, int sym_bytes, int64_t n, int64_t sigma, int kind,
+                    uint64_t* host_level_words, int64_t* host_zeros, int64_t* host_hist, void* dev_text,
+                    uint64_t* dev_level_words, void* dev_small, void* workspace, size_t workspace_bytes,
+                    void* stream) {
+  return wvlt_build_host_borders(host_text, sym_bytes, n, sigma, kind, host_level_words, host_zeros, host_hist,
+                                 nullptr, dev_text, dev_level_words, dev_small, workspace, workspace_bytes, stream);
 }
 
 // A sequence of independent builds with host buffers, software-pipelined over
@@ -3039,6 +3129,19 @@ int wvlt_merge_levels_peer(uint64_t* dst_words, int64_t dst_row_words, int width
   merge_peer_kernel<<<dim3((unsigned)blocks, (unsigned)width), 256, 0, (cudaStream_t)stream>>>(
       dst_words, dst_row_words, word_lo, word_hi, n_bits, bounds, bounds_off, src_starts, src_ranks, task_off,
       level_src, nranks);
+  return (int)cudaGetLastError();
+}
+
+int wvlt_peer_plan(const int64_t* rows, int64_t row_stride, int64_t borders_col, const int64_t* local_ns, int nranks,
+                   int width, int kind, int64_t* bounds, int64_t* src_starts, int32_t* src_ranks, int64_t* bounds_off,
+                   int64_t* task_off, void* stream) {
+  if (nranks < 1 || width < 0 || width > WVLT_MAX_WIDTH || (kind != WVLT_KIND_WT && kind != WVLT_KIND_WM))
+    return WVLT_E_ARG;
+  if (!rows || !local_ns || !bounds || !src_starts || !src_ranks || !bounds_off || !task_off) return WVLT_E_ARG;
+  const int64_t items = std::max<int64_t>((1ll << width) - 1, width + 1);
+  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((items + 255) / 256, (int64_t)sm_count() * 8));
+  peer_plan_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(rows, row_stride, borders_col, local_ns, nranks, width,
+                                                             kind, bounds, src_starts, src_ranks, bounds_off, task_off);
   return (int)cudaGetLastError();
 }
 

@@ -158,7 +158,8 @@ class DeviceBuilder:
             raise ValueError(f"symbols must lie in [0, {sigma})")
         return DeviceBuild(kind, n, sigma, w, lw, zeros, hist if histogram else None, bd, status)
 
-    def capture(self, text, sigma: int, kind: str = "wm", *, histogram: bool = False) -> "BuildGraph":
+    def capture(self, text, sigma: int, kind: str = "wm", *, histogram: bool = False,
+                borders: bool = False) -> "BuildGraph":
         """Capture one build of ``text`` (a device tensor kept as the graph's input
         buffer) into a CUDA graph: small, launch-bound builds replay it with one
         launch.  Refill ``text`` in place and call ``replay()`` for the next build
@@ -173,14 +174,14 @@ class DeviceBuilder:
         n = int(text.numel())
         need = self.workspace_bytes(n, text.element_size(), sigma, kind)
         with torch.cuda.stream(s):
-            outputs = self.alloc_outputs(n, sigma)
+            outputs = self.alloc_outputs(n, sigma, borders)
             ws = torch.empty(max(need, 256), dtype=torch.uint8, device=self.device)
-            self.build(text, sigma, kind, histogram=histogram, outputs=outputs, stream=s, check=False,
-                       workspace=ws)  # warm-up
+            self.build(text, sigma, kind, histogram=histogram, borders=borders, outputs=outputs, stream=s,
+                       check=False, workspace=ws)  # warm-up
         s.synchronize()
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=s):
-            res = self.build(text, sigma, kind, histogram=histogram, outputs=outputs,
+            res = self.build(text, sigma, kind, histogram=histogram, borders=borders, outputs=outputs,
                              stream=torch.cuda.current_stream(self.device), check=False, workspace=ws)
         return BuildGraph(g, res, text, ws)
 
@@ -192,6 +193,14 @@ class DeviceBuilder:
         full PCIe bandwidth).  Returns (level_words uint64[w, ceil(n/64)], zeros,
         hist or None).
         """
+        words, zeros, hist, _ = self.build_host_ex(arr, sigma, kind, out_words=out_words, histogram=histogram,
+                                                   borders=False, stream=stream)
+        return words, zeros, hist
+
+    def build_host_ex(self, arr: np.ndarray, sigma: int, kind: str, *, out_words: np.ndarray | None = None,
+                      histogram: bool = False, borders: bool = False, stream=None):
+        """``build_host`` that can also return the node borders (wvlt_build_host_borders):
+        (level_words, zeros, hist or None, borders int64[2^w - 2] or None)."""
         torch = _torch()
         if arr.dtype not in (np.uint8, np.uint16, np.uint32) or not arr.flags.c_contiguous:
             raise ValueError("host text must be a contiguous uint8/uint16/uint32 array")
@@ -203,21 +212,23 @@ class DeviceBuilder:
             out_words = np.empty((w, nwords), dtype=np.uint64)
         zeros = np.zeros(max(w, 1), dtype=np.int64)
         hist = np.zeros(1 << w, dtype=np.int64)
+        bd = np.zeros(max((1 << w) - 2, 1), dtype=np.int64)
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
         with torch.cuda.stream(s):
             dev_text = torch.empty(max(n * sb, 16), dtype=torch.uint8, device=self.device)
             dev_words = torch.empty(max(w * nwords, 1), dtype=torch.int64, device=self.device)
-            dev_small = torch.empty((1 << w) + w + 1, dtype=torch.int64, device=self.device)
+            dev_small = torch.empty((2 << w) + w + 1, dtype=torch.int64, device=self.device)
         ws, need = self.workspace(n, sb, sigma, kind, s)
-        rc = self.lib.wvlt_build_host(
+        rc = self.lib.wvlt_build_host_borders(
             arr.ctypes.data if n else None, sb, n, sigma, _lib.KINDS[kind],
             out_words.ctypes.data if out_words.size else None, zeros.ctypes.data,
-            hist.ctypes.data if histogram else None,
+            hist.ctypes.data if histogram else None, bd.ctypes.data if borders else None,
             dev_text.data_ptr(), dev_words.data_ptr(), dev_small.data_ptr(), ws.data_ptr(), need, s.cuda_stream)
         if rc == _lib.E_RANGE:
             raise ValueError(f"symbols must lie in [0, {sigma})")
         _lib.check(rc)
-        return out_words, [int(z) for z in zeros[:w]], (hist if histogram else None)
+        return (out_words, [int(z) for z in zeros[:w]], (hist if histogram else None),
+                (bd[: max((1 << w) - 2, 0)] if borders else None))
 
     def build_host_batch(self, arrs, sigma: int, kind: str, *, out_words=None, histogram: bool = False,
                          stream=None):

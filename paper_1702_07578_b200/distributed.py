@@ -207,8 +207,40 @@ def merge_peer_host(arrays, sources, word_lo: int, word_hi: int, n: int, width: 
     return out
 
 
+def plan_from_borders_host(rows_borders, local_ns, kind: str, width: int):
+    """Host restatement of the device plan (wvlt_peer_plan, test checker): every
+    level's (group in interval order, rank) pieces from the ranks' node borders.
+    rows_borders[r] is rank r's borders array (wvlt_build_device layout).
+    Returns (bounds, bounds_off, starts, ranks, task_off) like owner_plan_arrays,
+    but uncut and with empty pieces kept."""
+    R = len(local_ns)
+    bounds, starts, ranks = [], [], []
+    for ell in range(width):
+        ng = 1 << ell
+        if ell == 0:
+            st = np.zeros((1, R), dtype=np.int64)
+            ln = np.asarray(local_ns, dtype=np.int64).reshape(1, R)
+        else:
+            order = bit_reversal_permutation(ell) if (kind == "wm" and ell >= 2) else np.arange(ng)
+            blk = np.stack([np.asarray(rows_borders[r], dtype=np.int64)[(1 << ell) - 2: (1 << (ell + 1)) - 2]
+                            for r in range(R)], axis=1)  # [prefix, rank]
+            st = blk[order]                                # [interval order, rank]
+            nxt = np.vstack([st[1:], np.asarray(local_ns, dtype=np.int64).reshape(1, R)])
+            ln = nxt - st
+        g = st.sum(axis=1, keepdims=True)
+        within = np.cumsum(ln, axis=1) - ln
+        b = (g + within).reshape(-1)
+        bounds.append(np.concatenate([b, [int(np.sum(local_ns))]]))
+        starts.append(st.reshape(-1))
+        ranks.append(np.tile(np.arange(R, dtype=np.int32), ng))
+    task_off = np.array([R * ((1 << ell) - 1) for ell in range(width + 1)], dtype=np.int64)
+    bounds_off = np.array([R * ((1 << ell) - 1) + ell for ell in range(width)], dtype=np.int64)
+    cat = lambda xs, dt: np.concatenate(xs).astype(dt) if xs else np.zeros(1, dtype=dt)  # noqa: E731
+    return cat(bounds, np.int64), bounds_off, cat(starts, np.int64), cat(ranks, np.int32), task_off
+
+
 def build_sharded(local_text, sigma: int, kind: str = "wm", group=None, *, ops=None, gather: bool = False,
-                  transport: str = "nccl"):
+                  transport: str = "nccl", comm_device=None):
     """Sharded build over the ranks of ``group`` (default: the world group).
 
     Every rank passes its own contiguous shard of the text (rank order = text
@@ -218,9 +250,14 @@ def build_sharded(local_text, sigma: int, kind: str = "wm", group=None, *, ops=N
 
     ``transport``: "nccl" moves the needed bit segments with one all_to_all and
     shift-merges them (wvlt_merge_bits); "p2p" builds every rank's local levels in
-    symmetric (peer-mapped) memory and lets each owner assemble its words straight
-    from the peers' levels in one kernel (wvlt_merge_levels_peer) -- the exchange
-    fused into the merge, no staging copy.
+    peer-mapped memory and lets each owner assemble its words straight from the
+    peers' levels in one kernel (wvlt_merge_levels_peer) -- the exchange fused
+    into the merge, no staging copy.  The p2p merge plan is computed on the
+    device from the all-gathered node borders (wvlt_peer_plan): no host planning.
+
+    ``comm_device``: where the collectives' tensors live (default: the build
+    device).  "cpu" stages them through host memory, for a gloo group (the
+    one-GPU multi-process tests); the builds and merges stay on the GPU.
     """
     import torch
     import torch.distributed as dist
@@ -234,34 +271,34 @@ def build_sharded(local_text, sigma: int, kind: str = "wm", group=None, *, ops=N
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     dev = ops.device
+    cdev = torch.device(comm_device) if comm_device is not None else dev
     width = code_width(sigma)
 
     n_local = int(local_text.numel() if hasattr(local_text, "numel") else np.asarray(local_text).size)
-    ns = torch.zeros(world, dtype=torch.int64, device=dev)
-    mine = torch.tensor([n_local], dtype=torch.int64, device=dev)
+    ns = torch.zeros(world, dtype=torch.int64, device=cdev)
+    mine = torch.tensor([n_local], dtype=torch.int64, device=cdev)
     dist.all_gather_into_tensor(ns, mine, group=group)
     local_ns = [int(v) for v in ns.cpu().tolist()]
     n = sum(local_ns)
 
     if transport not in ("nccl", "p2p"):
         raise ValueError(f"unknown transport {transport!r}")
-    peer = None
-    # 1. local build (no communication)
+    total_words = (n + 63) >> 6
+    ranges = word_ranges(total_words, world)
+    w0, w1 = ranges[rank]
     if transport == "p2p" and width > 0:
-        # local levels in symmetric memory: every rank's buffer mapped into every peer
-        lnws = [(v + 63) >> 6 for v in local_ns]
-        hdl, buf = ops.peer_buffer(width * max(lnws), group)
-        peer = (hdl, buf, lnws)
-        words, hist, bad = ops.local_build(local_text, sigma, kind, out_words=buf[: width * lnws[rank]])
-    else:
-        words, hist, bad = ops.local_build(local_text, sigma, kind)
+        return _build_sharded_p2p(local_text, sigma, kind, group, ops, gather, local_ns, ns, n, rank, world, ranges,
+                                  cdev)
+
+    # 1. local build (no communication)
+    words, hist, bad = ops.local_build(local_text, sigma, kind)
     # 2. histograms (+ each rank's range flag) -> plan: one all_gather, one host read
     if torch.is_tensor(bad):
-        flag = (bad.reshape(-1)[:1].to(device=dev, dtype=torch.int64) & 1)
+        flag = (bad.reshape(-1)[:1].to(device=cdev, dtype=torch.int64) & 1)
     else:
-        flag = torch.tensor([1 if bad else 0], dtype=torch.int64, device=dev)
-    mine_h = torch.cat([hist.reshape(-1).to(device=dev, dtype=torch.int64), flag])
-    allh = torch.empty((world, (1 << width) + 1), dtype=torch.int64, device=dev)
+        flag = torch.tensor([1 if bad else 0], dtype=torch.int64, device=cdev)
+    mine_h = torch.cat([hist.reshape(-1).to(device=cdev, dtype=torch.int64), flag])
+    allh = torch.empty((world, (1 << width) + 1), dtype=torch.int64, device=cdev)
     dist.all_gather_into_tensor(allh, mine_h.reshape(1, -1), group=group)
     gathered = allh.cpu().numpy()
     if gathered[:, -1].any():
@@ -269,29 +306,10 @@ def build_sharded(local_text, sigma: int, kind: str = "wm", group=None, *, ops=N
     hists = np.ascontiguousarray(gathered[:, :-1])
     ghist = hists.sum(axis=0)
     zeros = zeros_from_hist(ghist, width) if width else []
-    total_words = (n + 63) >> 6
-    ranges = word_ranges(total_words, world)
-    w0, w1 = ranges[rank]
     # the merge kernels write every owned word (padding bits included)
     owned = torch.empty((width, max(w1 - w0, 0)), dtype=torch.int64, device=dev)
     if width == 0 or n == 0:
         return ShardedResult(n, sigma, kind, width, w0, w1, owned, zeros, ghist)
-    if peer is not None:
-        # 3+4. one kernel per owner reads the peers' local levels directly.  The
-        # histogram all_gather above is stream-ordered after every rank's local
-        # build, so the peers' levels are complete once it has finished here.
-        hdl, buf, lnws = peer
-        arrays = owner_plan_arrays(hists, kind, width, n, rank, world)
-        level_src = np.array([[int(hdl.buffer_ptrs[r]) + 8 * ell * lnws[r] for r in range(world)]
-                              for ell in range(width)], dtype=np.int64)
-        ops.merge_peer(owned, w0, w1, n, arrays, level_src, world)
-        # peers may reuse their buffers only after every owner has read them
-        done = torch.zeros(1, dtype=torch.int64, device=dev)
-        dist.all_reduce(done, group=group)
-        res = ShardedResult(n, sigma, kind, width, w0, w1, owned, zeros, ghist)
-        if gather:
-            res.full_words = _gather_levels(owned, ranges, width, total_words, rank, world, group, dev)
-        return res
 
     plans = exchange_plan(hists, kind, width, n, local_ns, world)[1]
     # 3. one all_to_all for every level: the send buffer is grouped by
@@ -314,9 +332,10 @@ def build_sharded(local_text, sigma: int, kind: str = "wm", group=None, *, ops=N
             for r in range(world):
                 a, b = pd["src"][r]
                 recv_sizes[r] += max(b - a, 0)
-    send = torch.cat(send_parts) if send_parts else torch.zeros(0, dtype=torch.int64, device=dev)
-    recv = torch.empty(sum(recv_sizes), dtype=torch.int64, device=dev)
+    send = torch.cat(send_parts).to(cdev) if send_parts else torch.zeros(0, dtype=torch.int64, device=cdev)
+    recv = torch.empty(sum(recv_sizes), dtype=torch.int64, device=cdev)
     dist.all_to_all_single(recv, send, recv_sizes, send_sizes, group=group)
+    recv = recv.to(dev)
 
     # receive-buffer offsets: segments arrive grouped by source rank, level-major inside
     seg_base = np.cumsum([0] + recv_sizes[:-1])
@@ -337,54 +356,132 @@ def build_sharded(local_text, sigma: int, kind: str = "wm", group=None, *, ops=N
         ops.merge(owned[ell], w0, w1, n, bounds, src_starts.astype(np.int64), recv)
     res = ShardedResult(n, sigma, kind, width, w0, w1, owned, zeros, ghist)
     if gather:
-        res.full_words = _gather_levels(owned, ranges, width, total_words, rank, world, group, dev)
+        res.full_words = _gather_levels(owned, ranges, width, total_words, rank, world, group, dev, cdev)
     return res
 
 
-def _gather_levels(owned, ranges, width, total_words, rank, world, group, dev):
+def _build_sharded_p2p(local_text, sigma, kind, group, ops, gather, local_ns, ns, n, rank, world, ranges, cdev):
+    """p2p transport: local levels in peer-mapped memory, plan and merge on the device."""
+    import torch
+    import torch.distributed as dist
+
+    dev = ops.device
+    width = code_width(sigma)
+    nb = 1 << width
+    w0, w1 = ranges[rank]
+    total_words = (n + 63) >> 6
+    lnws = [(v + 63) >> 6 for v in local_ns]
+    # 1. local build straight into this rank's peer-visible buffer, with its
+    #    histogram, node borders (= the rank's local group starts) and zero counts
+    hdl_ptrs, buf = ops.peer_buffer(width * max(lnws), group, cdev)
+    lb = ops.local_build(local_text, sigma, kind, out_words=buf[: width * lnws[rank]], borders=True)
+    words, hist, bad, borders, zeros_local = lb
+    # 2. one all_gather of [histogram | borders | zero counts | range flag] per rank
+    flag = (bad.reshape(-1)[:1].to(torch.int64) & 1) if torch.is_tensor(bad) else         torch.tensor([1 if bad else 0], dtype=torch.int64, device=dev)
+    nbd = max(nb - 2, 0)
+    row = torch.cat([hist.reshape(-1).to(torch.int64), borders.reshape(-1)[:nbd].to(torch.int64),
+                     zeros_local.reshape(-1)[:width].to(torch.int64), flag.reshape(-1)]).to(cdev)
+    rowlen = row.numel()
+    allrows = torch.empty((world, rowlen), dtype=torch.int64, device=cdev)
+    dist.all_gather_into_tensor(allrows, row.reshape(1, -1), group=group)
+    tail = allrows[:, nb + nbd:].cpu().numpy()  # per rank: zero counts + flag (one small host read)
+    if tail[:, -1].any():
+        raise ValueError(f"symbols must lie in [0, {sigma})")
+    zeros = [int(z) for z in tail[:, :width].sum(axis=0)]  # zero counts add over shards
+    rows_dev = allrows.to(dev)
+    ghist = rows_dev[:, :nb].sum(dim=0)
+    owned = torch.empty((width, max(w1 - w0, 0)), dtype=torch.int64, device=dev)
+    if n > 0:
+        # 3. the merge plan of every level on the device (wvlt_peer_plan), then
+        # 4. one kernel per owner reads the peers' local levels directly.  The
+        #    all_gather above is ordered after every rank's local build, so the
+        #    peers' levels are complete once it has finished here.
+        plan = ops.device_plan(rows_dev, rowlen, nb, ns.to(dev), world, width, kind)
+        level_src = ops.level_sources(hdl_ptrs, lnws, width, world)
+        ops.merge_peer_device(owned, w0, w1, n, plan, level_src, world)
+    # peers may reuse their buffers only after every owner has read them (a
+    # host-staged completion collective is not ordered after the merge kernel)
+    if cdev.type != "cuda":
+        torch.cuda.current_stream(dev).synchronize()
+    done = torch.zeros(1, dtype=torch.int64, device=cdev)
+    dist.all_reduce(done, group=group)
+    res = ShardedResult(n, sigma, kind, width, w0, w1, owned, zeros, ghist)
+    if gather:
+        res.full_words = _gather_levels(owned, ranges, width, total_words, rank, world, group, dev, cdev)
+    return res
+
+
+def _gather_levels(owned, ranges, width, total_words, rank, world, group, dev, cdev=None):
     """Assemble the full levels on rank 0 (owned ranges padded to equal size for gather)."""
     import torch
     import torch.distributed as dist
 
+    cdev = cdev if cdev is not None else dev
     sizes = [(b - a) * width for a, b in ranges]
     mx = max(sizes) if sizes else 0
-    flat = torch.zeros(mx, dtype=torch.int64, device=dev)
-    flat[: sizes[rank]] = owned.reshape(-1)
+    flat = torch.zeros(mx, dtype=torch.int64, device=cdev)
+    flat[: sizes[rank]] = owned.reshape(-1).to(cdev)
     if rank == 0:
-        parts = [torch.empty(mx, dtype=torch.int64, device=dev) for _ in range(world)]
+        parts = [torch.empty(mx, dtype=torch.int64, device=cdev) for _ in range(world)]
         dist.gather(flat, parts, dst=0, group=group)
         full = torch.empty((width, total_words), dtype=torch.int64, device=dev)
         for (a, b), p, sz in zip(ranges, parts, sizes):
-            full[:, a:b] = p[:sz].reshape(width, b - a)
+            full[:, a:b] = p[:sz].reshape(width, b - a).to(dev)
         return full
     dist.gather(flat, None, dst=0, group=group)
     return None
 
 
 class CudaOps:
-    """Local build + merge on this rank's CUDA device (hand-written kernels)."""
+    """Local build + merge on this rank's CUDA device (hand-written kernels).
 
-    def __init__(self, device=None):
+    ``peer``: how the p2p transport maps every rank's local levels into every
+    peer -- "symm" (torch symmetric memory over NVLink, the NCCL product path)
+    or "ipc" (CUDA IPC handles exchanged through the process group; several
+    processes sharing one GPU in the one-GPU multi-rank tests)."""
+
+    def __init__(self, device=None, peer: str = "symm"):
         import torch
 
         from .device import DeviceBuilder
 
+        if peer not in ("symm", "ipc"):
+            raise ValueError(f"unknown peer mapping {peer!r}")
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
         self.builder = DeviceBuilder(self.device)
-        self._peer = None  # (handle, buffer) of the p2p transport, reused while large enough
+        self.peer = peer
+        self._peer = None   # (peer pointers, buffer[, keep-alive]) of the p2p transport, reused while large enough
+        self._plan = None   # device plan buffers, reused while the shape matches
+        self._src = None    # ((pointers, lnws, width), device level-source table)
 
-    def peer_buffer(self, words: int, group=None):
-        """A symmetric-memory int64 buffer of at least ``words`` on every rank of
-        ``group`` (collective when it has to grow: every rank asks for the same size)."""
+    def peer_buffer(self, words: int, group=None, comm_device=None):
+        """An int64 buffer of at least ``words`` on every rank of ``group``, mapped
+        into every peer (collective when it has to grow: every rank asks for the
+        same size).  Returns (per-rank base pointers, this rank's buffer)."""
+        import torch
         import torch.distributed as dist
-        from torch.distributed import _symmetric_memory as symm_mem
 
         if self._peer is None or self._peer[1].numel() < words:
-            buf = symm_mem.empty(max(int(words), 1), dtype=torch_int64(), device=self.device)
-            self._peer = (symm_mem.rendezvous(buf, group if group is not None else dist.group.WORLD), buf)
-        return self._peer
+            self._peer = None
+            self._src = None
+            if self.peer == "symm":
+                from torch.distributed import _symmetric_memory as symm_mem
 
-    def local_build(self, text, sigma: int, kind: str, out_words=None):
+                buf = symm_mem.empty(max(int(words), 1), dtype=torch.int64, device=self.device)
+                hdl = symm_mem.rendezvous(buf, group if group is not None else dist.group.WORLD)
+                self._peer = ([int(p) for p in hdl.buffer_ptrs], buf, hdl)
+            else:
+                from torch.multiprocessing.reductions import reduce_tensor
+
+                buf = torch.empty(max(int(words), 1), dtype=torch.int64, device=self.device)
+                world, rank = dist.get_world_size(group), dist.get_rank(group)
+                handles = [None] * world
+                dist.all_gather_object(handles, reduce_tensor(buf), group=group)
+                peers = [buf if r == rank else fn(*args) for r, (fn, args) in enumerate(handles)]
+                self._peer = ([int(t.data_ptr()) for t in peers], buf, peers)
+        return self._peer[0], self._peer[1]
+
+    def local_build(self, text, sigma: int, kind: str, out_words=None, borders: bool = False):
         import torch
 
         if not isinstance(text, torch.Tensor):
@@ -393,12 +490,18 @@ class CudaOps:
             text = torch.from_numpy(_device_text(np.ascontiguousarray(np.asarray(text)), sigma))
         text = text.to(self.device)
         outputs = None
-        if out_words is not None:  # levels into a caller buffer (symmetric memory for the p2p merge)
-            lw, zeros, hist, bd, status = self.builder.alloc_outputs(int(text.numel()), sigma)
-            outputs = (out_words.view(lw.shape), zeros, hist, bd, status)
-        res = self.builder.build(text, sigma, kind, histogram=True, check=False, outputs=outputs)
+        if out_words is not None or borders:  # levels into a caller buffer (peer-mapped for the p2p merge)
+            lw, zeros, hist, bd, status = self.builder.alloc_outputs(int(text.numel()), sigma, borders=borders)
+            if out_words is not None:
+                lw = out_words.view(lw.shape)
+            if borders and bd is None:
+                bd = torch.zeros(1, dtype=torch.int64, device=self.device)
+            outputs = (lw, zeros, hist, bd, status)
+        res = self.builder.build(text, sigma, kind, histogram=True, borders=borders, check=False, outputs=outputs)
         # the range status stays on the device (read with the histograms, no extra sync)
         bad = res.status if res.status is not None else False
+        if borders:
+            return res.level_words, res.hist, bad, res.borders, res.zeros
         return res.level_words, res.hist, bad
 
     def merge(self, dst_row, word_lo: int, word_hi: int, n_bits: int, bounds, src_starts, src):
@@ -408,31 +511,64 @@ class CudaOps:
         s = torch.from_numpy(src_starts).to(self.device)
         self.builder.merge_bits(dst_row, word_lo, word_hi, n_bits, b, s, src, dst_offset_words=word_lo)
 
-    def merge_peer(self, owned, word_lo: int, word_hi: int, n_bits: int, arrays, level_src, nranks: int):
-        """wvlt_merge_levels_peer into ``owned`` [width, word_hi - word_lo]; ``level_src``
-        int64 [width, nranks] device addresses of every rank's local levels."""
+    def device_plan(self, rows, row_stride: int, borders_col: int, ns_dev, nranks: int, width: int, kind: str):
+        """wvlt_peer_plan into cached device buffers: (bounds, bounds_off, starts, ranks, task_off).
+        ``ns_dev``: int64 device tensor of the ranks' symbol counts."""
         import torch
 
         from . import _lib
 
-        bounds, boff, starts, ranks, toff = arrays
-        dev = self.device
-        flat = torch.from_numpy(np.concatenate([bounds, boff, starts, toff, level_src.reshape(-1)])).to(dev)
-        rk = torch.from_numpy(ranks).to(dev)
-        o1 = bounds.size
-        o2 = o1 + boff.size
-        o3 = o2 + starts.size
-        o4 = o3 + toff.size
-        base, e = flat.data_ptr(), flat.element_size()
+        ntask = nranks * ((1 << width) - 1)
+        key = (nranks, width)
+        if self._plan is None or self._plan[0] != key:
+            dev = self.device
+            self._plan = (key, (torch.empty(ntask + width, dtype=torch.int64, device=dev),
+                                torch.empty(max(width, 1), dtype=torch.int64, device=dev),
+                                torch.empty(max(ntask, 1), dtype=torch.int64, device=dev),
+                                torch.empty(max(ntask, 1), dtype=torch.int32, device=dev),
+                                torch.empty(width + 1, dtype=torch.int64, device=dev)))
+        bounds, boff, starts, ranks, toff = self._plan[1]
+        ns_dev = ns_dev.to(device=self.device, dtype=torch.int64).contiguous()
+        rc = _lib.load().wvlt_peer_plan(rows.data_ptr(), int(row_stride), int(borders_col), ns_dev.data_ptr(),
+                                        int(nranks), int(width), _lib.KINDS[kind], bounds.data_ptr(),
+                                        starts.data_ptr(), ranks.data_ptr(), boff.data_ptr(), toff.data_ptr(),
+                                        torch.cuda.current_stream(self.device).cuda_stream)
+        _lib.check(rc)
+        return bounds, boff, starts, ranks, toff
+
+    def level_sources(self, ptrs, lnws, width: int, nranks: int):
+        """Device table of every (level, rank)'s local level address, cached per buffer layout."""
+        import torch
+
+        key = (tuple(ptrs), tuple(lnws), width)
+        if self._src is None or self._src[0] != key:
+            tab = np.array([[ptrs[r] + 8 * ell * lnws[r] for r in range(nranks)] for ell in range(width)],
+                           dtype=np.int64)
+            self._src = (key, torch.from_numpy(tab.reshape(-1)).to(self.device))
+        return self._src[1]
+
+    def merge_peer_device(self, owned, word_lo: int, word_hi: int, n_bits: int, plan, level_src, nranks: int):
+        """wvlt_merge_levels_peer with a device plan and a device level-source table."""
+        import torch
+
+        from . import _lib
+
+        bounds, boff, starts, ranks, toff = plan
         width = int(owned.shape[0])
         rc = _lib.load().wvlt_merge_levels_peer(
             owned.data_ptr(), int(owned.shape[1]) if owned.dim() == 2 else 0, width, int(word_lo), int(word_hi),
-            int(n_bits), base, base + e * o1, base + e * o2, rk.data_ptr(), base + e * o3, base + e * o4, int(nranks),
-            torch.cuda.current_stream(dev).cuda_stream)
+            int(n_bits), bounds.data_ptr(), boff.data_ptr(), starts.data_ptr(), ranks.data_ptr(), toff.data_ptr(),
+            level_src.data_ptr(), int(nranks), torch.cuda.current_stream(self.device).cuda_stream)
         _lib.check(rc)
 
+    def merge_peer(self, owned, word_lo: int, word_hi: int, n_bits: int, arrays, level_src, nranks: int):
+        """wvlt_merge_levels_peer into ``owned`` [width, word_hi - word_lo] from host plan
+        arrays (owner_plan_arrays); ``level_src`` int64 [width, nranks] device addresses
+        of every rank's local levels."""
+        import torch
 
-def torch_int64():
-    import torch
-
-    return torch.int64
+        dev = self.device
+        bounds, boff, starts, ranks, toff = arrays
+        plan = tuple(torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in (bounds, boff, starts, ranks, toff))
+        src = torch.from_numpy(np.ascontiguousarray(level_src, dtype=np.int64).reshape(-1)).to(dev)
+        self.merge_peer_device(owned, word_lo, word_hi, n_bits, plan, src, nranks)

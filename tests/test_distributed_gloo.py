@@ -175,3 +175,45 @@ def test_owner_plan_equals_full_exchange_plan(kind, world, width):
         got = owner_plan_arrays(hists, kind, width, n, owner, world)
         for a, b in zip(want, got):
             assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("kind", ["wt", "wm"])
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+@pytest.mark.parametrize("width", [1, 2, 3, 8, 12])
+def test_device_plan_restatement_equals_merge_plan(kind, world, width):
+    """The device plan (wvlt_peer_plan, restated by plan_from_borders_host) built from
+    the ranks' node borders has, per level, exactly the pieces of the reference
+    merge plan (construct._merge_plan, construct.py:516-543 -> level_plan) once
+    the empty ones are dropped; the merge it drives (host restatement of
+    merge_peer_kernel) gives the single build's words for every owner."""
+    import oracle
+    from paper_1702_07578_b200.distributed import level_plan, merge_peer_host, plan_from_borders_host, word_ranges
+
+    rng = np.random.default_rng(world * 1000 + width * 7 + (kind == "wm"))
+    sigma = 1 << width
+    n = int(rng.integers(2000, 6000))
+    text = (rng.zipf(1.3, n) % sigma).astype(np.uint16 if width > 8 else np.uint8)
+    cuts = [0] + sorted(int(v) for v in rng.integers(0, n, world - 1)) + [n]
+    if world > 2:
+        cuts[1] = 0  # an empty shard
+    shards = [text[cuts[r]:cuts[r + 1]] for r in range(world)]
+    hists = np.stack([oracle.histogram(s, sigma) for s in shards])
+    borders = [oracle.borders(h, width, kind) for h in hists]
+    local_ns = [s.size for s in shards]
+    bounds, boff, starts, ranks, toff = plan_from_borders_host(borders, local_ns, kind, width)
+    for ell in range(width):
+        t0, t1 = int(toff[ell]), int(toff[ell + 1])
+        b = bounds[int(boff[ell]): int(boff[ell]) + (t1 - t0) + 1]
+        lens = np.diff(b)
+        keep = lens > 0
+        pr, pl, pn, pg = level_plan(hists, kind, width, ell)
+        assert np.array_equal(ranks[t0:t1][keep], pr)
+        assert np.array_equal(starts[t0:t1][keep], pl)
+        assert np.array_equal(lens[keep], pn)
+        assert np.array_equal(b[:-1][keep], pg)
+        assert int(b[-1]) == n
+    sources = [oracle.build(s, sigma, kind, "pc")[0] for s in shards]
+    want, _, _ = oracle.build(text, sigma, kind, "pc")
+    for owner, (w0, w1) in enumerate(word_ranges((n + 63) >> 6, world)):
+        got = merge_peer_host((bounds, boff, starts, ranks, toff), sources, w0, w1, n, width)
+        assert np.array_equal(got, np.asarray(want, dtype=np.uint64)[:, w0:w1]), owner

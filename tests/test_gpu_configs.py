@@ -142,11 +142,16 @@ def test_config_full_size_properties(config, kind):
 
 @pytest.mark.parametrize("config", ["c1", "c2", "c3", "c3s4", "c4", "c5"])
 def test_config_bytes_vs_oracle_ps(config):
+    """Default build (the WM one histogram-free) byte for byte vs oracle ps; the
+    build with node borders requested gives the same levels and the borders of
+    the oracle's histogram (oracle.borders, the interval_starts /
+    interval_start_table restatement)."""
     cfg = workloads.CONFIGS[config]
     torch.cuda.empty_cache()
     text = workloads.generate(config)
     host = text.cpu().numpy()
     threads = os.cpu_count() or 1
+    hist = oracle.histogram(host, cfg["sigma"])
     b = DeviceBuilder()
     for kind in ("wm", "wt"):
         res = b.build(text, cfg["sigma"], kind)
@@ -158,7 +163,14 @@ def test_config_bytes_vs_oracle_ps(config):
             assert bad.size == 0, (config, kind, ell, int(bad[0]) if bad.size else None, bad.size)
         if kind == "wm":
             assert [int(z) for z in res.zeros.cpu().tolist()] == oz
-        del res, ow
+        del ow
+        full = b.build(text, cfg["sigma"], kind, borders=True, histogram=True)
+        assert torch.equal(full.level_words, res.level_words), (config, kind)
+        assert torch.equal(full.zeros, res.zeros)
+        assert np.array_equal(full.hist.cpu().numpy(), hist)
+        w = res.width
+        assert np.array_equal(full.borders.cpu().numpy()[: (1 << w) - 2], oracle.borders(hist, w, kind))
+        del res, full
     del text, host
     torch.cuda.empty_cache()
 

@@ -36,6 +36,40 @@ def test_golden_cases_bit_exact(kind):
         assert wv.dump_structure(st) == g[f"dump_{kind}_{ci}"].tobytes(), (ci, n, sigma, dist)
 
 
+@pytest.mark.parametrize("kind", ["wt", "wm"])
+def test_golden_node_borders_from_drop_in(kind):
+    """build_structure(...).node_borders(l) == the reference's interval_starts of the
+    folded histogram (WT, levelstats.py:58-73) / interval_start_table block l (WM,
+    wt2wm.py:55-78), for every golden case and level (code widths above 12 carry
+    no golden borders: the oracle's restatement, pinned to the golden ones, of the
+    reference's golden histogram stands in)."""
+    g = golden()
+    for ci, n, sigma, dist in CASES:
+        st = wv.build_structure(g[f"text_{ci}"], sigma, kind)
+        key = f"borders_{kind}_{ci}"
+        want = g[key] if key in g else oracle.borders(g[f"hist_{ci}"], wv.code_width(sigma), kind)
+        w = wv.code_width(sigma)
+        assert st.borders is not None and st.borders.shape == want.shape, (ci, n, sigma)
+        for ell in range(1, w):
+            assert np.array_equal(st.node_borders(ell), want[(1 << ell) - 2 : (1 << (ell + 1)) - 2]), (ci, ell)
+        with pytest.raises(IndexError):
+            st.node_borders(0)
+
+
+@pytest.mark.parametrize("sigma", [4, 5, 256, 1000, 1 << 16, 70000, 1 << 20])
+@pytest.mark.parametrize("kind", ["wt", "wm"])
+def test_node_borders_vs_oracle(kind, sigma):
+    """Borders of larger texts through the drop-in (byte texts: the fused pass's
+    tables; wider alphabets: the group recurrence over the matrix levels)."""
+    rng = np.random.default_rng(sigma + 3)
+    for n in (16385, 300_001):
+        text = random_text(rng, n, sigma)
+        st = wv.build_structure(text, sigma, kind)
+        w = wv.code_width(sigma)
+        assert np.array_equal(st.borders, oracle.borders(oracle.histogram(text, sigma), w, kind))
+        assert wv.dump_structure(st) == ref_dump(text, sigma, kind)
+
+
 def test_running_example():
     wt = wv.build_structure(EXAMPLE_TEXT, EXAMPLE_SIGMA, "wt")
     wm = wv.build_structure(EXAMPLE_TEXT, EXAMPLE_SIGMA, "wm")

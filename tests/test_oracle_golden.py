@@ -33,6 +33,17 @@ def test_oracle_ps_matches_reference_dump(kind, threads):
         assert oracle.dump(kind, n, sigma, words, zeros) == g[f"dump_{kind}_{ci}"].tobytes(), ci
 
 
+@pytest.mark.parametrize("algo", ["ddpc", "ddps"])
+@pytest.mark.parametrize("kind", ["wt", "wm"])
+@pytest.mark.parametrize("threads", [1, 3, 8])
+def test_oracle_dd_matches_reference_dump(kind, threads, algo):
+    """Domain-decomposed builders (construct.py:437-543): identical bytes for any slice count."""
+    g = golden()
+    for ci, n, sigma, _ in golden_cases():
+        words, zeros, _ = oracle.build(g[f"text_{ci}"], sigma, kind, algo, threads)
+        assert oracle.dump(kind, n, max(sigma, 1), words, zeros) == g[f"dump_{kind}_{ci}"].tobytes(), (ci, threads)
+
+
 @pytest.mark.parametrize("kind", ["wt", "wm"])
 def test_naive_oracle_matches_reference_dump(kind):
     g = golden()
