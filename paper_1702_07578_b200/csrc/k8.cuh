@@ -609,6 +609,7 @@ __global__ void __launch_bounds__(T8_WARPS * 32) tiles8_kernel(const Pass8Args a
 #ifndef K8_Q
 #define K8_Q 4
 #endif
+
 template <int Q>
 struct K8Cfg {
   static constexpr int NT = K8_TILE / (8 * Q);
@@ -741,24 +742,26 @@ __global__ void __launch_bounds__(K8Cfg<Q>::NT, K8Cfg<Q>::CTAS) level_pass8_kern
     const uint32_t nxt = sbase + (uint32_t)((j + 1) & 1) * T;
 #pragma unroll
     for (int k = 0; k < Q; ++k) {
+      const int nz = 8 - (int)ones[k];
+      const uint32_t za = nxt + (uint32_t)(k * R + 8 * tid - opre[k]);
+      const uint32_t oa = nxt + (uint32_t)(Z + opre[k]);
       const uint32_t sel = s_lut[m[k]];  // prmt reads selector bits 0-15
       const uint32_t sv[2] = {prmt(x[2 * k], x[2 * k + 1], sel), prmt(x[2 * k], x[2 * k + 1], sel >> 16)};
-      const int nz = 8 - (int)ones[k];
       // zeros of run k go to k R + 8 t - opre (its zeros before), ones to Z + opre
-      const uint32_t za = opaque(nxt + (uint32_t)(k * R + 8 * tid - opre[k]));
-      const uint32_t oa = opaque(nxt + (uint32_t)(Z + opre[k] - nz));
+      const uint32_t zo = opaque(za);
+      const uint32_t oo = opaque(oa - (uint32_t)nz);
       // address selection mostly off the integer ALU pipe (its bound): the
       // carry of (15 - nz) 2^28 + (kk + 1) 2^28 out of 32 bits is [kk >= nz],
       // read as the high word of one mad.wide; then addr = za + flag (oa - za)
       const uint32_t F = (uint32_t)(15 - nz) << 28;
-      const uint32_t dz = oa - za;
+      const uint32_t dz = oo - zo;
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk) {
         const uint32_t v = sv[kk >> 2];
         const uint32_t vb = (kk & 3) == 0 ? v : (kk & 3) == 1 ? shr_mul<8>(v) : (kk & 3) == 2 ? shr_mul<16>(v) : shr_mul<24>(v);
         uint64_t t;
         asm("mad.wide.u32 %0, %1, 1, %2;" : "=l"(t) : "r"(F), "l"((uint64_t)(kk + 1) << 28));
-        const uint32_t addr = za + (uint32_t)(t >> 32) * dz + kk;
+        const uint32_t addr = zo + (uint32_t)(t >> 32) * dz + kk;
         asm volatile("st.shared.u8 [%0], %1;" ::"r"(addr), "r"(vb) : "memory");
       }
     }

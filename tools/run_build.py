@@ -15,7 +15,6 @@ sys.path.insert(0, str(ROOT))
 import torch  # noqa: E402
 
 import workloads  # noqa: E402
-from paper_1702_07578_b200.device import DeviceBuilder  # noqa: E402
 
 
 def main():
@@ -24,7 +23,14 @@ def main():
     ap.add_argument("--log2n", type=int, default=None)
     ap.add_argument("--kind", default=None)
     ap.add_argument("--iters", type=int, default=2)
+    ap.add_argument("--variant", default=None, help="a tools/variants/<name>.so tuning build instead of the product library")
     a = ap.parse_args()
+    if a.variant:
+        from paper_1702_07578_b200 import _lib
+
+        _lib.load_variant(ROOT / "tools" / "variants" / f"{a.variant}.so")
+    from paper_1702_07578_b200.device import DeviceBuilder
+
     cfg = workloads.CONFIGS[a.config]
     n = (1 << a.log2n) if a.log2n else cfg["n"]
     text = workloads.generate(a.config, n=n)

@@ -49,7 +49,11 @@ def child(name: str, config: str, steps: int) -> None:
     torch.cuda.synchronize()
     for k, v in _lib.profile_read():
         stages[k] = round(v, 4)
-    print(json.dumps({"variant": name, "config": config, "ms": e0.elapsed_time(e1) / steps, "stages_ms": stages}))
+    lw = outs[0]
+    w = torch.arange(1, lw.numel() + 1, device=lw.device, dtype=torch.int64)
+    digest = [int((lw.reshape(-1) * w).sum()), int(lw.reshape(-1).sum()), int(outs[1].sum())]
+    print(json.dumps({"variant": name, "config": config, "ms": e0.elapsed_time(e1) / steps, "stages_ms": stages,
+                      "digest": digest}))
 
 
 def main():
