@@ -59,6 +59,18 @@ int wvlt_code_width(int64_t sigma);
 size_t wvlt_workspace_bytes(int64_t n, int sym_bytes, int64_t sigma, int kind);
 
 /*
+ * What one build's workspace holds, by the reference ledger's categories
+ * (construct.AllocationLog, construct.py:48-127): parts[0] "positions" (count
+ * chains, node borders, placement tables, per-tile counts / prefixes / run
+ * tables), parts[1] "symbols" (level-order buffers in HBM; 0 for a byte text,
+ * whose fused pass keeps every order in shared memory), parts[2]
+ * "partial_bits" (a wide-alphabet tree's matrix before the reorder).  Bytes;
+ * want_hist / want_borders as the build requests them.
+ */
+int wvlt_workspace_parts(int64_t n, int sym_bytes, int64_t sigma, int kind, int want_hist, int want_borders,
+                         size_t* parts);
+
+/*
  * Symbol histogram, padded to 2^width bins, plus the range check.
  * Replaces hist_and_msb_bits / full_histogram (_kernels.py:23-42) and
  * levelstats.symbol_histogram (levelstats.py:30-47).

@@ -67,6 +67,8 @@ def _bind(L):
     L.wvlt_code_width.restype = i32
     L.wvlt_workspace_bytes.argtypes = [i64, i32, i64, i32]
     L.wvlt_workspace_bytes.restype = sz
+    L.wvlt_workspace_parts.argtypes = [i64, i32, i64, i32, i32, i32, vp]
+    L.wvlt_workspace_parts.restype = i32
     L.wvlt_histogram.argtypes = [vp, i32, i64, i64, vp, vp, vp]
     L.wvlt_histogram.restype = i32
     L.wvlt_build_device.argtypes = [vp, i32, i64, i64, i32, vp, vp, vp, vp, vp, sz, vp, vp]
@@ -98,6 +100,14 @@ def _bind(L):
     if L.wvlt_abi_version() != 1:
         raise ImportError("wvlt_b200 ABI version mismatch")
     return L
+
+
+def workspace_parts(n: int, sym_bytes: int, sigma: int, kind: str, histogram: bool, borders: bool):
+    """(positions, symbols, partial_bits) bytes of one build's workspace (wvlt_workspace_parts)."""
+    out = (ctypes.c_size_t * 3)()
+    rc = load().wvlt_workspace_parts(int(n), int(sym_bytes), int(sigma), KINDS[kind], int(histogram), int(borders), out)
+    check(rc)
+    return int(out[0]), int(out[1]), int(out[2])
 
 
 def check(rc: int) -> None:

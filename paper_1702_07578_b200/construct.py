@@ -84,22 +84,30 @@ def track_allocations():
         _active_log = prev
 
 
-def _note_device_build(n: int, sym_bytes: int, sigma: int, kind: str) -> None:
-    """Log the device build's auxiliary buffers, then release them (the build is synchronous)."""
+def _note_device_build(n: int, sym_bytes: int, sigma: int, kind: str, histogram: bool, borders: bool) -> None:
+    """Log the device build's auxiliary buffers, then release them (the build is synchronous).
+
+    The sizes are the build's own workspace carve (wvlt_workspace_parts): the
+    same allocations the device build makes, under the reference categories
+    (construct.py:48-127); entries are 8-byte units."""
     if _active_log is None:
         return
-    w = code_width(sigma)
+    from . import _lib
+
+    positions, symbols, partial = _lib.workspace_parts(n, sym_bytes, sigma, kind, histogram, borders)
     noted = []
 
-    def note(cat: str, entries: int, nbytes: int) -> None:
+    def note(cat: str, nbytes: int, entries: int) -> None:
         _active_log.note(cat, entries, nbytes)
         noted.append(nbytes)
 
-    note("positions", 2 << w, 8 * (2 << w))  # histogram fold chain (all levels)
-    note("positions", 2 << w, 8 * (2 << w))  # interval starts / placement tables
-    npass = -(-w // 4)
-    for _ in range(min(npass - 1, 2)):  # ping-pong level-order buffers
-        note("symbols", n, n * sym_bytes)
+    if positions:
+        note("positions", positions, positions // 8)
+    if symbols:  # the two ping-pong level-order buffers
+        note("symbols", symbols // 2, n)
+        note("symbols", symbols - symbols // 2, n)
+    if partial:
+        note("partial_bits", partial, partial // 8)
     _active_log.release(sum(noted))
 
 
@@ -204,7 +212,7 @@ def _build(text, sigma: int, kind: str, threads: int = 1):
     from .device import default_builder
 
     dev_arr = _device_text(arr, sigma)
-    _note_device_build(n, dev_arr.dtype.itemsize, sigma, kind)
+    _note_device_build(n, dev_arr.dtype.itemsize, sigma, kind, histogram=kind == "wt", borders=True)
     # the WT build computes the histogram anyway (its placement tables need it);
     # the node borders come with every build (byte texts: from the same tables;
     # wider alphabets: from the group recurrence over the matrix levels)

@@ -2484,6 +2484,36 @@ size_t wvlt_workspace_bytes(int64_t n, int sym_bytes, int64_t sigma, int kind) {
   return total;
 }
 
+int wvlt_workspace_parts(int64_t n, int sym_bytes, int64_t sigma, int kind, int want_hist, int want_borders,
+                         size_t* parts) {
+  if (!parts) return WVLT_E_ARG;
+  parts[0] = parts[1] = parts[2] = 0;
+  if (n < 0 || !(sym_bytes == 1 || sym_bytes == 2 || sym_bytes == 4) || sigma < 1) return WVLT_E_ARG;
+  if (kind != WVLT_KIND_WT && kind != WVLT_KIND_WM) return WVLT_E_ARG;
+  const bool lean = kind == WVLT_KIND_WM && !want_hist && !want_borders;
+  Plan P;
+  if (!make_plan(n, sym_bytes, sigma, kind, &P, lean)) return WVLT_E_WIDTH;
+  const int w = P.width;
+  if (n == 0 || w == 0) return 0;
+  // the same path choice as build_device_impl
+  WtViaWm L;
+  if ((kind == WVLT_KIND_WT || !lean) && w > 8 && wt_via_wm_layout(n, sym_bytes, sigma, kind, &L)) {
+    Plan M;
+    make_plan(n, sym_bytes, sigma, WVLT_KIND_WM, &M, true);
+    parts[0] = (L.off_ws - L.off_zeros) + M.off_buf0;                 // group tables + the matrix build's tables
+    parts[1] = 2 * M.buf_bytes + (M.widen_bytes ? align_up((size_t)n * M.widen_bytes, 256) : 0);
+    parts[2] = kind == WVLT_KIND_WT ? (size_t)w * (size_t)((n + 63) >> 6) * 8 : 0;  // the matrix before its reorder
+    return 0;
+  }
+  if (k8_eligible(sym_bytes, w, n) && !P.widen_bytes) {
+    parts[0] = k8_layout(n, w).total;  // per-tile counts, prefixes, run tables; the level orders stay on chip
+    return 0;
+  }
+  parts[0] = P.off_buf0;
+  parts[1] = 2 * P.buf_bytes + (P.widen_bytes ? align_up((size_t)n * P.widen_bytes, 256) : 0);
+  return 0;
+}
+
 int wvlt_histogram(const void* text, int sym_bytes, int64_t n, int64_t sigma, int64_t* hist, int32_t* status,
                    void* stream) {
   if (!(sym_bytes == 1 || sym_bytes == 2 || sym_bytes == 4) || n < 0 || sigma < 1 || !hist) return WVLT_E_ARG;

@@ -386,3 +386,20 @@ def test_pageable_host_buffers_are_staged(sigma, kind):
     ref_words, _, _ = oracle.build(text[:5_000_001], sigma, kind, "pc")
     for ell, lv in enumerate(st.levels):
         assert np.array_equal(lv.words, ref_words[ell])
+
+
+def test_allocation_ledger_of_real_builds(rng):
+    """track_allocations around real drop-in builds logs the device workspace
+    (positions always; symbols only for wide alphabets; partial_bits for a wide tree)."""
+    from paper_1702_07578_b200.construct import track_allocations
+
+    n = 200_001
+    for sigma, kind, nsym, partial in [(256, "wm", 0, False), (5, "wt", 0, False), (1 << 16, "wm", 2, False),
+                                       (1 << 20, "wt", 2, True)]:
+        text = random_text(rng, n, sigma)
+        with track_allocations() as log:
+            st = wv.build_structure(text, sigma, kind)
+        assert wv.dump_structure(st) == ref_dump(text, sigma, kind)
+        assert log.position_entries > 0
+        assert log.buffers("symbols") == [n] * nsym, (sigma, kind)
+        assert bool(log.buffers("partial_bits")) == partial

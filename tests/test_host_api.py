@@ -139,3 +139,34 @@ def test_track_allocations_logs_device_buffers_without_gpu_for_degenerate():
     with wv.track_allocations() as log:
         wv.build_structure([], 16, "wt")
     assert log.position_entries == 0  # nothing allocated for an empty text
+
+
+def test_allocation_ledger_is_the_device_workspace():
+    """track_allocations (construct.py:48-127; pinned counts in test_acceptance.py:184-199)
+    logs the device build's own workspace carve under the reference categories:
+    byte texts keep every level order on chip (no "symbols" buffers, unlike ps's
+    scratch of n symbols), wider alphabets ping-pong two n-symbol buffers, a wide
+    tree logs its matrix before the reorder as "partial_bits"; the logged bytes
+    never exceed wvlt_workspace_bytes."""
+    from paper_1702_07578_b200 import _lib
+    from paper_1702_07578_b200.construct import _note_device_build, track_allocations
+
+    lib = _lib.load()
+    n = 1_000_003
+    for sigma, sb, kind, symbols, partial in [(4, 1, "wm", [], 0), (256, 1, "wt", [], 0), (256, 1, "wm", [], 0),
+                                              (1 << 16, 2, "wm", [n, n], 0), (1 << 16, 2, "wt", [n, n], 16),
+                                              (1 << 20, 4, "wt", [n, n], 20), (1000, 2, "wm", [n, n], 0)]:
+        with track_allocations() as log:
+            _note_device_build(n, sb, sigma, kind, histogram=kind == "wt", borders=True)
+        assert log.buffers("symbols") == symbols, (sigma, kind)
+        assert log.position_entries > 0
+        if partial:
+            assert log.entries("partial_bits") == partial * ((n + 63) // 64), (sigma, kind)
+        else:
+            assert log.buffers("partial_bits") == []
+        logged = sum(b for _, _, b in log.events)
+        assert 0 < logged <= lib.wvlt_workspace_bytes(n, sb, sigma, 0 if kind == "wt" else 1)
+        assert log.peak_bytes == logged
+    with track_allocations() as log:
+        _note_device_build(0, 1, 256, "wm", histogram=False, borders=True)
+    assert log.events == []
