@@ -3,18 +3,22 @@
 from __future__ import annotations
 
 import numpy as np
+import pytest
 import torch
 
 import workloads
 
 
-def test_markov3_chain_is_one_sequential_chain():
+@pytest.mark.parametrize("coalesce_steps", [256, 1, 0])
+def test_markov3_chain_is_one_sequential_chain(coalesce_steps):
     """The segment-parallel generator equals the chain run step by step with the
-    same draws (one order-3 Markov chain, Dirichlet(0.5) rows)."""
+    same draws (one order-3 Markov chain, Dirichlet(0.5) rows), also
+    when segments are still followed from every entry context (few or no
+    coalescing steps)."""
     n = (1 << 14) * 3 + 77
     g = torch.Generator()
     g.manual_seed(3)
-    out = workloads._markov3_chain(g, n, "cpu").numpy()
+    out = workloads._markov3_chain(g, n, "cpu", coalesce_steps).numpy()
     g = torch.Generator()
     g.manual_seed(3)
     alpha = torch.full((64, 4), 0.5, dtype=torch.float64)

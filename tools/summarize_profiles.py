@@ -59,7 +59,7 @@ want = ["Kernel Name", "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__
         "smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
         "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active", "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
         "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "launch__registers_per_thread", "sm__warps_active.avg.pct_of_peak_sustained_active",
-        "smsp__inst_executed.sum"]
+        "smsp__inst_executed.sum", "l1tex__throughput.avg.pct_of_peak_sustained_active"]
 units = rr[1]
 full = []
 for r in rr[2:]:
@@ -80,8 +80,8 @@ lines = [f"# Profile summary, round tag `{tag}` (c2: WM, n=2^30 uint8, sigma=256
 for k, v in sorted(tot.items(), key=lambda x: -x[1]):
     lines.append(f"| `{k}` | {cnt[k]} | {v / 1e6:.3f} | {100 * v / grand:.1f}% |")
 lines += ["", "## `--set full` capture of the top kernels (one launch each)", "",
-          "| kernel | time us | DRAM read MB | DRAM write MB | DRAM %peak | SM %peak | issue % | ALU % | LSU % | smem wavefronts | bank conflicts | regs |",
-          "|---|---|---|---|---|---|---|---|---|---|---|---|"]
+          "| kernel | time us | DRAM read MB | DRAM write MB | DRAM %peak | SM %peak | issue % | ALU % | LSU % | L1 %peak | smem wavefronts | bank conflicts | regs |",
+          "|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
 traffic = {}
 smem = {}
 ui = {w: units[h.index(w)] for w in want if w in h}
@@ -94,6 +94,7 @@ for r in full:
     lines.append(f"| `{name}` | {t_us:.1f} | {rd:.1f} | {wr:.1f} | {r['gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed']} | "
                  f"{r['sm__throughput.avg.pct_of_peak_sustained_elapsed']} | {r['smsp__issue_active.avg.pct_of_peak_sustained_active']} | "
                  f"{r['sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active']} | {r['sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active']} | "
+                 f"{r.get('l1tex__throughput.avg.pct_of_peak_sustained_active', '')} | "
                  f"{r['l1tex__data_pipe_lsu_wavefronts_mem_shared.sum']} | {r['l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum']} | {r['launch__registers_per_thread']} |")
     if "level_pass" in name:
         traffic[f"pass{pass_idx}"] = (rd + wr) * 1e6

@@ -49,17 +49,20 @@ def _zipf_ranks(g, n, k, s, device):
     return torch.searchsorted(cdf, u).clamp_(max=k - 1)
 
 
-def _markov3_chain(g, n, device):
+def _markov3_chain(g, n, device, coalesce_steps: int = 256):
     """ONE order-3 Markov chain over {0..3} of n steps: 64 contexts x Dirichlet(0.5)
     transition rows, a uniform initial context (the first 3 symbols), step t
     consuming one uniform draw.
 
     The chain is computed in 2^14-step segments advanced in lock step.  Pass 1
-    runs every segment from all 64 possible entry contexts at once (same draws)
-    to get each segment's exit context as a function of its entry; the entry
-    context of every segment then follows sequentially from the chain's head
-    (one table lookup per segment); pass 2 replays the same draws from those
-    entries and emits the symbols.  The output is exactly the sequential chain.
+    runs every segment from all 64 possible entry contexts at once (same draws);
+    driven by the same draws the 64 trajectories coalesce within a few dozen
+    steps, after which one trajectory per segment is followed (segments that
+    have not coalesced after the first 256 steps keep all 64).  That gives each
+    segment's exit context as a function of its entry; the entry context of
+    every segment then follows sequentially from the chain's head, and pass 2
+    replays the same draws from those entries and emits the symbols.  The
+    output is exactly the sequential chain (tests/test_workloads.py).
     """
     alpha = torch.full((64, 4), 0.5, dtype=torch.float64, device=device)
     gam = torch._standard_gamma(alpha, generator=g)
@@ -69,12 +72,29 @@ def _markov3_chain(g, n, device):
     nseg = max((n + seg - 1) // seg, 1)
     head = int(torch.randint(0, 64, (1,), generator=g, device=device).item())
     state = g.get_state()
+
+    def step(ctx, u):
+        sym = (u.view(-1, *([1] * (ctx.dim() - 1)), 1) > table[ctx]).sum(-1).clamp_(max=3)
+        return ((ctx << 2) | sym) & 63, sym
+
     ctx = torch.arange(64, device=device).repeat(nseg, 1)  # [segment, entry context]
-    for _ in range(seg):
+    t = 0
+    t = min(coalesce_steps, seg)
+    for _ in range(t):
+        ctx, _ = step(ctx, torch.rand(nseg, generator=g, dtype=torch.float64, device=device))
+    coal = (ctx == ctx[:, :1]).all(1)
+    single = ctx[:, 0].clone()
+    rest = torch.nonzero(~coal).flatten()  # segments still tracked from every entry
+    full = ctx[rest]
+    for _ in range(t, seg):
         u = torch.rand(nseg, generator=g, dtype=torch.float64, device=device)
-        sym = (u[:, None, None] > table[ctx]).sum(2).clamp_(max=3)
-        ctx = ((ctx << 2) | sym) & 63
-    exit_of = ctx.cpu().numpy()
+        single, _ = step(single, u)
+        if rest.numel():
+            full, _ = step(full, u[rest])
+    exit_of = single.view(-1, 1).expand(nseg, 64).clone()
+    if rest.numel():
+        exit_of[rest] = full
+    exit_of = exit_of.cpu().numpy()
     entries = [0] * nseg
     c = head
     for k in range(nseg):
@@ -84,10 +104,8 @@ def _markov3_chain(g, n, device):
     ctx = torch.tensor(entries, device=device)
     buf = torch.empty((nseg, seg), dtype=torch.uint8, device=device)
     for t in range(seg):
-        u = torch.rand(nseg, generator=g, dtype=torch.float64, device=device)
-        sym = (u[:, None] > table[ctx]).sum(1).clamp_(max=3)
+        ctx, sym = step(ctx, torch.rand(nseg, generator=g, dtype=torch.float64, device=device))
         buf[:, t] = sym.to(torch.uint8)
-        ctx = ((ctx << 2) | sym) & 63
     return buf.view(-1)[:n]
 
 
