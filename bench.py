@@ -55,7 +55,8 @@ def code_width(sigma: int) -> int:
 
 
 def pass_plan(n: int, sym_bytes: int, sigma: int, kind: str):
-    """Mirror of the device plan (make_plan() / k8_eligible() in csrc): (level, K, in_bytes, out_bytes) per pass."""
+    """Mirror of the device plan (make_plan() / k8_eligible() in csrc): (level, K, in_bytes, out_bytes) per pass.
+    The fused stages (k8 / k16 / k32) get their first level from their counting kernel (hist8/16/32)."""
     w = code_width(sigma)
     if sym_bytes == 1 and 2 <= w <= 8 and 0 < n < (1 << 32) - 64:
         return [(0, w, 1, 0)]  # k8.cuh: every level in one fused pass
@@ -99,6 +100,31 @@ def stage_bytes(name: str, n: int, sym_bytes: int, sigma: int, kind: str) -> flo
         ell, K, ib, ob = pass_plan(n, sym_bytes, sigma, kind)[int(name[4:])]
         return n * ib + n * ob + K * ((n + 63) // 64) * 8
     return 0.0
+
+
+def fused_stage(plan_entry, n: int, sym_bytes: int, sigma: int, kind: str) -> bool:
+    """True for the fused k8 / k16 / k32 stages (their first level comes from the stage's counting kernel)."""
+    ell, K, ib, ob = plan_entry
+    w = code_width(sigma)
+    if sym_bytes == 1 and 2 <= w <= 8 and 0 < n < (1 << 32) - 64:
+        return True
+    fused = kind == "wm" and w > 8 and 0 < n < (1 << 32) - 64
+    return fused and ((ob == 0 and ib == 1 and w - ell <= 8) or (ib, ob) in ((4, 2), (2, 1)))
+
+
+def stage_levels(name: str, n: int, sym_bytes: int, sigma: int, kind: str) -> int:
+    """Levels a stage's kernel emits (SURVEY 8d charges n s + n/8 bytes per level)."""
+    plan = pass_plan(n, sym_bytes, sigma, kind)
+    if name.startswith("pass"):
+        e = plan[int(name[4:])]
+        return e[1] - (1 if fused_stage(e, n, sym_bytes, sigma, kind) else 0)
+    single = len(plan) == 1 and plan[0][2] == 1 and plan[0][3] == 0 and plan[0][0] == 0
+    if name == "hist":  # the byte path's counting kernel (hist8) writes level 0
+        return 1 if single and fused_stage(plan[0], n, sym_bytes, sigma, kind) else 0
+    if name.startswith("scan") and name[4:].isdigit():  # wide fused stages: counting kernel + tables, first level
+        p = int(name[4:])
+        return 1 if not single and p < len(plan) and fused_stage(plan[p], n, sym_bytes, sigma, kind) else 0
+    return 0
 
 
 def metric_bytes(n: int, sym_bytes: int, sigma: int) -> float:
@@ -383,10 +409,12 @@ def main():
     dominant = max((k for k in stages if k == "hist" or k.startswith("pass")), key=lambda k: stages[k])
     peak, peak_src = peaks()
     mbytes = metric_bytes(n, sym_bytes, sigma)
-    # SURVEY §8(d) bytes of the build (text read once per level + level bits)
-    # over the dominant kernel's own CUDA-event time: the fused pass emits the
-    # build (every level but level 0) in one kernel
-    achieved = mbytes / (stages[dominant] * 1e-3) / 1e9
+    # SURVEY §8(d)'s per-unit figure (s + 1/8 bytes per symbol per level, s the
+    # text's symbol bytes) times the units the dominant kernel processes per
+    # launch (n symbols x the levels it emits), over its CUDA-event time
+    dom_levels = stage_levels(dominant, n, sym_bytes, sigma, kind)
+    dom_8d = dom_levels * (n * sym_bytes + 8 * ((n + 63) // 64))
+    achieved = dom_8d / (stages[dominant] * 1e-3) / 1e9
     dom_bytes = stage_bytes(dominant, n, sym_bytes, sigma, kind)
     traffic = None
     tf = ROOT / "profiles" / f"ncu_traffic_{args.config}_{kind}.json"
@@ -421,9 +449,10 @@ def main():
                                    if world > 1 else "single")},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "kernel": dominant, "kernel_ms": stages[dominant],
-                     "algorithmic_bytes": mbytes,
-                     "definition": "SURVEY 8d bytes of the build, B = L (n s + n/8), over the dominant kernel's "
-                                   "CUDA-event time",
+                     "algorithmic_bytes": dom_8d, "levels": dom_levels,
+                     "definition": "SURVEY 8d per-unit bytes (s + 1/8 per symbol per level) x the n symbols x levels "
+                                   "the dominant kernel emits (its counting kernel emits the stage's first level), "
+                                   "over its CUDA-event time",
                      "physical": {"bytes": traffic, "frac": (traffic / (stages[dominant] * 1e-3) / 1e9 / peak)
                                   if traffic else None, "kernel_own_bytes": dom_bytes,
                                   "kernel_own_frac": dom_bytes / (stages[dominant] * 1e-3) / 1e9 / peak,

@@ -634,12 +634,12 @@ __global__ void __launch_bounds__(K8Cfg<Q>::NT, K8Cfg<Q>::CTAS) level_pass8_kern
   __shared__ __align__(8) uint64_t s_mbar;
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int64_t tile = blockIdx.x;
-  const int64_t base = tile * T;
-  const int cnt = (int)min((int64_t)T, a.n - base);
   const uint8_t* text = a.src;
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
   const uint32_t mbar = (uint32_t)__cvta_generic_to_shared(&s_mbar);
+  const int64_t tile = blockIdx.x;
+  const int64_t base = tile * T;
+  const int cnt = (int)min((int64_t)T, a.n - base);
   const bool bulk = (((uintptr_t)text) & 15) == 0 && cnt == T;
   if (tid == 0) {
     mbar_init(mbar, 1);
