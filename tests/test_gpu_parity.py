@@ -403,3 +403,28 @@ def test_allocation_ledger_of_real_builds(rng):
         assert log.position_entries > 0
         assert log.buffers("symbols") == [n] * nsym, (sigma, kind)
         assert bool(log.buffers("partial_bits")) == partial
+
+
+@pytest.mark.parametrize("kind", ["wt", "wm"])
+def test_borders_wider_storage_every_path(kind):
+    """Device builds with node borders over storage wider than the alphabet needs
+    (u16 / u32 texts with byte or 2-byte alphabets take the generic passes, not
+    the fused byte pass) and the byte fast path, all against oracle.borders."""
+    from paper_1702_07578_b200.device import DeviceBuilder
+
+    rng = np.random.default_rng(77)
+    b = DeviceBuilder()
+    for sigma, dt in [(5, torch.uint16), (256, torch.uint32), (1000, torch.uint32), (256, torch.uint8),
+                      (70000, torch.uint32), (2, torch.uint8), (3, torch.uint16)]:
+        n = 123_457
+        text = rng.integers(0, sigma, n).astype(np.int64)
+        t = torch.from_numpy(text).to(torch.int32).to(dt).cuda() if dt != torch.uint8 else \
+            torch.from_numpy(text.astype(np.uint8)).cuda()
+        res = b.build(t, sigma, kind, borders=True, histogram=True)
+        w = wv.code_width(sigma)
+        hist = oracle.histogram(text, sigma)
+        assert np.array_equal(res.hist.cpu().numpy(), hist), (sigma, dt)
+        if w >= 2:
+            assert np.array_equal(res.borders.cpu().numpy()[: (1 << w) - 2], oracle.borders(hist, w, kind)), (sigma, dt)
+        words, zeros, _ = oracle.build(text, sigma, kind, "pc")
+        assert np.array_equal(res.level_words.cpu().numpy().view(np.uint64), words), (sigma, dt)
