@@ -794,6 +794,11 @@ cudaError_t launch_pass8(const Pass8Args& a, void* tabs, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+#ifndef K8_QUAD
+#define K8_QUAD 1  // two levels per shared-memory round (k8q.cuh); 0: one level per round
+#endif
+#include "k8q.cuh"
+
 template <int W>
 cudaError_t launch_hist8(const uint8_t* text, int64_t n, int64_t ntiles, uint32_t vmax_ok, int check,
                          uint32_t* tcnt8, uint64_t* level0, int64_t nwords, int32_t* status, cudaStream_t s) {
@@ -913,15 +918,21 @@ int build_k8(const uint8_t* text, int64_t n, int64_t sigma, int w, int kind, uin
   if (e != cudaSuccess) return (int)e;
   ++g_launches;
   prof_mark(s, tail ? WVLT_STAGE_SCAN0 + tail_pass : WVLT_STAGE_TABLES);
+#if K8_QUAD
+#define K8_PASS launch_pass8q
+#else
+#define K8_PASS launch_pass8
+#endif
   switch (w) {
-    case 2: e = launch_pass8<2>(a, tabs, s); break;
-    case 3: e = launch_pass8<3>(a, tabs, s); break;
-    case 4: e = launch_pass8<4>(a, tabs, s); break;
-    case 5: e = launch_pass8<5>(a, tabs, s); break;
-    case 6: e = launch_pass8<6>(a, tabs, s); break;
-    case 7: e = launch_pass8<7>(a, tabs, s); break;
-    default: e = launch_pass8<8>(a, tabs, s); break;
+    case 2: e = K8_PASS<2>(a, tabs, s); break;
+    case 3: e = K8_PASS<3>(a, tabs, s); break;
+    case 4: e = K8_PASS<4>(a, tabs, s); break;
+    case 5: e = K8_PASS<5>(a, tabs, s); break;
+    case 6: e = K8_PASS<6>(a, tabs, s); break;
+    case 7: e = K8_PASS<7>(a, tabs, s); break;
+    default: e = K8_PASS<8>(a, tabs, s); break;
   }
+#undef K8_PASS
   if (e != cudaSuccess) return (int)e;
   ++g_launches;
   prof_mark(s, WVLT_STAGE_PASS0 + (tail ? tail_pass : 0));

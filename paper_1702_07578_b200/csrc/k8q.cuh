@@ -1,0 +1,304 @@
+// K8Q: the fused byte pass with TWO levels per shared-memory round.
+//
+// Same contract as level_pass8_kernel (k8.cuh): one CTA per K8_TILE-symbol
+// tile, every level's tile-local bits in shared memory, emitted at the end as
+// whole destination words.  What changes is how the tile-local orders are
+// produced.  A round starting at order A_j (bytes in shared memory):
+//
+//   * L_j   = the b_j flags of A_j                       (one byte per 8-symbol run)
+//   * A_j+2 = A_j stably sorted by the class c = 2 b_j+1 + b_j: ONE 4-way byte
+//             scatter instead of two 2-way ones (A_j+1 is never materialised)
+//   * L_j+1 = b_j+1 over A_j+1 = [b_j+1 of A_j's b_j-zeros] ++ [... of its ones]:
+//             each run already sorts its 8 bytes by b_j (PRMT) for the scatter,
+//             so its contribution is the run's sorted b_j+1 flags g split at its
+//             zero count z -- two bit pieces.  They are concatenated after the
+//             round by threads that own 4 CONSECUTIVE runs (lane-sequential
+//             shifts into a 32-bit accumulator per stream, then one OR per
+//             stream word into the level's bit array), instead of a bit scatter
+//             per run.
+//
+// Per two levels this halves the byte scatters (the shared-memory store
+// wavefronts that bound the one-level-per-round kernel), at the price of a
+// second PRMT sort, a 3-class count scan and the concatenation.  The last
+// round of an even width only emits L_W-2 and L_W-1 (no scatter), the last of
+// an odd width only L_W-1.
+//
+// 4-way store addressing: the class-sorted run's byte kk goes to
+// D[c(kk)] + kk, with the four per-run bases D (16-bit offsets into the two
+// stage buffers, all < 2 T = 32768) packed in two registers; one PRMT builds a
+// byte's selector from its 2-bit class (nibbles 2c', 2c'+1, and 9 = the sign
+// of a high byte < 0x80, i.e. zero, for the upper half), one PRMT looks the
+// base up.  The shared window offset of the buffers rides in the store's
+// immediate.
+//
+// Included from k8.cuh (same translation unit, anonymous namespace).
+
+template <int W>
+struct Q8Smem {
+  static constexpr int T = K8_TILE;
+  static constexpr int NC = T / 32;
+  static constexpr size_t tab = 2 * (size_t)T;                              // after the ping-pong orders
+  static constexpr size_t bits = tab + sizeof(TabW<W>);                     // levels 1..W-1, NC + 4 words each
+  static constexpr size_t gbuf = bits + (size_t)(W - 1) * (NC + 4) * 4;    // 2 x T/8 run flag bytes
+  static constexpr size_t za = gbuf + 2 * (size_t)(T / 8);                  // T/32 u16: zero prefix per 4 runs
+  static constexpr size_t tot = za + (size_t)(T / 32) * 2;                  // [4][16] uint2 warp totals
+  static constexpr size_t lut = tot + 4 * 16 * 8;                           // 256 sort selectors
+  static constexpr size_t mbar = lut + 1024;
+  static constexpr size_t total = mbar + 16;
+};
+
+// The 8 flags of bit `sh` of a run's bytes (x0: bytes 0-3, x1: bytes 4-7).
+// `bits` gets the flag bits in place (for POPC); the return value holds the
+// 8-bit mask in its low byte with garbage above (`flags_lo` cleans it): one
+// multiply gathers the flags (bits 8i and 8i + 4 -> bit i), the high word of a
+// second one shifts them down, so only the two masks use the integer ALU.
+__device__ __forceinline__ uint32_t run_flags8(uint32_t x0, uint32_t x1, int sh, uint32_t& bits) {
+  const uint32_t M = 0x01010101u << sh;
+  // flag of byte i at bit 8i + p, of byte 4 + i at bit 8i + 4 + p (p = sh, or
+  // sh - 4 with bytes 0-3 moved down by a multiply so nothing leaves the word)
+  const int p = sh >= 4 ? sh - 4 : sh;
+  bits = sh >= 4 ? __umulhi(x0 & M, 1u << 28) + (x1 & M) : (x1 & M) * 16u + (x0 & M);
+  if (p == 0) return (bits * 0x01020408u) >> 24;
+  return __umulhi(bits, 0x01020408u << (8 - p));
+}
+__device__ __forceinline__ uint32_t flags_lo(uint32_t f) { return f & 0xFFu; }
+
+// OR a bit string v (its length implied: bits above it are zero) into L at bit pos
+__device__ __forceinline__ void or_bits32(uint32_t* L, uint32_t pos, uint32_t v) {
+  if (!v) return;
+  const uint32_t w = pos >> 5, s = pos & 31;
+  atomicOr(L + w, v << s);
+  if (s) {
+    const uint32_t hi = v >> (32 - s);
+    if (hi) atomicOr(L + w + 1, hi);
+  }
+}
+
+template <int W>
+__global__ void __launch_bounds__(K8_TILE / 32, K8_CTAS) level_pass8q_kernel(const Pass8Args a,
+                                                                            const TabW<W>* __restrict__ tabs) {
+  constexpr int T = K8_TILE;
+  constexpr int Q = 4;           // runs per thread (one per region)
+  constexpr int NT = T / (8 * Q);
+  constexpr int R = T / Q;       // region of run k
+  constexpr int RR = R / 8;      // runs per region
+  constexpr int NC = T / 32;
+  constexpr int NW = NT / 32;
+  using L = Q8Smem<W>;
+  static_assert(NW <= 32 && 2 * T <= 32768, "16-bit store bases");
+  extern __shared__ __align__(128) unsigned char smem[];
+  TabW<W>& tt = *reinterpret_cast<TabW<W>*>(smem + L::tab);
+  uint32_t* bits = reinterpret_cast<uint32_t*>(smem + L::bits) - (NC + 4);  // level j at j (NC + 4)
+  uint8_t* bits8 = reinterpret_cast<uint8_t*>(bits);
+  uint16_t* za16 = reinterpret_cast<uint16_t*>(smem + L::za);
+  uint2* s_tot = reinterpret_cast<uint2*>(smem + L::tot);
+  uint32_t* s_lut = reinterpret_cast<uint32_t*>(smem + L::lut);
+
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const uint8_t* text = a.src;
+  const uint32_t sb = (uint32_t)__cvta_generic_to_shared(smem);
+  const uint32_t mbar = sb + (uint32_t)L::mbar;
+  const int64_t tile = blockIdx.x;
+  const int64_t base = tile * T;
+  const int cnt = (int)min((int64_t)T, a.n - base);
+  const bool bulk = (((uintptr_t)text) & 15) == 0 && cnt == T;
+  if (tid == 0) {
+    mbar_init(mbar, 1);
+    fence_mbar_init();
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar),
+                 "r"((uint32_t)(sizeof(TabW<W>) + (bulk ? T : 0)))
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     sb + (uint32_t)L::tab),
+                 "l"(tabs + tile), "r"((uint32_t)sizeof(TabW<W>)), "r"(mbar)
+                 : "memory");
+    if (bulk)
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(sb),
+                   "l"(text + base), "r"((uint32_t)T), "r"(mbar)
+                   : "memory");
+  }
+  for (int i = tid; i < 256; i += NT) s_lut[i] = g_sort_lut.sel[i];
+  // the levels filled by OR-ing bit strings (odd levels: the skipped level of
+  // every round) start at zero
+#pragma unroll
+  for (int j = 1; j < W; j += 2)
+    for (int i = tid; i < NC + 4; i += NT) bits[j * (NC + 4) + i] = 0u;
+  if (!bulk)
+    for (int p = tid; p < T; p += NT) smem[p] = p < cnt ? text[base + p] : (uint8_t)0xFF;
+  bar_sync(1, NT);
+  mbar_wait(mbar, 0);
+
+  // level 0's flags (hist8_kernel emits level 0) are only needed for round 0's
+  // concatenation: they go to a scratch that is free until later -- level W-1's
+  // array (re-zeroed after use when W-1 is an OR-ed level), or for W = 2 the
+  // second flag buffer
+  uint8_t* const m0b = W == 2 ? smem + L::gbuf + T / 8 : bits8 + (W - 1) * 4 * (NC + 4);
+
+#pragma unroll
+  for (int j = 0; j < W; j += 2) {
+    const int sh = W - 1 - j;
+    const uint8_t* cur = smem + (size_t)((j >> 1) & 1) * T;
+    uint8_t* mb = j == 0 ? m0b : bits8 + j * 4 * (NC + 4);
+    if (j == W - 1) {  // odd width: the last level's flags only
+#pragma unroll
+      for (int k = 0; k < Q; ++k) {
+        const uint2 qv = reinterpret_cast<const uint2*>(cur + k * R)[tid];
+        uint32_t fb;
+        mb[k * RR + tid] = (uint8_t)run_flags8(qv.x, qv.y, 0, fb);
+      }
+      break;
+    }
+    const bool quad = j + 2 < W;
+    uint8_t* gb = smem + L::gbuf + (size_t)((j >> 1) & 1) * (T / 8);
+    uint32_t cq[Q], iq[Q];
+    uint32_t ones[Q];
+#pragma unroll
+    for (int k = 0; k < Q; ++k) {
+      const uint2 qv = reinterpret_cast<const uint2*>(cur + k * R)[tid];
+      uint32_t mbits, gbits;
+      const uint32_t m = run_flags8(qv.x, qv.y, sh, mbits);
+      mb[k * RR + tid] = (uint8_t)m;
+      const uint32_t sel = s_lut[flags_lo(m)];
+      const uint32_t s0 = prmt(qv.x, qv.y, sel), s1 = prmt(qv.x, qv.y, sel >> 16);
+      const uint32_t g = run_flags8(s0, s1, sh - 1, gbits);
+      gb[k * RR + tid] = (uint8_t)g;
+      if (quad) {
+        const uint32_t sel2 = s_lut[flags_lo(g)];
+        // the class-sorted run goes back to its own slot (read again after
+        // the barrier: fewer live registers than keeping all Q runs)
+        reinterpret_cast<uint2*>(const_cast<uint8_t*>(cur) + k * R)[tid] =
+            make_uint2(prmt(s0, s1, sel2), prmt(s0, s1, sel2 >> 16));
+        // class counts n0..n3 (c = 2 b_j+1 + b_j) as bytes: z = n0 + n1 (b_j
+        // zeros), n2 = the zeros' b_j+1 ones, n3 = the ones' b_j+1 ones
+        const uint32_t z = 8u - __popc(mbits);
+        const uint32_t n2 = __popc(g & ((1u << z) - 1u));
+        const uint32_t n3 = __popc(gbits) - n2;
+        // n0 + n1 2^8 + n2 2^16 + n3 2^24 with n0 = z - n2, n1 = 8 - z - n3 (mod 2^32)
+        cq[k] = z * 0xFFFFFF01u + 0x800u + n2 * 0xFFFFu + n3 * 0xFFFF00u;
+        // exclusive warp scan by bytes (every prefix <= 31 * 8 < 256)
+        iq[k] = warp_incl_scan(__shfl_up_sync(FULL, cq[k], 1) & (lane ? 0xFFFFFFFFu : 0u));
+        if (lane == 31) {  // warp totals as 16-bit pairs (a class may reach 256)
+          const uint32_t t02 = prmt(iq[k], 0u, 0x4240u) + prmt(cq[k], 0u, 0x4240u);
+          const uint32_t t13 = prmt(iq[k], 0u, 0x4341u) + prmt(cq[k], 0u, 0x4341u);
+          s_tot[k * NW + wid] = make_uint2(t02, t13);
+        }
+      } else {
+        ones[k] = __popc(mbits);
+      }
+    }
+    uint32_t Zt;  // the tile's b_j zeros: where L_j+1's ones stream starts
+    if (quad) {
+      bar_sync(1, NT);
+      // class totals of the tile (classes 0, 1 packed 16|16, class 2) and the
+      // class starts C_c of A_j+2
+      // (lane l < NW holds warp l's totals; per-lane sums over the regions
+      // turn every prefix into one REDUX)
+      uint32_t sx = 0, sy = 0;
+#pragma unroll
+      for (int k = 0; k < Q; ++k) {
+        const uint2 v = lane < NW ? s_tot[k * NW + lane] : make_uint2(0u, 0u);
+        sx += v.x;
+        sy += v.y;
+      }
+      const uint32_t T02 = __reduce_add_sync(FULL, sx), T13 = __reduce_add_sync(FULL, sy);
+      const uint32_t C1 = T02 & 0xFFFFu, C2 = C1 + (T13 & 0xFFFFu), C3 = C2 + (T02 >> 16);
+      Zt = (T02 & 0xFFFFu) + (T02 >> 16);  // classes 0 and 2: b_j = 0
+      const uint32_t dst = (uint32_t)(((j >> 1) + 1) & 1) * T * 0x10001u;
+      const uint32_t CA = dst + (C2 << 16), CB = dst + (C1 | (C3 << 16));
+      uint32_t ax = 0, ay = 0;  // this lane's warp over the regions before
+#pragma unroll
+      for (int k = 0; k < Q; ++k) {
+        const uint2 v = lane < NW ? s_tot[k * NW + lane] : make_uint2(0u, 0u);
+        const uint32_t A02 = __reduce_add_sync(FULL, ax + (lane < wid ? v.x : 0u));
+        const uint32_t A13 = __reduce_add_sync(FULL, ay + (lane < wid ? v.y : 0u));
+        ax += v.x;
+        ay += v.y;
+        // the run's class c base minus the class's start inside the sorted run,
+        // as 16-bit pairs (D0 | D2 << 16, D1 | D3 << 16): c's global start +
+        // regions / warps before + this lane's exclusive prefix - the run's
+        // classes before c
+        const uint32_t e = iq[k], sv = cq[k] * 0x01010100u;
+        const uint32_t E02 = prmt(e, 0u, 0x4240u) + A02;
+        const uint32_t DA = CA + E02 - prmt(sv, 0u, 0x4240u);
+        const uint32_t DB = CB + A13 + prmt(e, 0u, 0x4341u) - prmt(sv, 0u, 0x4341u);
+        if ((tid & 3) == 0) za16[(k * RR + tid) >> 2] = (uint16_t)((E02 * 0x10001u) >> 16);  // b_j zeros before
+        const uint2 uk = reinterpret_cast<const uint2*>(cur + k * R)[tid];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t w = h ? uk.y : uk.x;
+          const uint32_t x = w >> (sh - 1);
+          // PRMT selectors of bytes 0, 2 and 1, 3: nibbles 2c', 2c'+1 pick the
+          // byte's 16-bit base (c' = 2 b_j + b_j+1), 0x99 zero-fills the top half
+          const uint32_t s02 = (x & 0x00030003u) * 0x22u + 0x99109910u;
+          const uint32_t s13 = __umulhi(x & 0x03000300u, 0x22000000u) + 0x99109910u;
+          const uint32_t a0 = prmt(DA, DB, s02), a1 = prmt(DA, DB, s13);
+          const uint32_t a2 = prmt(DA, DB, __umulhi(s02, 0x10000u)), a3 = prmt(DA, DB, __umulhi(s13, 0x10000u));
+          asm volatile("st.shared.u8 [%0], %1;" ::"r"(a0 + sb + (uint32_t)(4 * h)), "r"(w) : "memory");
+          asm volatile("st.shared.u8 [%0], %1;" ::"r"(a1 + sb + (uint32_t)(4 * h + 1)), "r"(__umulhi(w, 1u << 24)) : "memory");
+          asm volatile("st.shared.u8 [%0], %1;" ::"r"(a2 + sb + (uint32_t)(4 * h + 2)), "r"(__umulhi(w, 1u << 16)) : "memory");
+          asm volatile("st.shared.u8 [%0], %1;" ::"r"(a3 + sb + (uint32_t)(4 * h + 3)), "r"(__umulhi(w, 1u << 8)) : "memory");
+        }
+      }
+    } else {
+      // last round of an even width: a 2-way count scan for L_W-1's pieces
+      constexpr int P = Q / 2;
+      uint32_t incl[P];
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        const uint32_t pk = ones[2 * p] | (ones[2 * p + 1] << 16);
+        incl[p] = warp_incl_scan(pk);
+        if (lane == 31) s_tot[p * NW + wid].x = incl[p];
+        incl[p] -= pk;
+      }
+      bar_sync(1, NT);
+      uint32_t run_tot = 0;
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        const uint32_t wv = lane < NW ? s_tot[p * NW + lane].x : 0u;
+        const uint32_t ex = __reduce_add_sync(FULL, lane < wid ? wv : 0u) + incl[p];
+        const uint32_t tot = __reduce_add_sync(FULL, wv);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int k = 2 * p + h;
+          const uint32_t opre = run_tot + (h ? ex >> 16 : ex & 0xFFFFu);
+          if ((tid & 3) == 0) za16[(k * RR + tid) >> 2] = (uint16_t)((uint32_t)(k * R + 8 * tid) - opre);
+          run_tot += h ? tot >> 16 : tot & 0xFFFFu;
+        }
+      }
+      Zt = (uint32_t)T - run_tot;
+    }
+    bar_sync(1, NT);
+    // L_j+1 from the runs' flag pieces: thread t owns runs 4t .. 4t+3
+    {
+      const uint32_t gw = reinterpret_cast<const uint32_t*>(gb)[tid];
+      uint32_t* mwp = reinterpret_cast<uint32_t*>(mb) + tid;
+      const uint32_t mw = *mwp;
+      if (j == 0 && W >= 4 && (W & 1) == 0) *mwp = 0u;  // level W-1 (OR-ed later) lent its array
+      const uint32_t zpos = za16[tid];
+      uint32_t accz = 0, acco = 0, fz = 0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint32_t g = (gw >> (8 * i)) & 0xFFu;
+        const uint32_t z = 8u - __popc((mw >> (8 * i)) & 0xFFu);
+        accz |= (g & ((1u << z) - 1u)) << fz;
+        acco |= (g >> z) << (8u * i - fz);
+        fz += z;
+      }
+      uint32_t* Lw = bits + (j + 1) * (NC + 4);
+      or_bits32(Lw, zpos, accz);
+      or_bits32(Lw, Zt + 32u * tid - zpos, acco);
+    }
+  }
+  bar_sync(1, NT);  // every level's bits are in place
+  emit_levels8<W, NC>(tt, bits, a.words, a.nwords, tid, NT, smem);  // stage buffers are free now
+}
+
+template <int W>
+cudaError_t launch_pass8q(const Pass8Args& a, void* tabs, cudaStream_t s) {
+  constexpr size_t smem = Q8Smem<W>::total;
+  auto kern = level_pass8q_kernel<W>;
+  cudaError_t e0 = ensure_smem_attr((const void*)kern, (int)smem, true);
+  if (e0 != cudaSuccess) return e0;
+  kern<<<(unsigned)a.ntiles, K8_TILE / 32, smem, s>>>(a, (const TabW<W>*)tabs);
+  return cudaGetLastError();
+}
