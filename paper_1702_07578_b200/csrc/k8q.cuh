@@ -24,12 +24,12 @@
 // an odd width only L_W-1.
 //
 // 4-way store addressing: the class-sorted run's byte kk goes to
-// D[c(kk)] + kk, with the four per-run bases D (16-bit offsets into the two
-// stage buffers, all < 2 T = 32768) packed in two registers; one PRMT builds a
+// D[c(kk)] + kk, with the four per-run bases D (16-bit offsets inside the
+// destination buffer, < T <= 32768) packed in two registers; one PRMT builds a
 // byte's selector from its 2-bit class (nibbles 2c', 2c'+1, and 9 = the sign
 // of a high byte < 0x80, i.e. zero, for the upper half), one PRMT looks the
-// base up.  The shared window offset of the buffers rides in the store's
-// immediate.
+// base up.  The buffer's shared-window address rides in the store's
+// uniform-register + immediate operands.
 //
 // Included from k8.cuh (same translation unit, anonymous namespace).
 
@@ -41,8 +41,8 @@ struct Q8Smem {
   static constexpr size_t bits = tab + sizeof(TabW<W>);                     // levels 1..W-1, NC + 4 words each
   static constexpr size_t gbuf = bits + (size_t)(W - 1) * (NC + 4) * 4;    // 2 x T/8 run flag bytes
   static constexpr size_t za = gbuf + 2 * (size_t)(T / 8);                  // T/32 u16: zero prefix per 4 runs
-  static constexpr size_t tot = za + (size_t)(T / 32) * 2;                  // [4][16] uint2 warp totals
-  static constexpr size_t lut = tot + 4 * 16 * 8;                           // 256 sort selectors
+  static constexpr size_t tot = za + (size_t)(T / 32) * 2;                  // [4 regions][warps] uint2 warp totals
+  static constexpr size_t lut = tot + 4 * (size_t)(T / 1024) * 8;          // 256 sort selectors
   static constexpr size_t mbar = lut + 1024;
   static constexpr size_t total = mbar + 16;
 };
@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(K8_TILE / 32, K8_CTAS) level_pass8q_kernel(con
   constexpr int NC = T / 32;
   constexpr int NW = NT / 32;
   using L = Q8Smem<W>;
-  static_assert(NW <= 32 && 2 * T <= 32768, "16-bit store bases");
+  static_assert(NW <= 32 && T <= 32768, "16-bit store bases (offsets inside the destination buffer)");
   extern __shared__ __align__(128) unsigned char smem[];
   TabW<W>& tt = *reinterpret_cast<TabW<W>*>(smem + L::tab);
   uint32_t* bits = reinterpret_cast<uint32_t*>(smem + L::bits) - (NC + 4);  // level j at j (NC + 4)
@@ -175,8 +175,8 @@ __global__ void __launch_bounds__(K8_TILE / 32, K8_CTAS) level_pass8q_kernel(con
         const uint32_t n3 = __popc(gbits) - n2;
         // n0 + n1 2^8 + n2 2^16 + n3 2^24 with n0 = z - n2, n1 = 8 - z - n3 (mod 2^32)
         cq[k] = z * 0xFFFFFF01u + 0x800u + n2 * 0xFFFFu + n3 * 0xFFFF00u;
-        // exclusive warp scan by bytes (every prefix <= 31 * 8 < 256)
-        iq[k] = warp_incl_scan(__shfl_up_sync(FULL, cq[k], 1) & (lane ? 0xFFFFFFFFu : 0u));
+        // exclusive warp scan by bytes (every exclusive prefix <= 31 * 8 < 256)
+        iq[k] = warp_incl_scan(cq[k]) - cq[k];  // exact as integers even where a byte of the inclusive sum carries
         if (lane == 31) {  // warp totals as 16-bit pairs (a class may reach 256)
           const uint32_t t02 = prmt(iq[k], 0u, 0x4240u) + prmt(cq[k], 0u, 0x4240u);
           const uint32_t t13 = prmt(iq[k], 0u, 0x4341u) + prmt(cq[k], 0u, 0x4341u);
@@ -203,8 +203,8 @@ __global__ void __launch_bounds__(K8_TILE / 32, K8_CTAS) level_pass8q_kernel(con
       const uint32_t T02 = __reduce_add_sync(FULL, sx), T13 = __reduce_add_sync(FULL, sy);
       const uint32_t C1 = T02 & 0xFFFFu, C2 = C1 + (T13 & 0xFFFFu), C3 = C2 + (T02 >> 16);
       Zt = (T02 & 0xFFFFu) + (T02 >> 16);  // classes 0 and 2: b_j = 0
-      const uint32_t dst = (uint32_t)(((j >> 1) + 1) & 1) * T * 0x10001u;
-      const uint32_t CA = dst + (C2 << 16), CB = dst + (C1 | (C3 << 16));
+      const uint32_t dst = sb + (uint32_t)(((j >> 1) + 1) & 1) * T;  // destination buffer (store immediates)
+      const uint32_t CA = C2 << 16, CB = C1 | (C3 << 16);
       uint32_t ax = 0, ay = 0;  // this lane's warp over the regions before
 #pragma unroll
       for (int k = 0; k < Q; ++k) {
@@ -233,10 +233,10 @@ __global__ void __launch_bounds__(K8_TILE / 32, K8_CTAS) level_pass8q_kernel(con
           const uint32_t s13 = __umulhi(x & 0x03000300u, 0x22000000u) + 0x99109910u;
           const uint32_t a0 = prmt(DA, DB, s02), a1 = prmt(DA, DB, s13);
           const uint32_t a2 = prmt(DA, DB, __umulhi(s02, 0x10000u)), a3 = prmt(DA, DB, __umulhi(s13, 0x10000u));
-          asm volatile("st.shared.u8 [%0], %1;" ::"r"(a0 + sb + (uint32_t)(4 * h)), "r"(w) : "memory");
-          asm volatile("st.shared.u8 [%0], %1;" ::"r"(a1 + sb + (uint32_t)(4 * h + 1)), "r"(__umulhi(w, 1u << 24)) : "memory");
-          asm volatile("st.shared.u8 [%0], %1;" ::"r"(a2 + sb + (uint32_t)(4 * h + 2)), "r"(__umulhi(w, 1u << 16)) : "memory");
-          asm volatile("st.shared.u8 [%0], %1;" ::"r"(a3 + sb + (uint32_t)(4 * h + 3)), "r"(__umulhi(w, 1u << 8)) : "memory");
+          asm volatile("st.shared.u8 [%0], %1;" ::"r"(a0 + dst + (uint32_t)(4 * h)), "r"(w) : "memory");
+          asm volatile("st.shared.u8 [%0], %1;" ::"r"(a1 + dst + (uint32_t)(4 * h + 1)), "r"(__umulhi(w, 1u << 24)) : "memory");
+          asm volatile("st.shared.u8 [%0], %1;" ::"r"(a2 + dst + (uint32_t)(4 * h + 2)), "r"(__umulhi(w, 1u << 16)) : "memory");
+          asm volatile("st.shared.u8 [%0], %1;" ::"r"(a3 + dst + (uint32_t)(4 * h + 3)), "r"(__umulhi(w, 1u << 8)) : "memory");
         }
       }
     } else {
