@@ -420,17 +420,30 @@ def main():
     tf = ROOT / "profiles" / f"ncu_traffic_{args.config}_{kind}.json"
     if tf.exists():
         traffic = json.loads(tf.read_text()).get(dominant)
-    # the fused pass is bound by the shared-memory pipe, not HBM: its ncu wavefront
-    # count per launch over (SMs x cycles of its CUDA-event duration at the sampled clock)
+    # the fused pass is not HBM-bound: its limiter comes from the same ncu capture
+    # -- shared-memory wavefronts per SM per cycle of its CUDA-event duration at
+    # the sampled clock, next to ncu's L1, issue-slot and ALU-pipe utilisation;
+    # the busiest of these is reported as the resource
     limiter = None
     sf = ROOT / "profiles" / f"ncu_smem_{args.config}_{kind}.json"
     if sf.exists() and clocks.get("sm_mhz"):
-        wf = json.loads(sf.read_text()).get(dominant)
-        if wf:
+        rec = json.loads(sf.read_text()).get(dominant)
+        if isinstance(rec, (int, float)):
+            rec = {"smem_wavefronts": rec}
+        if rec and rec.get("smem_wavefronts"):
             sms = torch.cuda.get_device_properties(dev).multi_processor_count
+            wf = rec["smem_wavefronts"]
             per_cycle = wf / (sms * stages[dominant] * 1e-3 * clocks["sm_mhz"] * 1e6)
-            limiter = {"resource": "shared-memory pipe", "unit": "wavefronts / SM / cycle", "achieved": per_cycle,
-                       "peak": 1.0, "frac": per_cycle, "wavefronts_per_launch": wf,
+            util = {"shared-memory pipe (wavefronts / SM / cycle)": per_cycle}
+            if rec.get("issue_pct") is not None:
+                util["instruction issue (ncu issue-active)"] = rec["issue_pct"] / 100
+            if rec.get("l1_pct") is not None:
+                util["L1 / shared-memory throughput (ncu)"] = rec["l1_pct"] / 100
+            if rec.get("alu_pct") is not None:
+                util["integer ALU pipe (ncu)"] = rec["alu_pct"] / 100
+            res = max(util, key=util.get)
+            limiter = {"resource": res, "frac": util[res], "utilisation": util, "wavefronts_per_launch": wf,
+                       "inst_executed_per_launch": rec.get("inst_executed"),
                        "source": f"profiles/ncu_smem_{args.config}_{kind}.json (ncu --set full, one launch)"}
 
     value = world * n / (ms * 1e-3)

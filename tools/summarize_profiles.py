@@ -20,7 +20,7 @@ out.mkdir(exist_ok=True)
 
 
 def short(name):
-    for k in ("hist8_kernel", "tiles8_kernel", "level_pass8_kernel", "scan8_chunks_kernel", "scan8_carry_kernel",
+    for k in ("hist8_kernel", "tiles8_kernel", "level_pass8q_kernel", "level_pass8_kernel", "scan8_chunks_kernel", "scan8_carry_kernel",
               "scan8_apply_kernel", "tables8_kernel",
               "hist_u8_kernel", "hist_generic_kernel", "digits_fast_kernel", "digits_kernel", "wm_pass_tables_kernel", "tables_kernel", "scan_reduce_kernel",
               "scan_apply_kernel", "level_pass_u8_kernel", "level_pass_kernel", "merge_bits_kernel", "widen_kernel"):
@@ -98,7 +98,12 @@ for r in full:
                  f"{r['l1tex__data_pipe_lsu_wavefronts_mem_shared.sum']} | {r['l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum']} | {r['launch__registers_per_thread']} |")
     if "level_pass" in name:
         traffic[f"pass{pass_idx}"] = (rd + wr) * 1e6
-        smem[f"pass{pass_idx}"] = float(r["l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"].replace(",", ""))
+        fnum = lambda k: float(r[k].replace(",", "")) if r.get(k) not in (None, "", "n/a") else None
+        smem[f"pass{pass_idx}"] = {"smem_wavefronts": fnum("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"),
+                                   "l1_pct": fnum("l1tex__throughput.avg.pct_of_peak_sustained_active"),
+                                   "issue_pct": fnum("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                                   "alu_pct": fnum("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active"),
+                                   "inst_executed": fnum("smsp__inst_executed.sum")}
         pass_idx += 1
     elif "hist" in name or "digits" in name:
         traffic["hist"] = (rd + wr) * 1e6
@@ -106,6 +111,6 @@ for r in full:
         traffic["tiles8"] = (rd + wr) * 1e6
 (out / f"{tag}_summary.md").write_text("\n".join(lines) + "\n")
 json.dump(traffic, open(out / "ncu_traffic_c2_wm.json", "w"), indent=1)
-json.dump(smem, open(out / "ncu_smem_c2_wm.json", "w"), indent=1)  # shared-memory wavefronts per launch
+json.dump(smem, open(out / "ncu_smem_c2_wm.json", "w"), indent=1)  # per launch: smem wavefronts, L1 / issue / ALU utilisation
 print("\n".join(lines))
 print(traffic)
