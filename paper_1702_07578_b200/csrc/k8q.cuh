@@ -63,15 +63,13 @@ __device__ __forceinline__ uint32_t run_flags8(uint32_t x0, uint32_t x1, int sh,
 }
 __device__ __forceinline__ uint32_t flags_lo(uint32_t f) { return f & 0xFFu; }
 
-// OR a bit string v (its length implied: bits above it are zero) into L at bit pos
+// OR a bit string v (its length implied: bits above it are zero) into L at
+// bit pos; branch-free (two predicated shared atomics)
 __device__ __forceinline__ void or_bits32(uint32_t* L, uint32_t pos, uint32_t v) {
-  if (!v) return;
-  const uint32_t w = pos >> 5, s = pos & 31;
-  atomicOr(L + w, v << s);
-  if (s) {
-    const uint32_t hi = v >> (32 - s);
-    if (hi) atomicOr(L + w + 1, hi);
-  }
+  const uint64_t t = (uint64_t)v << (pos & 31);
+  uint32_t* w = L + (pos >> 5);
+  if ((uint32_t)t) atomicOr(w, (uint32_t)t);
+  if ((uint32_t)(t >> 32)) atomicOr(w + 1, (uint32_t)(t >> 32));
 }
 
 template <int W>
@@ -177,17 +175,18 @@ __global__ void __launch_bounds__(K8_TILE / 32, K8_CTAS) level_pass8q_kernel(con
         cq[k] = z * 0xFFFFFF01u + 0x800u + n2 * 0xFFFFu + n3 * 0xFFFF00u;
         // exclusive warp scan by bytes (every exclusive prefix <= 31 * 8 < 256)
         iq[k] = warp_incl_scan(cq[k]) - cq[k];  // exact as integers even where a byte of the inclusive sum carries
-        if (lane == 31) {  // warp totals as 16-bit pairs (a class may reach 256)
-          const uint32_t t02 = prmt(iq[k], 0u, 0x4240u) + prmt(cq[k], 0u, 0x4240u);
-          const uint32_t t13 = prmt(iq[k], 0u, 0x4341u) + prmt(cq[k], 0u, 0x4341u);
-          s_tot[k * NW + wid] = make_uint2(t02, t13);
-        }
       } else {
         ones[k] = __popc(mbits);
       }
     }
     uint32_t Zt;  // the tile's b_j zeros: where L_j+1's ones stream starts
     if (quad) {
+      if (lane == 31) {  // warp totals per region as 16-bit pairs (a class may reach 256)
+#pragma unroll
+        for (int k = 0; k < Q; ++k)
+          s_tot[k * NW + wid] = make_uint2(prmt(iq[k], 0u, 0x4240u) + prmt(cq[k], 0u, 0x4240u),
+                                           prmt(iq[k], 0u, 0x4341u) + prmt(cq[k], 0u, 0x4341u));
+      }
       bar_sync(1, NT);
       // class totals of the tile (classes 0, 1 packed 16|16, class 2) and the
       // class starts C_c of A_j+2
@@ -229,8 +228,9 @@ __global__ void __launch_bounds__(K8_TILE / 32, K8_CTAS) level_pass8q_kernel(con
           const uint32_t x = w >> (sh - 1);
           // PRMT selectors of bytes 0, 2 and 1, 3: nibbles 2c', 2c'+1 pick the
           // byte's 16-bit base (c' = 2 b_j + b_j+1), 0x99 zero-fills the top half
-          const uint32_t s02 = (x & 0x00030003u) * 0x22u + 0x99109910u;
-          const uint32_t s13 = __umulhi(x & 0x03000300u, 0x22000000u) + 0x99109910u;
+          // (0x22 c' has no bit of 0x10 / 0x99 set: OR adds them, no constant register)
+          const uint32_t s02 = ((x & 0x00030003u) * 0x22u) | 0x99109910u;
+          const uint32_t s13 = __umulhi(x & 0x03000300u, 0x22000000u) | 0x99109910u;
           const uint32_t a0 = prmt(DA, DB, s02), a1 = prmt(DA, DB, s13);
           const uint32_t a2 = prmt(DA, DB, __umulhi(s02, 0x10000u)), a3 = prmt(DA, DB, __umulhi(s13, 0x10000u));
           asm volatile("st.shared.u8 [%0], %1;" ::"r"(a0 + dst + (uint32_t)(4 * h)), "r"(w) : "memory");
