@@ -119,8 +119,9 @@ __global__ void __launch_bounds__(K8_TILE / 32, K8_CTAS) level_pass8q_kernel(con
   // the levels filled by OR-ing bit strings (odd levels: the skipped level of
   // every round) start at zero
 #pragma unroll
-  for (int j = 1; j < W; j += 2)
-    for (int i = tid; i < NC + 4; i += NT) bits[j * (NC + 4) + i] = 0u;
+  for (int j = 1; j < W; ++j)
+    if ((j & 1) || ((W & 1) && j == W - 1 && W >= 3))  // (odd W: the last round ORs level W-1 too)
+      for (int i = tid; i < NC + 4; i += NT) bits[j * (NC + 4) + i] = 0u;
   if (!bulk)
     for (int p = tid; p < T; p += NT) smem[p] = p < cnt ? text[base + p] : (uint8_t)0xFF;
   bar_sync(1, NT);
@@ -128,9 +129,9 @@ __global__ void __launch_bounds__(K8_TILE / 32, K8_CTAS) level_pass8q_kernel(con
 
   // level 0's flags (hist8_kernel emits level 0) are only needed for round 0's
   // concatenation: they go to a scratch that is free until later -- level W-1's
-  // array (re-zeroed after use when W-1 is an OR-ed level), or for W = 2 the
-  // second flag buffer
-  uint8_t* const m0b = W == 2 ? smem + L::gbuf + T / 8 : bits8 + (W - 1) * 4 * (NC + 4);
+  // array (re-zeroed after use: W-1 is an OR-ed level for every W >= 4), for
+  // W = 2 the second flag buffer, for W = 3 the stage buffer round 0 leaves unused
+  uint8_t* const m0b = W == 2 ? smem + L::gbuf + T / 8 : W == 3 ? smem + T : bits8 + (W - 1) * 4 * (NC + 4);
 
 #pragma unroll
   for (int j = 0; j < W; j += 2) {
@@ -146,8 +147,16 @@ __global__ void __launch_bounds__(K8_TILE / 32, K8_CTAS) level_pass8q_kernel(con
       }
       break;
     }
-    const bool quad = j + 2 < W;
+    // odd width: the last round starts at A_W-3 and emits three levels without a
+    // scatter -- L_W-2 and L_W-1 are concatenated from the runs' 2- and 4-class pieces
+    const bool triple = (W & 1) && j + 3 == W;
+    const bool quad = j + 2 < W && !triple;
     uint8_t* gb = smem + L::gbuf + (size_t)((j >> 1) & 1) * (T / 8);
+    // (triple round: the unused destination buffer holds its run flags h and
+    // the class prefixes of every 4th run; for W = 3 after round 0's m0 bytes)
+    uint8_t* const nxtb = smem + (size_t)(((j >> 1) + 1) & 1) * T;
+    uint8_t* const hb = nxtb + T / 8;
+    uint2* const cpre = reinterpret_cast<uint2*>(nxtb + 2 * (T / 8));
     uint32_t cq[Q], iq[Q];
     uint32_t ones[Q];
 #pragma unroll
@@ -160,12 +169,17 @@ __global__ void __launch_bounds__(K8_TILE / 32, K8_CTAS) level_pass8q_kernel(con
       const uint32_t s0 = prmt(qv.x, qv.y, sel), s1 = prmt(qv.x, qv.y, sel >> 16);
       const uint32_t g = run_flags8(s0, s1, sh - 1, gbits);
       gb[k * RR + tid] = (uint8_t)g;
-      if (quad) {
+      if (quad || triple) {
         const uint32_t sel2 = s_lut[flags_lo(g)];
-        // the class-sorted run goes back to its own slot (read again after
-        // the barrier: fewer live registers than keeping all Q runs)
-        reinterpret_cast<uint2*>(const_cast<uint8_t*>(cur) + k * R)[tid] =
-            make_uint2(prmt(s0, s1, sel2), prmt(s0, s1, sel2 >> 16));
+        const uint32_t u0 = prmt(s0, s1, sel2), u1 = prmt(s0, s1, sel2 >> 16);
+        if (quad) {
+          // the class-sorted run goes back to its own slot (read again after
+          // the barrier: fewer live registers than keeping all Q runs)
+          reinterpret_cast<uint2*>(const_cast<uint8_t*>(cur) + k * R)[tid] = make_uint2(u0, u1);
+        } else {
+          uint32_t hbits;
+          hb[k * RR + tid] = (uint8_t)run_flags8(u0, u1, sh - 2, hbits);  // b_j+2 in class order
+        }
         // class counts n0..n3 (c = 2 b_j+1 + b_j) as bytes: z = n0 + n1 (b_j
         // zeros), n2 = the zeros' b_j+1 ones, n3 = the ones' b_j+1 ones
         const uint32_t z = 8u - __popc(mbits);
@@ -180,7 +194,8 @@ __global__ void __launch_bounds__(K8_TILE / 32, K8_CTAS) level_pass8q_kernel(con
       }
     }
     uint32_t Zt;  // the tile's b_j zeros: where L_j+1's ones stream starts
-    if (quad) {
+    uint32_t C1 = 0, C2 = 0, C3 = 0;  // class starts of A_j+2 (triple round: L_j+2's streams)
+    if (quad || triple) {
       if (lane == 31) {  // warp totals per region as 16-bit pairs (a class may reach 256)
 #pragma unroll
         for (int k = 0; k < Q; ++k)
@@ -188,7 +203,7 @@ __global__ void __launch_bounds__(K8_TILE / 32, K8_CTAS) level_pass8q_kernel(con
                                            prmt(iq[k], 0u, 0x4341u) + prmt(cq[k], 0u, 0x4341u));
       }
       bar_sync(1, NT);
-      // class totals of the tile (classes 0, 1 packed 16|16, class 2) and the
+      // class totals of the tile (classes 0|2 and 1|3 packed 16|16) and the
       // class starts C_c of A_j+2
       // (lane l < NW holds warp l's totals; per-lane sums over the regions
       // turn every prefix into one REDUX)
@@ -200,7 +215,9 @@ __global__ void __launch_bounds__(K8_TILE / 32, K8_CTAS) level_pass8q_kernel(con
         sy += v.y;
       }
       const uint32_t T02 = __reduce_add_sync(FULL, sx), T13 = __reduce_add_sync(FULL, sy);
-      const uint32_t C1 = T02 & 0xFFFFu, C2 = C1 + (T13 & 0xFFFFu), C3 = C2 + (T02 >> 16);
+      C1 = T02 & 0xFFFFu;
+      C2 = C1 + (T13 & 0xFFFFu);
+      C3 = C2 + (T02 >> 16);
       Zt = (T02 & 0xFFFFu) + (T02 >> 16);  // classes 0 and 2: b_j = 0
       const uint32_t dst = sb + (uint32_t)(((j >> 1) + 1) & 1) * T;  // destination buffer (store immediates)
       const uint32_t CA = C2 << 16, CB = C1 | (C3 << 16);
@@ -218,6 +235,10 @@ __global__ void __launch_bounds__(K8_TILE / 32, K8_CTAS) level_pass8q_kernel(con
         // classes before c
         const uint32_t e = iq[k], sv = cq[k] * 0x01010100u;
         const uint32_t E02 = prmt(e, 0u, 0x4240u) + A02;
+        if (triple) {  // no scatter: the class prefixes of every 4th run for the concatenation
+          if ((tid & 3) == 0) cpre[(k * RR + tid) >> 2] = make_uint2(E02, prmt(e, 0u, 0x4341u) + A13);
+          continue;
+        }
         const uint32_t DA = CA + E02 - prmt(sv, 0u, 0x4240u);
         const uint32_t DB = CB + A13 + prmt(e, 0u, 0x4341u) - prmt(sv, 0u, 0x4341u);
         if ((tid & 3) == 0) za16[(k * RR + tid) >> 2] = (uint16_t)((E02 * 0x10001u) >> 16);  // b_j zeros before
@@ -273,8 +294,9 @@ __global__ void __launch_bounds__(K8_TILE / 32, K8_CTAS) level_pass8q_kernel(con
       const uint32_t gw = reinterpret_cast<const uint32_t*>(gb)[tid];
       uint32_t* mwp = reinterpret_cast<uint32_t*>(mb) + tid;
       const uint32_t mw = *mwp;
-      if (j == 0 && W >= 4 && (W & 1) == 0) *mwp = 0u;  // level W-1 (OR-ed later) lent its array
-      const uint32_t zpos = za16[tid];
+      if (j == 0 && W >= 4) *mwp = 0u;  // level W-1 (OR-ed later) lent its array
+      const uint2 cp = triple ? cpre[tid] : make_uint2(0u, 0u);
+      const uint32_t zpos = triple ? (cp.x * 0x10001u) >> 16 : za16[tid];
       uint32_t accz = 0, acco = 0, fz = 0;
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
@@ -287,6 +309,31 @@ __global__ void __launch_bounds__(K8_TILE / 32, K8_CTAS) level_pass8q_kernel(con
       uint32_t* Lw = bits + (j + 1) * (NC + 4);
       or_bits32(Lw, zpos, accz);
       or_bits32(Lw, Zt + 32u * tid - zpos, acco);
+      if (triple) {
+        // L_j+2 = b_j+2 over A_j+2: each run's class-sorted b_j+2 flags h, split
+        // into its four class pieces, appended to the four class streams
+        const uint32_t hw = reinterpret_cast<const uint32_t*>(hb)[tid];
+        uint32_t acc[4] = {0u, 0u, 0u, 0u}, f[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const uint32_t g = (gw >> (8 * i)) & 0xFFu, h = (hw >> (8 * i)) & 0xFFu;
+          const uint32_t z = 8u - __popc((mw >> (8 * i)) & 0xFFu);
+          const uint32_t n2 = __popc(g & ((1u << z) - 1u)), n3 = __popc(g) - n2;
+          const uint32_t n[4] = {z - n2, 8u - z - n3, n2, n3};
+          const uint32_t st[4] = {0u, z - n2, 8u - n2 - n3, 8u - n3};  // class starts in the sorted run
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            acc[c] |= ((h >> st[c]) & ((1u << n[c]) - 1u)) << f[c];
+            f[c] += n[c];
+          }
+        }
+        uint32_t* L2 = bits + (j + 2) * (NC + 4);
+        or_bits32(L2, cp.x & 0xFFFFu, acc[0]);
+        or_bits32(L2, C1 + (cp.y & 0xFFFFu), acc[1]);
+        or_bits32(L2, C2 + (cp.x >> 16), acc[2]);
+        or_bits32(L2, C3 + (cp.y >> 16), acc[3]);
+        break;
+      }
     }
   }
   bar_sync(1, NT);  // every level's bits are in place
