@@ -561,8 +561,11 @@ __device__ __forceinline__ void emit_levels8(const TabW<W>& tt, const uint32_t* 
     const uint32_t* L = bits + j * (NC + 4);
     const uint64_t v = extract_bits(L, tt.ls[r] + (int)(lo - g), len) << (lo - wb);
     uint64_t* dstw = words + (int64_t)j * nwords + wd;
-    if (len == 64) *dstw = v;
-    else if (v) atomicOr(reinterpret_cast<unsigned long long*>(dstw), (unsigned long long)v);
+    // whole word: plain store; run edge: OR (shared with a neighbouring run), skipped if empty
+    asm volatile(
+        "{\n\t.reg .pred p, q;\n\tsetp.eq.s32 p, %2, 64;\n\tsetp.ne.and.b64 q, %1, 0, !p;\n\t"
+        "@p st.global.b64 [%0], %1;\n\t@q red.global.or.b64 [%0], %1;\n\t}" ::"l"(dstw), "l"(v), "r"(len)
+        : "memory");
   }
 }
 

@@ -63,13 +63,24 @@ __device__ __forceinline__ uint32_t run_flags8(uint32_t x0, uint32_t x1, int sh,
 }
 __device__ __forceinline__ uint32_t flags_lo(uint32_t f) { return f & 0xFFu; }
 
-// OR a bit string v (its length implied: bits above it are zero) into L at
-// bit pos; branch-free (two predicated shared atomics)
-__device__ __forceinline__ void or_bits32(uint32_t* L, uint32_t pos, uint32_t v) {
+// ((1 << width) - 1) << pos (width 0 or pos 32: 0)
+__device__ __forceinline__ uint32_t bmsk(uint32_t pos, uint32_t width) {
+  uint32_t d;
+  asm("bmsk.clamp.b32 %0, %1, %2;" : "=r"(d) : "r"(pos), "r"(width));
+  return d;
+}
+// shared OR of v, predicated on v != 0 (no branch)
+__device__ __forceinline__ void red_or_nz(uint32_t saddr, uint32_t v) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\t@q red.shared.or.b32 [%0], %1;\n\t}" ::"r"(saddr), "r"(v)
+               : "memory");
+}
+// OR a bit string v (its length implied: bits above it are zero) into the
+// shared bit array at shared address L, bit pos
+__device__ __forceinline__ void or_bits32(uint32_t L, uint32_t pos, uint32_t v) {
   const uint64_t t = (uint64_t)v << (pos & 31);
-  uint32_t* w = L + (pos >> 5);
-  if ((uint32_t)t) atomicOr(w, (uint32_t)t);
-  if ((uint32_t)(t >> 32)) atomicOr(w + 1, (uint32_t)(t >> 32));
+  const uint32_t a = L + (pos >> 5) * 4u;
+  red_or_nz(a, (uint32_t)t);
+  red_or_nz(a + 4u, (uint32_t)(t >> 32));
 }
 
 template <int W>
@@ -300,13 +311,15 @@ __global__ void __launch_bounds__(K8_TILE / 32, K8_CTAS) level_pass8q_kernel(con
       uint32_t accz = 0, acco = 0, fz = 0;
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        const uint32_t g = (gw >> (8 * i)) & 0xFFu;
-        const uint32_t z = 8u - __popc((mw >> (8 * i)) & 0xFFu);
-        accz |= (g & ((1u << z) - 1u)) << fz;
-        acco |= (g >> z) << (8u * i - fz);
+        // run 4t + i: its zeros' flags (bits [8i, 8i + z) of gw) go to fz, its
+        // ones' flags (bits [8i + z, 8i + 8)) to the 8i - fz ones before it
+        const uint32_t z = 8u - __popc(mw & (0xFFu << (8 * i)));
+        const uint32_t zm = bmsk(8u * i, z);
+        accz |= (gw & zm) >> (8u * i - fz);
+        acco |= (gw & (0xFFu << (8 * i)) & ~zm) >> (z + fz);
         fz += z;
       }
-      uint32_t* Lw = bits + (j + 1) * (NC + 4);
+      const uint32_t Lw = sb + (uint32_t)((const unsigned char*)(bits + (j + 1) * (NC + 4)) - smem);
       or_bits32(Lw, zpos, accz);
       or_bits32(Lw, Zt + 32u * tid - zpos, acco);
       if (triple) {
@@ -316,18 +329,18 @@ __global__ void __launch_bounds__(K8_TILE / 32, K8_CTAS) level_pass8q_kernel(con
         uint32_t acc[4] = {0u, 0u, 0u, 0u}, f[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          const uint32_t g = (gw >> (8 * i)) & 0xFFu, h = (hw >> (8 * i)) & 0xFFu;
-          const uint32_t z = 8u - __popc((mw >> (8 * i)) & 0xFFu);
+          const uint32_t g = (gw >> (8 * i)) & 0xFFu;
+          const uint32_t z = 8u - __popc(mw & (0xFFu << (8 * i)));
           const uint32_t n2 = __popc(g & ((1u << z) - 1u)), n3 = __popc(g) - n2;
           const uint32_t n[4] = {z - n2, 8u - z - n3, n2, n3};
           const uint32_t st[4] = {0u, z - n2, 8u - n2 - n3, 8u - n3};  // class starts in the sorted run
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
-            acc[c] |= ((h >> st[c]) & ((1u << n[c]) - 1u)) << f[c];
+            acc[c] |= (hw & bmsk(8u * i + st[c], n[c])) >> (8u * i + st[c] - f[c]);
             f[c] += n[c];
           }
         }
-        uint32_t* L2 = bits + (j + 2) * (NC + 4);
+        const uint32_t L2 = sb + (uint32_t)((const unsigned char*)(bits + (j + 2) * (NC + 4)) - smem);
         or_bits32(L2, cp.x & 0xFFFFu, acc[0]);
         or_bits32(L2, C1 + (cp.y & 0xFFFFu), acc[1]);
         or_bits32(L2, C2 + (cp.x >> 16), acc[2]);
