@@ -428,3 +428,34 @@ def test_borders_wider_storage_every_path(kind):
             assert np.array_equal(res.borders.cpu().numpy()[: (1 << w) - 2], oracle.borders(hist, w, kind)), (sigma, dt)
         words, zeros, _ = oracle.build(text, sigma, kind, "pc")
         assert np.array_equal(res.level_words.cpu().numpy().view(np.uint64), words), (sigma, dt)
+
+
+@pytest.mark.parametrize("kind", ["wm", "wt"])
+@pytest.mark.parametrize("sigma", [4, 5, 8, 9, 16, 17, 32, 33, 64, 65, 128, 129, 256])
+def test_byte_pass_class_extremes(kind, sigma):
+    """Inputs that drive the two-levels-per-round byte pass (k8q.cuh) to its
+    packed-count limits: whole warp regions (32 runs x 8 symbols) of a single
+    2-bit class (a byte field of the exclusive scan at 31 x 8, a warp total of
+    256), tiles of one class, alternating classes per run and per symbol, and a
+    partial last tile; every width 2..8, against the oracle."""
+    rng = np.random.default_rng(sigma * 31 + (kind == "wt"))
+    n = 3 * 16384 + 8 * 357 + 5
+    top = sigma - 1
+    base = np.arange(n)
+    texts = {
+        "const0": np.zeros(n, np.uint8),
+        "const_top": np.full(n, top, np.uint8),
+        # runs of 256 symbols (one warp region of one 4-byte region) of one value
+        "warp_blocks": (rng.integers(0, sigma, n // 256 + 1).repeat(256)[:n]).astype(np.uint8),
+        # each 8-symbol run constant, runs cycling through the values
+        "run_cycle": ((base // 8) % sigma).astype(np.uint8),
+        # symbol-level alternation of two far-apart values
+        "alt": np.where(base % 2 == 0, 0, top).astype(np.uint8),
+        # one tile of zeros, one of the top value, then random
+        "tiles": np.concatenate([np.zeros(16384, np.uint8), np.full(16384, top, np.uint8),
+                                 rng.integers(0, sigma, n - 32768).astype(np.uint8)]),
+        # two values that differ only in the lowest bit, in long random runs
+        "low_bit": (np.repeat(rng.integers(0, 2, n // 97 + 1), 97)[:n] + (top & ~1)).clip(0, top).astype(np.uint8),
+    }
+    for name, text in texts.items():
+        assert wv.dump_structure(wv.build_structure(text, sigma, kind)) == ref_dump(text, sigma, kind), (sigma, name)
