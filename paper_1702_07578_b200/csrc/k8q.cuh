@@ -40,8 +40,8 @@ struct Q8Smem {
   static constexpr size_t tab = 2 * (size_t)T;                              // after the ping-pong orders
   static constexpr size_t bits = tab + sizeof(TabW<W>);                     // levels 1..W-1, NC + 4 words each
   static constexpr size_t gbuf = bits + (size_t)(W - 1) * (NC + 4) * 4;    // 2 x T/8 run flag bytes
-  static constexpr size_t za = gbuf + 2 * (size_t)(T / 8);                  // T/32 u16: zero prefix per 4 runs
-  static constexpr size_t tot = za + (size_t)(T / 32) * 2;                  // [4 regions][warps] uint2 warp totals
+  static constexpr size_t za = gbuf + 2 * (size_t)(T / 8);                  // T/32 u32: classes 0|2 prefix per 4 runs
+  static constexpr size_t tot = za + (size_t)(T / 32) * 4;                  // [4 regions][warps] uint2 warp totals
   static constexpr size_t lut = tot + 4 * (size_t)(T / 1024) * 8;          // 256 sort selectors
   static constexpr size_t mbar = lut + 1024;
   static constexpr size_t total = mbar + 16;
@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(K8_TILE / 32, K8_CTAS) level_pass8q_kernel(con
   TabW<W>& tt = *reinterpret_cast<TabW<W>*>(smem + L::tab);
   uint32_t* bits = reinterpret_cast<uint32_t*>(smem + L::bits) - (NC + 4);  // level j at j (NC + 4)
   uint8_t* bits8 = reinterpret_cast<uint8_t*>(bits);
-  uint16_t* za16 = reinterpret_cast<uint16_t*>(smem + L::za);
+  uint32_t* za32 = reinterpret_cast<uint32_t*>(smem + L::za);  // per 4th run: b_j zeros before it (as lo + hi halves)
   uint2* s_tot = reinterpret_cast<uint2*>(smem + L::tot);
   uint32_t* s_lut = reinterpret_cast<uint32_t*>(smem + L::lut);
 
@@ -131,8 +131,10 @@ __global__ void __launch_bounds__(K8_TILE / 32, K8_CTAS) level_pass8q_kernel(con
   // every round) start at zero
 #pragma unroll
   for (int j = 1; j < W; ++j)
-    if ((j & 1) || ((W & 1) && j == W - 1 && W >= 3))  // (odd W: the last round ORs level W-1 too)
-      for (int i = tid; i < NC + 4; i += NT) bits[j * (NC + 4) + i] = 0u;
+    if ((j & 1) || ((W & 1) && j == W - 1 && W >= 3)) {  // (odd W: the last round ORs level W-1 too)
+      uint4* b4 = reinterpret_cast<uint4*>(bits + j * (NC + 4));  // (NC + 4) words: 16-byte aligned rows
+      for (int i = tid; i < (NC + 4) / 4; i += NT) b4[i] = make_uint4(0u, 0u, 0u, 0u);
+    }
   if (!bulk)
     for (int p = tid; p < T; p += NT) smem[p] = p < cnt ? text[base + p] : (uint8_t)0xFF;
   bar_sync(1, NT);
@@ -252,7 +254,7 @@ __global__ void __launch_bounds__(K8_TILE / 32, K8_CTAS) level_pass8q_kernel(con
         }
         const uint32_t DA = CA + E02 - prmt(sv, 0u, 0x4240u);
         const uint32_t DB = CB + A13 + prmt(e, 0u, 0x4341u) - prmt(sv, 0u, 0x4341u);
-        if ((tid & 3) == 0) za16[(k * RR + tid) >> 2] = (uint16_t)((E02 * 0x10001u) >> 16);  // b_j zeros before
+        if ((tid & 3) == 0) za32[(k * RR + tid) >> 2] = E02;  // b_j zeros before: classes 0 + 2
         const uint2 uk = reinterpret_cast<const uint2*>(cur + k * R)[tid];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
@@ -293,7 +295,7 @@ __global__ void __launch_bounds__(K8_TILE / 32, K8_CTAS) level_pass8q_kernel(con
         for (int h = 0; h < 2; ++h) {
           const int k = 2 * p + h;
           const uint32_t opre = run_tot + (h ? ex >> 16 : ex & 0xFFFFu);
-          if ((tid & 3) == 0) za16[(k * RR + tid) >> 2] = (uint16_t)((uint32_t)(k * R + 8 * tid) - opre);
+          if ((tid & 3) == 0) za32[(k * RR + tid) >> 2] = (uint32_t)(k * R + 8 * tid) - opre;
           run_tot += h ? tot >> 16 : tot & 0xFFFFu;
         }
       }
@@ -307,7 +309,8 @@ __global__ void __launch_bounds__(K8_TILE / 32, K8_CTAS) level_pass8q_kernel(con
       const uint32_t mw = *mwp;
       if (j == 0 && W >= 4) *mwp = 0u;  // level W-1 (OR-ed later) lent its array
       const uint2 cp = triple ? cpre[tid] : make_uint2(0u, 0u);
-      const uint32_t zpos = triple ? (cp.x * 0x10001u) >> 16 : za16[tid];
+      const uint32_t zq = triple ? cp.x : za32[tid];
+      const uint32_t zpos = quad || triple ? (zq * 0x10001u) >> 16 : zq;  // (quad / triple: lo + hi halves)
       uint32_t accz = 0, acco = 0, fz = 0;
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
