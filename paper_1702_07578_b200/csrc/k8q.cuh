@@ -87,10 +87,11 @@ template <int W>
 __global__ void __launch_bounds__(K8_TILE / 32, K8_CTAS) level_pass8q_kernel(const Pass8Args a,
                                                                             const TabW<W>* __restrict__ tabs) {
   constexpr int T = K8_TILE;
-  constexpr int Q = 4;           // runs per thread (one per region)
-  constexpr int NT = T / (8 * Q);
-  constexpr int R = T / Q;       // region of run k
-  constexpr int RR = R / 8;      // runs per region
+  constexpr int RUN = 16;              // bytes per thread run: two 8-symbol halves, each sorted by PRMT
+  constexpr int QR = 2;                // runs per thread, one per region
+  constexpr int NT = T / (RUN * QR);
+  constexpr int RG = T / QR;           // region of run k: [k RG, (k + 1) RG)
+  constexpr int HR = RG / 8;           // 8-symbol half-runs per region
   constexpr int NC = T / 32;
   constexpr int NW = NT / 32;
   using L = Q8Smem<W>;
@@ -99,7 +100,7 @@ __global__ void __launch_bounds__(K8_TILE / 32, K8_CTAS) level_pass8q_kernel(con
   TabW<W>& tt = *reinterpret_cast<TabW<W>*>(smem + L::tab);
   uint32_t* bits = reinterpret_cast<uint32_t*>(smem + L::bits) - (NC + 4);  // level j at j (NC + 4)
   uint8_t* bits8 = reinterpret_cast<uint8_t*>(bits);
-  uint32_t* za32 = reinterpret_cast<uint32_t*>(smem + L::za);  // per 4th run: b_j zeros before it (as lo + hi halves)
+  uint32_t* za32 = reinterpret_cast<uint32_t*>(smem + L::za);  // per 4th half-run: b_j zeros before it
   uint2* s_tot = reinterpret_cast<uint2*>(smem + L::tot);
   uint32_t* s_lut = reinterpret_cast<uint32_t*>(smem + L::lut);
 
@@ -149,168 +150,164 @@ __global__ void __launch_bounds__(K8_TILE / 32, K8_CTAS) level_pass8q_kernel(con
 #pragma unroll
   for (int j = 0; j < W; j += 2) {
     const int sh = W - 1 - j;
-    const uint8_t* cur = smem + (size_t)((j >> 1) & 1) * T;
-    uint8_t* mb = j == 0 ? m0b : bits8 + j * 4 * (NC + 4);
-    if (j == W - 1) {  // odd width: the last level's flags only
-#pragma unroll
-      for (int k = 0; k < Q; ++k) {
-        const uint2 qv = reinterpret_cast<const uint2*>(cur + k * R)[tid];
-        uint32_t fb;
-        mb[k * RR + tid] = (uint8_t)run_flags8(qv.x, qv.y, 0, fb);
-      }
-      break;
-    }
+    uint8_t* const cur = smem + (size_t)((j >> 1) & 1) * T;
+    uint8_t* const mb = j == 0 ? m0b : bits8 + j * 4 * (NC + 4);
     // odd width: the last round starts at A_W-3 and emits three levels without a
     // scatter -- L_W-2 and L_W-1 are concatenated from the runs' 2- and 4-class pieces
     const bool triple = (W & 1) && j + 3 == W;
     const bool quad = j + 2 < W && !triple;
-    uint8_t* gb = smem + L::gbuf + (size_t)((j >> 1) & 1) * (T / 8);
+    uint8_t* const gb = smem + L::gbuf + (size_t)((j >> 1) & 1) * (T / 8);
     // (triple round: the unused destination buffer holds its run flags h and
-    // the class prefixes of every 4th run; for W = 3 after round 0's m0 bytes)
+    // the class prefixes of every 4th half-run; for W = 3 after round 0's m0 bytes)
     uint8_t* const nxtb = smem + (size_t)(((j >> 1) + 1) & 1) * T;
     uint8_t* const hb = nxtb + T / 8;
     uint2* const cpre = reinterpret_cast<uint2*>(nxtb + 2 * (T / 8));
-    uint32_t cq[Q], iq[Q];
-    uint32_t ones[Q];
+    uint32_t cA[QR], cB[QR], ff[QR], ee[QR];  // per run: class counts of its halves (bytes), 10-bit sums, scan
+    uint32_t ones[QR];
 #pragma unroll
-    for (int k = 0; k < Q; ++k) {
-      const uint2 qv = reinterpret_cast<const uint2*>(cur + k * R)[tid];
-      uint32_t mbits, gbits;
-      const uint32_t m = run_flags8(qv.x, qv.y, sh, mbits);
-      mb[k * RR + tid] = (uint8_t)m;
-      const uint32_t sel = s_lut[flags_lo(m)];
-      const uint32_t s0 = prmt(qv.x, qv.y, sel), s1 = prmt(qv.x, qv.y, sel >> 16);
-      const uint32_t g = run_flags8(s0, s1, sh - 1, gbits);
-      gb[k * RR + tid] = (uint8_t)g;
-      if (quad || triple) {
-        const uint32_t sel2 = s_lut[flags_lo(g)];
-        const uint32_t u0 = prmt(s0, s1, sel2), u1 = prmt(s0, s1, sel2 >> 16);
-        if (quad) {
-          // the class-sorted run goes back to its own slot (read again after
-          // the barrier: fewer live registers than keeping all Q runs)
-          reinterpret_cast<uint2*>(const_cast<uint8_t*>(cur) + k * R)[tid] = make_uint2(u0, u1);
+    for (int k = 0; k < QR; ++k) {
+      const uint4 qv = reinterpret_cast<const uint4*>(cur + k * RG)[tid];
+      uint32_t xw[4] = {qv.x, qv.y, qv.z, qv.w};
+      uint32_t cb[2] = {0u, 0u}, f10 = 0u, o = 0u;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int r8 = k * HR + 2 * tid + h;  // the half's 8-symbol run
+        uint32_t mbits, gbits;
+        const uint32_t m = run_flags8(xw[2 * h], xw[2 * h + 1], sh, mbits);
+        mb[r8] = (uint8_t)m;
+        const uint32_t sel = s_lut[flags_lo(m)];
+        const uint32_t s0 = prmt(xw[2 * h], xw[2 * h + 1], sel), s1 = prmt(xw[2 * h], xw[2 * h + 1], sel >> 16);
+        const uint32_t g = run_flags8(s0, s1, sh - 1, gbits);
+        gb[r8] = (uint8_t)g;
+        if (quad || triple) {
+          const uint32_t sel2 = s_lut[flags_lo(g)];
+          xw[2 * h] = prmt(s0, s1, sel2);
+          xw[2 * h + 1] = prmt(s0, s1, sel2 >> 16);
+          if (triple) {
+            uint32_t hbits;
+            hb[r8] = (uint8_t)run_flags8(xw[2 * h], xw[2 * h + 1], sh - 2, hbits);  // b_j+2 in class order
+          }
+          // class counts n0..n3 (c = 2 b_j+1 + b_j): z = n0 + n1 (b_j zeros),
+          // n2 = the zeros' b_j+1 ones, n3 = the ones' b_j+1 ones; as bytes and
+          // as three 10-bit fields (n0 | n1 << 10 | n2 << 20), both mod 2^32
+          const uint32_t z = 8u - __popc(mbits);
+          const uint32_t n2 = __popc(g & ((1u << z) - 1u));
+          const uint32_t n3 = __popc(gbits) - n2;
+          cb[h] = z * 0xFFFFFF01u + 0x800u + n2 * 0xFFFFu + n3 * 0xFFFF00u;
+          f10 += z * (1u - 1024u) + 8u * 1024u + n2 * ((1u << 20) - 1u) - n3 * 1024u;
         } else {
-          uint32_t hbits;
-          hb[k * RR + tid] = (uint8_t)run_flags8(u0, u1, sh - 2, hbits);  // b_j+2 in class order
+          o += __popc(mbits);
         }
-        // class counts n0..n3 (c = 2 b_j+1 + b_j) as bytes: z = n0 + n1 (b_j
-        // zeros), n2 = the zeros' b_j+1 ones, n3 = the ones' b_j+1 ones
-        const uint32_t z = 8u - __popc(mbits);
-        const uint32_t n2 = __popc(g & ((1u << z) - 1u));
-        const uint32_t n3 = __popc(gbits) - n2;
-        // n0 + n1 2^8 + n2 2^16 + n3 2^24 with n0 = z - n2, n1 = 8 - z - n3 (mod 2^32)
-        cq[k] = z * 0xFFFFFF01u + 0x800u + n2 * 0xFFFFu + n3 * 0xFFFF00u;
-        // exclusive warp scan by bytes (every exclusive prefix <= 31 * 8 < 256)
-        iq[k] = warp_incl_scan(cq[k]) - cq[k];  // exact as integers even where a byte of the inclusive sum carries
+      }
+      if (quad)  // the class-sorted halves go back to the run's own slot (read again after the barrier)
+        reinterpret_cast<uint4*>(cur + k * RG)[tid] = make_uint4(xw[0], xw[1], xw[2], xw[3]);
+      if (quad || triple) {
+        cA[k] = cb[0];
+        cB[k] = cb[1];
+        ff[k] = f10;
+        ee[k] = warp_incl_scan(f10);  // 10-bit fields: at most 32 x 16 per class
       } else {
-        ones[k] = __popc(mbits);
+        ones[k] = o;
       }
     }
     uint32_t Zt;  // the tile's b_j zeros: where L_j+1's ones stream starts
     uint32_t C1 = 0, C2 = 0, C3 = 0;  // class starts of A_j+2 (triple round: L_j+2's streams)
     if (quad || triple) {
-      if (lane == 31) {  // warp totals per region as 16-bit pairs (a class may reach 256)
+      if (lane == 31) {  // warp totals per region: (n0 | n1 << 16, n2)
 #pragma unroll
-        for (int k = 0; k < Q; ++k)
-          s_tot[k * NW + wid] = make_uint2(prmt(iq[k], 0u, 0x4240u) + prmt(cq[k], 0u, 0x4240u),
-                                           prmt(iq[k], 0u, 0x4341u) + prmt(cq[k], 0u, 0x4341u));
+        for (int k = 0; k < QR; ++k)
+          s_tot[k * NW + wid] = make_uint2((ee[k] & 0x3FFu) | (((ee[k] >> 10) & 0x3FFu) << 16), ee[k] >> 20);
       }
       bar_sync(1, NT);
-      // class totals of the tile (classes 0|2 and 1|3 packed 16|16) and the
-      // class starts C_c of A_j+2
       // (lane l < NW holds warp l's totals; per-lane sums over the regions
       // turn every prefix into one REDUX)
       uint32_t sx = 0, sy = 0;
 #pragma unroll
-      for (int k = 0; k < Q; ++k) {
+      for (int k = 0; k < QR; ++k) {
         const uint2 v = lane < NW ? s_tot[k * NW + lane] : make_uint2(0u, 0u);
         sx += v.x;
         sy += v.y;
       }
-      const uint32_t T02 = __reduce_add_sync(FULL, sx), T13 = __reduce_add_sync(FULL, sy);
-      C1 = T02 & 0xFFFFu;
-      C2 = C1 + (T13 & 0xFFFFu);
-      C3 = C2 + (T02 >> 16);
-      Zt = (T02 & 0xFFFFu) + (T02 >> 16);  // classes 0 and 2: b_j = 0
+      const uint32_t TA = __reduce_add_sync(FULL, sx), TB = __reduce_add_sync(FULL, sy);
+      C1 = TA & 0xFFFFu;
+      C2 = C1 + (TA >> 16);
+      C3 = C2 + TB;
+      Zt = (TA & 0xFFFFu) + TB;  // classes 0 and 2: b_j = 0
       const uint32_t dst = sb + (uint32_t)(((j >> 1) + 1) & 1) * T;  // destination buffer (store immediates)
-      const uint32_t CA = C2 << 16, CB = C1 | (C3 << 16);
       uint32_t ax = 0, ay = 0;  // this lane's warp over the regions before
 #pragma unroll
-      for (int k = 0; k < Q; ++k) {
+      for (int k = 0; k < QR; ++k) {
         const uint2 v = lane < NW ? s_tot[k * NW + lane] : make_uint2(0u, 0u);
-        const uint32_t A02 = __reduce_add_sync(FULL, ax + (lane < wid ? v.x : 0u));
-        const uint32_t A13 = __reduce_add_sync(FULL, ay + (lane < wid ? v.y : 0u));
+        const uint32_t A = __reduce_add_sync(FULL, ax + (lane < wid ? v.x : 0u));
+        const uint32_t B = __reduce_add_sync(FULL, ay + (lane < wid ? v.y : 0u));
         ax += v.x;
         ay += v.y;
-        // the run's class c base minus the class's start inside the sorted run,
-        // as 16-bit pairs (D0 | D2 << 16, D1 | D3 << 16): c's global start +
-        // regions / warps before + this lane's exclusive prefix - the run's
-        // classes before c
-        const uint32_t e = iq[k], sv = cq[k] * 0x01010100u;
-        const uint32_t E02 = prmt(e, 0u, 0x4240u) + A02;
-        if (triple) {  // no scatter: the class prefixes of every 4th run for the concatenation
-          if ((tid & 3) == 0) cpre[(k * RR + tid) >> 2] = make_uint2(E02, prmt(e, 0u, 0x4341u) + A13);
-          continue;
+        // the run's class prefixes: regions / warps before + this lane's exclusive scan
+        const uint32_t e = ee[k] - ff[k];
+        const uint32_t P0 = (A & 0xFFFFu) + (e & 0x3FFu);
+        const uint32_t P1 = (A >> 16) + ((e >> 10) & 0x3FFu);
+        const uint32_t P2 = B + (e >> 20);
+        const uint32_t P3 = (uint32_t)(k * RG + RUN * tid) - P0 - P1 - P2;
+        if ((tid & 1) == 0) {  // half-run 2t of the region is a 4th half-run: the concatenation's offsets
+          const int q4 = (k * HR + 2 * tid) >> 2;
+          if (triple) cpre[q4] = make_uint2(P0 | (P2 << 16), P1 | (P3 << 16));
+          else za32[q4] = P0 + P2;  // b_j zeros before it
         }
-        const uint32_t DA = CA + E02 - prmt(sv, 0u, 0x4240u);
-        const uint32_t DB = CB + A13 + prmt(e, 0u, 0x4341u) - prmt(sv, 0u, 0x4341u);
-        if ((tid & 3) == 0) za32[(k * RR + tid) >> 2] = E02;  // b_j zeros before: classes 0 + 2
-        const uint2 uk = reinterpret_cast<const uint2*>(cur + k * R)[tid];
+        if (triple) continue;  // no scatter
+        // the run's class bases as 16-bit pairs (classes 0|2, 1|3); a half's
+        // class c byte kk goes to base_c + (half 1: half 0's class-c count) - S_c + kk
+        const uint32_t BA = P0 | ((C2 + P2) << 16), BB = (C1 + P1) | ((C3 + P3) << 16);
+        const uint4 uk = reinterpret_cast<const uint4*>(cur + k * RG)[tid];
+        const uint32_t uw[4] = {uk.x, uk.y, uk.z, uk.w};
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const uint32_t w = h ? uk.y : uk.x;
-          const uint32_t x = w >> (sh - 1);
-          // PRMT selectors of bytes 0, 2 and 1, 3: nibbles 2c', 2c'+1 pick the
-          // byte's 16-bit base (c' = 2 b_j + b_j+1), 0x99 zero-fills the top half
-          // (0x22 c' has no bit of 0x10 / 0x99 set: OR adds them, no constant register)
-          const uint32_t s02 = ((x & 0x00030003u) * 0x22u) | 0x99109910u;
-          const uint32_t s13 = __umulhi(x & 0x03000300u, 0x22000000u) | 0x99109910u;
-          const uint32_t a0 = prmt(DA, DB, s02), a1 = prmt(DA, DB, s13);
-          const uint32_t a2 = prmt(DA, DB, __umulhi(s02, 0x10000u)), a3 = prmt(DA, DB, __umulhi(s13, 0x10000u));
-          asm volatile("st.shared.u8 [%0], %1;" ::"r"(a0 + dst + (uint32_t)(4 * h)), "r"(w) : "memory");
-          asm volatile("st.shared.u8 [%0], %1;" ::"r"(a1 + dst + (uint32_t)(4 * h + 1)), "r"(__umulhi(w, 1u << 24)) : "memory");
-          asm volatile("st.shared.u8 [%0], %1;" ::"r"(a2 + dst + (uint32_t)(4 * h + 2)), "r"(__umulhi(w, 1u << 16)) : "memory");
-          asm volatile("st.shared.u8 [%0], %1;" ::"r"(a3 + dst + (uint32_t)(4 * h + 3)), "r"(__umulhi(w, 1u << 8)) : "memory");
+          const uint32_t sv = (h ? cB[k] : cA[k]) * 0x01010100u;  // class starts inside the half
+          const uint32_t DA = BA - prmt(sv, 0u, 0x4240u) + (h ? prmt(cA[k], 0u, 0x4240u) : 0u);
+          const uint32_t DB = BB - prmt(sv, 0u, 0x4341u) + (h ? prmt(cA[k], 0u, 0x4341u) : 0u);
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            const uint32_t w = uw[2 * h + hh];
+            const uint32_t x = w >> (sh - 1);
+            // PRMT selectors of bytes 0, 2 and 1, 3: nibbles 2c', 2c'+1 pick the
+            // byte's 16-bit base (c' = 2 b_j + b_j+1), 0x99 zero-fills the top half
+            // (0x22 c' has no bit of 0x10 / 0x99 set: OR adds them, no constant register)
+            const uint32_t s02 = ((x & 0x00030003u) * 0x22u) | 0x99109910u;
+            const uint32_t s13 = __umulhi(x & 0x03000300u, 0x22000000u) | 0x99109910u;
+            const uint32_t a0 = prmt(DA, DB, s02), a1 = prmt(DA, DB, s13);
+            const uint32_t a2 = prmt(DA, DB, __umulhi(s02, 0x10000u)), a3 = prmt(DA, DB, __umulhi(s13, 0x10000u));
+            asm volatile("st.shared.u8 [%0], %1;" ::"r"(a0 + dst + (uint32_t)(4 * hh)), "r"(w) : "memory");
+            asm volatile("st.shared.u8 [%0], %1;" ::"r"(a1 + dst + (uint32_t)(4 * hh + 1)), "r"(__umulhi(w, 1u << 24)) : "memory");
+            asm volatile("st.shared.u8 [%0], %1;" ::"r"(a2 + dst + (uint32_t)(4 * hh + 2)), "r"(__umulhi(w, 1u << 16)) : "memory");
+            asm volatile("st.shared.u8 [%0], %1;" ::"r"(a3 + dst + (uint32_t)(4 * hh + 3)), "r"(__umulhi(w, 1u << 8)) : "memory");
+          }
         }
       }
     } else {
       // last round of an even width: a 2-way count scan for L_W-1's pieces
-      constexpr int P = Q / 2;
-      uint32_t incl[P];
-#pragma unroll
-      for (int p = 0; p < P; ++p) {
-        const uint32_t pk = ones[2 * p] | (ones[2 * p + 1] << 16);
-        incl[p] = warp_incl_scan(pk);
-        if (lane == 31) s_tot[p * NW + wid].x = incl[p];
-        incl[p] -= pk;
-      }
+      // (two runs per thread, one per region, packed 16|16)
+      static_assert(QR == 2, "one packed scan for the two regions");
+      const uint32_t pk = ones[0] | (ones[1] << 16);
+      const uint32_t incl = warp_incl_scan(pk);
+      if (lane == 31) s_tot[wid].x = incl;
       bar_sync(1, NT);
-      uint32_t run_tot = 0;
-#pragma unroll
-      for (int p = 0; p < P; ++p) {
-        const uint32_t wv = lane < NW ? s_tot[p * NW + lane].x : 0u;
-        const uint32_t ex = __reduce_add_sync(FULL, lane < wid ? wv : 0u) + incl[p];
-        const uint32_t tot = __reduce_add_sync(FULL, wv);
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int k = 2 * p + h;
-          const uint32_t opre = run_tot + (h ? ex >> 16 : ex & 0xFFFFu);
-          if ((tid & 3) == 0) za32[(k * RR + tid) >> 2] = (uint32_t)(k * R + 8 * tid) - opre;
-          run_tot += h ? tot >> 16 : tot & 0xFFFFu;
-        }
+      const uint32_t wv = lane < NW ? s_tot[lane].x : 0u;
+      const uint32_t ex = __reduce_add_sync(FULL, lane < wid ? wv : 0u) + incl - pk;
+      const uint32_t tot = __reduce_add_sync(FULL, wv);
+      if ((tid & 1) == 0) {  // zeros before the run = its position - the ones before it
+        za32[(2 * tid) >> 2] = (uint32_t)(RUN * tid) - (ex & 0xFFFFu);
+        za32[(HR + 2 * tid) >> 2] = (uint32_t)(RG + RUN * tid) - ((tot & 0xFFFFu) + (ex >> 16));
       }
-      Zt = (uint32_t)T - run_tot;
+      Zt = (uint32_t)T - (tot & 0xFFFFu) - (tot >> 16);
     }
     bar_sync(1, NT);
-    // L_j+1 from the runs' flag pieces: thread t owns runs 4t .. 4t+3
+    // L_j+1 from the half-runs' flag pieces: thread t owns half-runs 4t .. 4t+3
     {
       const uint32_t gw = reinterpret_cast<const uint32_t*>(gb)[tid];
       uint32_t* mwp = reinterpret_cast<uint32_t*>(mb) + tid;
       const uint32_t mw = *mwp;
       if (j == 0 && W >= 4) *mwp = 0u;  // level W-1 (OR-ed later) lent its array
       const uint2 cp = triple ? cpre[tid] : make_uint2(0u, 0u);
-      const uint32_t zq = triple ? cp.x : za32[tid];
-      const uint32_t zpos = quad || triple ? (zq * 0x10001u) >> 16 : zq;  // (quad / triple: lo + hi halves)
+      const uint32_t zpos = triple ? (cp.x & 0xFFFFu) + (cp.x >> 16) : za32[tid];
       uint32_t accz = 0, acco = 0, fz = 0;
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
@@ -326,8 +323,8 @@ __global__ void __launch_bounds__(K8_TILE / 32, K8_CTAS) level_pass8q_kernel(con
       or_bits32(Lw, zpos, accz);
       or_bits32(Lw, Zt + 32u * tid - zpos, acco);
       if (triple) {
-        // L_j+2 = b_j+2 over A_j+2: each run's class-sorted b_j+2 flags h, split
-        // into its four class pieces, appended to the four class streams
+        // L_j+2 = b_j+2 over A_j+2: each half-run's class-sorted b_j+2 flags h,
+        // split into its four class pieces, appended to the four class streams
         const uint32_t hw = reinterpret_cast<const uint32_t*>(hb)[tid];
         uint32_t acc[4] = {0u, 0u, 0u, 0u}, f[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
