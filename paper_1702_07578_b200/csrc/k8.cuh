@@ -391,6 +391,10 @@ struct Pass8Args {
   const int64_t* base;  // [8][256]
 };
 
+#ifndef K8_EMIT_WORDS
+#define K8_EMIT_WORDS 2  // destination words per emission task
+#endif
+
 // Runs of levels 1..W-1 flattened: run r = 2^j - 2 + d (j = level, d = LSD digit).
 // (positions fit 32 bits: the single-pass path needs n < 2^32)
 struct Tables8 {
@@ -476,7 +480,8 @@ __device__ __forceinline__ void table8_compute(Tables8& tt, const uint32_t* s_ba
       nw[k] = 0;
       if (c[k]) {
         const uint32_t g = tt.gs[r];
-        nw[k] = ((g + c[k] - 1) >> 6) - (g >> 6) + 1;
+        // emission tasks of the run: K8_EMIT_WORDS destination words each
+        nw[k] = (((g + c[k] - 1) >> 6) - (g >> 6) + K8_EMIT_WORDS) / K8_EMIT_WORDS;
       }
       sc += c[k];
       sw += nw[k];
@@ -553,19 +558,26 @@ __device__ __forceinline__ void emit_levels8(const TabW<W>& tt, const uint32_t* 
     // 32-bit bit positions: the fused passes keep n < 2^32 - 64
     const uint32_t g = tt.gs[r];
     const uint32_t c = tt.cnt[r];
-    const uint32_t wd = (g >> 6) + (uint32_t)(q - tt.wpre[r]);
-    const uint32_t wb = wd << 6;
-    const uint32_t lo = g > wb ? g : wb;
-    const uint32_t hi = (g + c) < wb + 64 ? (g + c) : wb + 64;
-    const int len = (int)(hi - lo);
     const uint32_t* L = bits + j * (NC + 4);
-    const uint64_t v = extract_bits(L, tt.ls[r] + (int)(lo - g), len) << (lo - wb);
-    uint64_t* dstw = words + (int64_t)j * nwords + wd;
-    // whole word: plain store; run edge: OR (shared with a neighbouring run), skipped if empty
-    asm volatile(
-        "{\n\t.reg .pred p, q;\n\tsetp.eq.s32 p, %2, 64;\n\tsetp.ne.and.b64 q, %1, 0, !p;\n\t"
-        "@p st.global.b64 [%0], %1;\n\t@q red.global.or.b64 [%0], %1;\n\t}" ::"l"(dstw), "l"(v), "r"(len)
-        : "memory");
+    const uint32_t w0 = (g >> 6) + K8_EMIT_WORDS * (uint32_t)(q - tt.wpre[r]);
+    const uint32_t wlast = (g + c - 1) >> 6;
+    const int ls = tt.ls[r];
+    uint64_t* dst0 = words + (int64_t)j * nwords + w0;
+#pragma unroll
+    for (int u = 0; u < K8_EMIT_WORDS; ++u) {
+      const uint32_t wd = w0 + u;
+      if (wd > wlast) break;
+      const uint32_t wb = wd << 6;
+      const uint32_t lo = g > wb ? g : wb;
+      const uint32_t hi = (g + c) < wb + 64 ? (g + c) : wb + 64;
+      const int len = (int)(hi - lo);
+      const uint64_t v = extract_bits(L, ls + (int)(lo - g), len) << (lo - wb);
+      // whole word: plain store; run edge: OR (shared with a neighbouring run), skipped if empty
+      asm volatile(
+          "{\n\t.reg .pred p, q;\n\tsetp.eq.s32 p, %2, 64;\n\tsetp.ne.and.b64 q, %1, 0, !p;\n\t"
+          "@p st.global.b64 [%0], %1;\n\t@q red.global.or.b64 [%0], %1;\n\t}" ::"l"(dst0 + u), "l"(v), "r"(len)
+          : "memory");
+    }
   }
 }
 
