@@ -468,42 +468,79 @@ __device__ __forceinline__ void table8_compute(Tables8& tt, const uint32_t* s_ba
   }
   // one pass over the flattened runs (lane: PER consecutive ones): exclusive
   // prefixes of the run sizes (P) and of the destination words (wpre); a
-  // run's tile-local start is P minus P at its level's first run
+  // run's tile-local start is P minus P at its level's first run.  (W = 8:
+  // each lane's 8 runs move as 16-byte vectors -- scalar accesses at an
+  // 8-run stride were 4- to 8-way bank conflicts)
   {
     constexpr int PER = (NR + 31) / 32;
-    uint32_t c[PER], nw[PER];
+    uint32_t c[PER], g[PER], nw[PER];
+    if constexpr (PER == 8) {
+      const uint4 cv = reinterpret_cast<const uint4*>(tt.cnt)[lane];
+      const uint4 g0 = reinterpret_cast<const uint4*>(tt.gs)[2 * lane], g1 = reinterpret_cast<const uint4*>(tt.gs)[2 * lane + 1];
+      const uint32_t cw[4] = {cv.x, cv.y, cv.z, cv.w};
+#pragma unroll
+      for (int k = 0; k < 8; ++k) c[k] = (cw[k >> 1] >> (16 * (k & 1))) & 0xFFFFu;
+      g[0] = g0.x; g[1] = g0.y; g[2] = g0.z; g[3] = g0.w;
+      g[4] = g1.x; g[5] = g1.y; g[6] = g1.z; g[7] = g1.w;
+    } else {
+#pragma unroll
+      for (int k = 0; k < PER; ++k) {
+        c[k] = tt.cnt[lane * PER + k];
+        g[k] = tt.gs[lane * PER + k];
+      }
+    }
     uint32_t sc = 0, sw = 0;
 #pragma unroll
     for (int k = 0; k < PER; ++k) {
       const int r = lane * PER + k;
-      c[k] = r < NR ? tt.cnt[r] : 0u;
-      nw[k] = 0;
-      if (c[k]) {
-        const uint32_t g = tt.gs[r];
-        // emission tasks of the run: K8_EMIT_WORDS destination words each
-        nw[k] = (((g + c[k] - 1) >> 6) - (g >> 6) + K8_EMIT_WORDS) / K8_EMIT_WORDS;
-      }
+      if (r >= NR) c[k] = 0;  // (scratch beyond the runs)
+      // emission tasks of the run: K8_EMIT_WORDS destination words each
+      nw[k] = c[k] ? (((g[k] + c[k] - 1) >> 6) - (g[k] >> 6) + K8_EMIT_WORDS) / K8_EMIT_WORDS : 0u;
       sc += c[k];
       sw += nw[k];
     }
     uint32_t pc = warp_incl_scan(sc) - sc, pw = warp_incl_scan(sw) - sw;
-    __syncwarp();
+    uint32_t P[PER], Wp[PER];
 #pragma unroll
     for (int k = 0; k < PER; ++k) {
-      const int r = lane * PER + k;
-      if (r < NR) {
-        tt.lb[r] = pc;  // (lb is free once gs is set) P of run r
-        tt.wpre[r] = (uint16_t)pw;
-      }
+      P[k] = pc;
+      Wp[k] = pw;
       pc += c[k];
       pw += nw[k];
     }
+    __syncwarp();
+    if constexpr (PER == 8) {
+      reinterpret_cast<uint4*>(tt.lb)[2 * lane] = make_uint4(P[0], P[1], P[2], P[3]);  // (lb is free once gs is set)
+      reinterpret_cast<uint4*>(tt.lb)[2 * lane + 1] = make_uint4(P[4], P[5], P[6], P[7]);
+      reinterpret_cast<uint4*>(tt.wpre)[lane] =
+          make_uint4(Wp[0] | (Wp[1] << 16), Wp[2] | (Wp[3] << 16), Wp[4] | (Wp[5] << 16), Wp[6] | (Wp[7] << 16));
+    } else {
+#pragma unroll
+      for (int k = 0; k < PER; ++k) {
+        const int r = lane * PER + k;
+        if (r < NR) {
+          tt.lb[r] = P[k];
+          tt.wpre[r] = (uint16_t)Wp[k];
+        }
+      }
+    }
     if (lane == 31) tt.wpre[NR] = (uint16_t)pw;
     __syncwarp();
+    uint32_t lsv[PER];
 #pragma unroll
     for (int k = 0; k < PER; ++k) {
       const int r = lane * PER + k;
-      if (r < NR) tt.ls[r] = (uint16_t)(tt.lb[r] - tt.lb[(1 << (31 - __clz(r + 2))) - 2]);
+      lsv[k] = r < NR ? P[k] - tt.lb[(1 << (31 - __clz(r + 2))) - 2] : 0u;
+    }
+    if constexpr (PER == 8) {
+      reinterpret_cast<uint4*>(tt.ls)[lane] =
+          make_uint4(lsv[0] | (lsv[1] << 16), lsv[2] | (lsv[3] << 16), lsv[4] | (lsv[5] << 16), lsv[6] | (lsv[7] << 16));
+    } else {
+#pragma unroll
+      for (int k = 0; k < PER; ++k) {
+        const int r = lane * PER + k;
+        if (r < NR) tt.ls[r] = (uint16_t)lsv[k];
+      }
     }
   }
 }
@@ -608,11 +645,13 @@ __global__ void __launch_bounds__(T8_WARPS * 32) tiles8_kernel(const Pass8Args a
     table8_compute<W>(tt, s_base, lane);
     __syncwarp();
     TabW<W>* o = out + tile;
-    for (int r = lane; r < TabW<W>::NRP; r += 32) {
-      o->gs[r] = tt.gs[r];
-      o->cnt[r] = tt.cnt[r];
-      o->ls[r] = tt.ls[r];
-      o->wpre[r] = tt.wpre[r];
+    constexpr int NRP = TabW<W>::NRP;  // (a multiple of 8: every field is whole 16-byte vectors)
+    for (int i = lane; i < NRP / 4; i += 32)
+      reinterpret_cast<uint4*>(o->gs)[i] = reinterpret_cast<const uint4*>(tt.gs)[i];
+    for (int i = lane; i < NRP / 8; i += 32) {
+      reinterpret_cast<uint4*>(o->cnt)[i] = reinterpret_cast<const uint4*>(tt.cnt)[i];
+      reinterpret_cast<uint4*>(o->ls)[i] = reinterpret_cast<const uint4*>(tt.ls)[i];
+      reinterpret_cast<uint4*>(o->wpre)[i] = reinterpret_cast<const uint4*>(tt.wpre)[i];
     }
     __syncwarp();
   }
