@@ -40,9 +40,9 @@ struct Q8Smem {
   static constexpr size_t tab = 2 * (size_t)T;                              // after the ping-pong orders
   static constexpr size_t bits = tab + sizeof(TabW<W>);                     // levels 1..W-1, NC + 4 words each
   static constexpr size_t gbuf = bits + (size_t)(W - 1) * (NC + 4) * 4;    // 2 x T/8 run flag bytes
-  static constexpr size_t za = gbuf + 2 * (size_t)(T / 8);                  // T/32 u32: classes 0|2 prefix per 4 runs
-  static constexpr size_t tot = za + (size_t)(T / 32) * 4;                  // [4 regions][warps] uint2 warp totals
-  static constexpr size_t lut = tot + 4 * (size_t)(T / 1024) * 8;          // 256 sort selectors
+  static constexpr size_t za = gbuf + 2 * (size_t)(T / 8);                  // T/32 u16: zero prefix per 4 half-runs
+  static constexpr size_t tot = za + (size_t)(T / 32) * 2;                  // [2 regions][warps] uint2 warp totals
+  static constexpr size_t lut = tot + 2 * (size_t)(T / 1024) * 8;          // 256 sort selectors
   static constexpr size_t mbar = lut + 1024;
   static constexpr size_t total = mbar + 16;
 };
@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(K8_TILE / 32, K8_CTAS) level_pass8q_kernel(con
   TabW<W>& tt = *reinterpret_cast<TabW<W>*>(smem + L::tab);
   uint32_t* bits = reinterpret_cast<uint32_t*>(smem + L::bits) - (NC + 4);  // level j at j (NC + 4)
   uint8_t* bits8 = reinterpret_cast<uint8_t*>(bits);
-  uint32_t* za32 = reinterpret_cast<uint32_t*>(smem + L::za);  // per 4th half-run: b_j zeros before it
+  uint16_t* za16 = reinterpret_cast<uint16_t*>(smem + L::za);  // per 4th half-run: b_j zeros before it
   uint2* s_tot = reinterpret_cast<uint2*>(smem + L::tot);
   uint32_t* s_lut = reinterpret_cast<uint32_t*>(smem + L::lut);
 
@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(K8_TILE / 32, K8_CTAS) level_pass8q_kernel(con
         if ((tid & 1) == 0) {  // half-run 2t of the region is a 4th half-run: the concatenation's offsets
           const int q4 = (k * HR + 2 * tid) >> 2;
           if (triple) cpre[q4] = make_uint2(P0 | (P2 << 16), P1 | (P3 << 16));
-          else za32[q4] = P0 + P2;  // b_j zeros before it
+          else za16[q4] = (uint16_t)(P0 + P2);  // b_j zeros before it
         }
         if (triple) continue;  // no scatter
         // the run's class bases as 16-bit pairs (classes 0|2, 1|3); a half's
@@ -294,8 +294,8 @@ __global__ void __launch_bounds__(K8_TILE / 32, K8_CTAS) level_pass8q_kernel(con
       const uint32_t ex = __reduce_add_sync(FULL, lane < wid ? wv : 0u) + incl - pk;
       const uint32_t tot = __reduce_add_sync(FULL, wv);
       if ((tid & 1) == 0) {  // zeros before the run = its position - the ones before it
-        za32[(2 * tid) >> 2] = (uint32_t)(RUN * tid) - (ex & 0xFFFFu);
-        za32[(HR + 2 * tid) >> 2] = (uint32_t)(RG + RUN * tid) - ((tot & 0xFFFFu) + (ex >> 16));
+        za16[(2 * tid) >> 2] = (uint16_t)((uint32_t)(RUN * tid) - (ex & 0xFFFFu));
+        za16[(HR + 2 * tid) >> 2] = (uint16_t)((uint32_t)(RG + RUN * tid) - ((tot & 0xFFFFu) + (ex >> 16)));
       }
       Zt = (uint32_t)T - (tot & 0xFFFFu) - (tot >> 16);
     }
@@ -307,7 +307,7 @@ __global__ void __launch_bounds__(K8_TILE / 32, K8_CTAS) level_pass8q_kernel(con
       const uint32_t mw = *mwp;
       if (j == 0 && W >= 4) *mwp = 0u;  // level W-1 (OR-ed later) lent its array
       const uint2 cp = triple ? cpre[tid] : make_uint2(0u, 0u);
-      const uint32_t zpos = triple ? (cp.x & 0xFFFFu) + (cp.x >> 16) : za32[tid];
+      const uint32_t zpos = triple ? (cp.x & 0xFFFFu) + (cp.x >> 16) : za16[tid];
       uint32_t accz = 0, acco = 0, fz = 0;
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
@@ -356,6 +356,7 @@ __global__ void __launch_bounds__(K8_TILE / 32, K8_CTAS) level_pass8q_kernel(con
 template <int W>
 cudaError_t launch_pass8q(const Pass8Args& a, void* tabs, cudaStream_t s) {
   constexpr size_t smem = Q8Smem<W>::total;
+  static_assert((smem + 1024) * K8_CTAS <= 228 * 1024, "K8_CTAS CTAs per SM must fit the shared memory");
   auto kern = level_pass8q_kernel<W>;
   cudaError_t e0 = ensure_smem_attr((const void*)kern, (int)smem, true);
   if (e0 != cudaSuccess) return e0;
