@@ -33,18 +33,28 @@
 //
 // Included from k8.cuh (same translation unit, anonymous namespace).
 
+#ifndef K8Q_LUT
+// copies of the sort LUT, interleaved (entry e of copy c at e K8Q_LUT + c, lane
+// l reads copy l % K8Q_LUT): a warp's 32 random lookups spread over 32 / K8Q_LUT
+// lanes per copy, each copy on its own banks
+#define K8Q_LUT 1  // (measured: 4 interleaved copies slower, 2.85 vs 2.82 ms on c2)
+#endif
+
 template <int W>
 struct Q8Smem {
   static constexpr int T = K8_TILE;
   static constexpr int NC = T / 32;
-  static constexpr size_t tab = 2 * (size_t)T;                              // after the ping-pong orders
-  static constexpr size_t bits = tab + sizeof(TabW<W>);                     // levels 1..W-1, NC + 4 words each
+  static constexpr size_t bits = 2 * (size_t)T;                             // levels 1..W-1, NC + 4 words each
   static constexpr size_t gbuf = bits + (size_t)(W - 1) * (NC + 4) * 4;    // 2 x T/8 run flag bytes
   static constexpr size_t za = gbuf + 2 * (size_t)(T / 8);                  // T/32 u16: zero prefix per 4 half-runs
   static constexpr size_t tot = za + (size_t)(T / 32) * 2;                  // [2 regions][warps] uint2 warp totals
-  static constexpr size_t lut = tot + 2 * (size_t)(T / 1024) * 8;          // 256 sort selectors
-  static constexpr size_t mbar = lut + 1024;
+  static constexpr size_t lut = tot + 2 * (size_t)(T / 1024) * 8;          // K8Q_LUT interleaved copies of the 256 sort selectors
+  static constexpr size_t mbar = lut + 1024 * K8Q_LUT;                     // tile, then run table
   static constexpr size_t total = mbar + 16;
+  // the run table (needed by the emission only) lands in the final round's
+  // unused destination buffer, above everything that round keeps there
+  static constexpr int JL = (W & 1) ? W - 3 : W - 2;
+  static constexpr size_t tab = (size_t)(((JL >> 1) + 1) & 1) * T + 12288;
 };
 
 // The 8 flags of bit `sh` of a run's bytes (x0: bytes 0-3, x1: bytes 4-7).
@@ -98,36 +108,31 @@ __global__ void __launch_bounds__(K8_TILE / 32, K8_CTAS) level_pass8q_kernel(con
   static_assert(NW <= 32 && T <= 32768, "16-bit store bases (offsets inside the destination buffer)");
   extern __shared__ __align__(128) unsigned char smem[];
   TabW<W>& tt = *reinterpret_cast<TabW<W>*>(smem + L::tab);
+  static_assert(T == 16384 && 12288 + sizeof(TabW<W>) <= (size_t)T, "run table slot");
   uint32_t* bits = reinterpret_cast<uint32_t*>(smem + L::bits) - (NC + 4);  // level j at j (NC + 4)
   uint8_t* bits8 = reinterpret_cast<uint8_t*>(bits);
   uint16_t* za16 = reinterpret_cast<uint16_t*>(smem + L::za);  // per 4th half-run: b_j zeros before it
   uint2* s_tot = reinterpret_cast<uint2*>(smem + L::tot);
   uint32_t* s_lut = reinterpret_cast<uint32_t*>(smem + L::lut);
+  const uint32_t* my_lut = s_lut + (threadIdx.x % K8Q_LUT);  // this lane's copy
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const uint8_t* text = a.src;
   const uint32_t sb = (uint32_t)__cvta_generic_to_shared(smem);
-  const uint32_t mbar = sb + (uint32_t)L::mbar;
+  const uint32_t mbar = sb + (uint32_t)L::mbar, mbar_tab = mbar + 8u;
   const int64_t tile = blockIdx.x;
   const int64_t base = tile * T;
   const int cnt = (int)min((int64_t)T, a.n - base);
   const bool bulk = (((uintptr_t)text) & 15) == 0 && cnt == T;
   if (tid == 0) {
     mbar_init(mbar, 1);
+    mbar_init(mbar_tab, 1);
     fence_mbar_init();
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar),
-                 "r"((uint32_t)(sizeof(TabW<W>) + (bulk ? T : 0)))
-                 : "memory");
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     sb + (uint32_t)L::tab),
-                 "l"(tabs + tile), "r"((uint32_t)sizeof(TabW<W>)), "r"(mbar)
-                 : "memory");
-    if (bulk)
-      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(sb),
-                   "l"(text + base), "r"((uint32_t)T), "r"(mbar)
-                   : "memory");
+    if (bulk) bulk_load(sb, text + base, (uint32_t)T, mbar);
+    else asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(mbar) : "memory");
+    if (L::JL == 0) bulk_load(sb + (uint32_t)L::tab, tabs + tile, (uint32_t)sizeof(TabW<W>), mbar_tab);
   }
-  for (int i = tid; i < 256; i += NT) s_lut[i] = g_sort_lut.sel[i];
+  for (int i = tid; i < 256 * K8Q_LUT; i += NT) s_lut[i] = g_sort_lut.sel[i / K8Q_LUT];
   // the levels filled by OR-ing bit strings (odd levels: the skipped level of
   // every round) start at zero
 #pragma unroll
@@ -150,6 +155,8 @@ __global__ void __launch_bounds__(K8_TILE / 32, K8_CTAS) level_pass8q_kernel(con
 #pragma unroll
   for (int j = 0; j < W; j += 2) {
     const int sh = W - 1 - j;
+    if (j == L::JL && j > 0 && tid == 0)  // the run table into the buffer the final round leaves unused
+      bulk_load(sb + (uint32_t)L::tab, tabs + tile, (uint32_t)sizeof(TabW<W>), mbar_tab);
     uint8_t* const cur = smem + (size_t)((j >> 1) & 1) * T;
     uint8_t* const mb = j == 0 ? m0b : bits8 + j * 4 * (NC + 4);
     // odd width: the last round starts at A_W-3 and emits three levels without a
@@ -175,12 +182,12 @@ __global__ void __launch_bounds__(K8_TILE / 32, K8_CTAS) level_pass8q_kernel(con
         uint32_t mbits, gbits;
         const uint32_t m = run_flags8(xw[2 * h], xw[2 * h + 1], sh, mbits);
         mb[r8] = (uint8_t)m;
-        const uint32_t sel = s_lut[flags_lo(m)];
+        const uint32_t sel = my_lut[flags_lo(m) * K8Q_LUT];
         const uint32_t s0 = prmt(xw[2 * h], xw[2 * h + 1], sel), s1 = prmt(xw[2 * h], xw[2 * h + 1], sel >> 16);
         const uint32_t g = run_flags8(s0, s1, sh - 1, gbits);
         gb[r8] = (uint8_t)g;
         if (quad || triple) {
-          const uint32_t sel2 = s_lut[flags_lo(g)];
+          const uint32_t sel2 = my_lut[flags_lo(g) * K8Q_LUT];
           xw[2 * h] = prmt(s0, s1, sel2);
           xw[2 * h + 1] = prmt(s0, s1, sel2 >> 16);
           if (triple) {
@@ -299,6 +306,8 @@ __global__ void __launch_bounds__(K8_TILE / 32, K8_CTAS) level_pass8q_kernel(con
       }
       Zt = (uint32_t)T - (tot & 0xFFFFu) - (tot >> 16);
     }
+    // (the run table's slot was last read here: order that before the bulk copy of the next round)
+    if (j + 2 == L::JL) fence_proxy_async_smem();
     bar_sync(1, NT);
     // L_j+1 from the half-runs' flag pieces: thread t owns half-runs 4t .. 4t+3
     {
@@ -350,7 +359,8 @@ __global__ void __launch_bounds__(K8_TILE / 32, K8_CTAS) level_pass8q_kernel(con
     }
   }
   bar_sync(1, NT);  // every level's bits are in place
-  emit_levels8<W, NC>(tt, bits, a.words, a.nwords, tid, NT, smem);  // stage buffers are free now
+  mbar_wait(mbar_tab, 0);
+  emit_levels8<W, NC>(tt, bits, a.words, a.nwords, tid, NT, smem);  // (coarse map: stage buffer 0's first bytes)
 }
 
 template <int W>
