@@ -105,6 +105,9 @@ __global__ void __launch_bounds__(K8_TILE / 32, K8_CTAS) level_pass8q_kernel(con
   constexpr int NC = T / 32;
   constexpr int NW = NT / 32;
   using L = Q8Smem<W>;
+  // the class-sorted runs stay in registers across the round's barrier where they
+  // fit the 32 registers without spills (measured: W = 8 2.82 -> 2.80 ms; W = 4, 5, 7 spill)
+  constexpr bool KEEP_U = W == 8 || W == 6;
   static_assert(NW <= 32 && T <= 32768, "16-bit store bases (offsets inside the destination buffer)");
   extern __shared__ __align__(128) unsigned char smem[];
   TabW<W>& tt = *reinterpret_cast<TabW<W>*>(smem + L::tab);
@@ -170,6 +173,7 @@ __global__ void __launch_bounds__(K8_TILE / 32, K8_CTAS) level_pass8q_kernel(con
     uint8_t* const hb = nxtb + T / 8;
     uint2* const cpre = reinterpret_cast<uint2*>(nxtb + 2 * (T / 8));
     uint32_t cA[QR], cB[QR], ff[QR], ee[QR];  // per run: class counts of its halves (bytes), 10-bit sums, scan
+    uint4 ukeep[QR];  // (KEEP_U) the class-sorted runs across the barrier
     uint32_t ones[QR];
 #pragma unroll
     for (int k = 0; k < QR; ++k) {
@@ -206,8 +210,11 @@ __global__ void __launch_bounds__(K8_TILE / 32, K8_CTAS) level_pass8q_kernel(con
           o += __popc(mbits);
         }
       }
-      if (quad)  // the class-sorted halves go back to the run's own slot (read again after the barrier)
-        reinterpret_cast<uint4*>(cur + k * RG)[tid] = make_uint4(xw[0], xw[1], xw[2], xw[3]);
+      if (quad) {
+        if (KEEP_U) ukeep[k] = make_uint4(xw[0], xw[1], xw[2], xw[3]);
+        else  // the class-sorted halves go back to the run's own slot (read again after the barrier)
+          reinterpret_cast<uint4*>(cur + k * RG)[tid] = make_uint4(xw[0], xw[1], xw[2], xw[3]);
+      }
       if (quad || triple) {
         cA[k] = cb[0];
         cB[k] = cb[1];
@@ -264,7 +271,7 @@ __global__ void __launch_bounds__(K8_TILE / 32, K8_CTAS) level_pass8q_kernel(con
         // the run's class bases as 16-bit pairs (classes 0|2, 1|3); a half's
         // class c byte kk goes to base_c + (half 1: half 0's class-c count) - S_c + kk
         const uint32_t BA = P0 | ((C2 + P2) << 16), BB = (C1 + P1) | ((C3 + P3) << 16);
-        const uint4 uk = reinterpret_cast<const uint4*>(cur + k * RG)[tid];
+        const uint4 uk = KEEP_U ? ukeep[k] : reinterpret_cast<const uint4*>(cur + k * RG)[tid];
         const uint32_t uw[4] = {uk.x, uk.y, uk.z, uk.w};
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
