@@ -600,6 +600,21 @@ __device__ __forceinline__ void emit_levels8(const TabW<W>& tt, const uint32_t* 
     const uint32_t wlast = (g + c - 1) >> 6;
     const int ls = tt.ls[r];
     uint64_t* dst0 = words + (int64_t)j * nwords + w0;
+#if K8_EMIT_WORDS == 2
+    // the task's source bits are contiguous: [ls + lo0 - g, + up to 128) -- five
+    // words from three aligned 64-bit loads instead of two 3-word extractions
+    const uint32_t wb0 = w0 << 6;
+    const uint32_t lo0 = g > wb0 ? g : wb0;
+    const int src = ls + (int)(lo0 - g);
+    const uint2* L2 = reinterpret_cast<const uint2*>(L) + (src >> 6);
+    const uint2 qa = L2[0], qb = L2[1], qc = L2[2];
+    const bool odd = (src >> 5) & 1;
+    const uint32_t x0 = odd ? qa.y : qa.x, x1 = odd ? qb.x : qa.y, x2 = odd ? qb.y : qb.x, x3 = odd ? qc.x : qb.y,
+                   x4 = odd ? qc.y : qc.x;
+    const uint32_t sh = src & 31;
+    const uint64_t s0 = (uint64_t)__funnelshift_r(x0, x1, sh) | ((uint64_t)__funnelshift_r(x1, x2, sh) << 32);
+    const uint64_t s1 = (uint64_t)__funnelshift_r(x2, x3, sh) | ((uint64_t)__funnelshift_r(x3, x4, sh) << 32);
+#endif
 #pragma unroll
     for (int u = 0; u < K8_EMIT_WORDS; ++u) {
       const uint32_t wd = w0 + u;
@@ -608,7 +623,14 @@ __device__ __forceinline__ void emit_levels8(const TabW<W>& tt, const uint32_t* 
       const uint32_t lo = g > wb ? g : wb;
       const uint32_t hi = (g + c) < wb + 64 ? (g + c) : wb + 64;
       const int len = (int)(hi - lo);
+#if K8_EMIT_WORDS == 2
+      // word 0: source bits [0, len) of s0 s1; word 1: [64 - (lo0 - wb0), + len)
+      const uint32_t off = u ? 64u - (lo0 - wb0) : 0u;  // (word 1 starts where word 0's 64 - its offset bits end)
+      const uint64_t raw = off == 0 ? s0 : off == 64 ? s1 : ((s0 >> off) | (s1 << (64 - off)));
+      const uint64_t v = (len >= 64 ? raw : (raw & ((1ull << len) - 1))) << (lo - wb);
+#else
       const uint64_t v = extract_bits(L, ls + (int)(lo - g), len) << (lo - wb);
+#endif
       // whole word: plain store; run edge: OR (shared with a neighbouring run), skipped if empty
       asm volatile(
           "{\n\t.reg .pred p, q;\n\tsetp.eq.s32 p, %2, 64;\n\tsetp.ne.and.b64 q, %1, 0, !p;\n\t"
