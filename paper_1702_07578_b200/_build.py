@@ -29,7 +29,7 @@ LIB_NAME = "_wvlt_b200.so"
 LIB_PATH = PKG_DIR / LIB_NAME
 
 SOURCES = [CSRC / "wvlt_b200.cu"]
-INCLUDED = [CSRC / "support.cuh", CSRC / "k8.cuh", CSRC / "k8q.cuh", CSRC / "k16.cuh", CSRC / "k32.cuh"]  # #included by wvlt_b200.cu
+INCLUDED = [CSRC / "support.cuh", CSRC / "k8.cuh", CSRC / "k8q.cuh", CSRC / "k16.cuh", CSRC / "k16q.cuh", CSRC / "k32.cuh"]  # #included by wvlt_b200.cu
 HEADERS = [INCLUDE / "wvlt_b200.h"]
 
 NVCC_FLAGS = [

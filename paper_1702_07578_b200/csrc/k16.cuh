@@ -334,6 +334,13 @@ cudaError_t launch_pass16(const Pass16Args& a, const void* tabs, cudaStream_t s)
   return cudaGetLastError();
 }
 
+}  // namespace
+#ifndef K16_QUAD
+#define K16_QUAD 1  // even widths: two levels per shared-memory round (k16q.cuh)
+#endif
+#include "k16q.cuh"
+namespace {
+
 // Workspace of the 2-byte fused pass (its tables; the byte output is separate).
 struct K16Layout {
   size_t off_tcnt, off_tpre, off_chunk, off_totals, off_base, off_baseW, off_tabs, total;
@@ -428,7 +435,7 @@ int build_k16(const uint16_t* src, int64_t n, int W, uint64_t* level_words, int6
   a.baseW = baseW;
   switch (W) {
 #define WVLT_K16P(WW) \
-  case WW: e = launch_pass16<WW>(a, tabs, s); break;
+  case WW: e = (K16_QUAD && (WW % 2 == 0)) ? launch_pass16q<(WW % 2 == 0 ? WW : 2)>(a, tabs, s) : launch_pass16<WW>(a, tabs, s); break;
     WVLT_K16P(2) WVLT_K16P(3) WVLT_K16P(4) WVLT_K16P(5) WVLT_K16P(6) WVLT_K16P(7) WVLT_K16P(8)
 #undef WVLT_K16P
   }

@@ -459,3 +459,25 @@ def test_byte_pass_class_extremes(kind, sigma):
     }
     for name, text in texts.items():
         assert wv.dump_structure(wv.build_structure(text, sigma, kind)) == ref_dump(text, sigma, kind), (sigma, name)
+
+
+@pytest.mark.parametrize("kind", ["wm", "wt"])
+@pytest.mark.parametrize("sigma", [600, 1500, 3000, 5000, 12000, 20000, 1 << 16])
+def test_two_byte_pass_every_width(kind, sigma):
+    """The fused 2-byte pass at every width W = live bits - 8 (2..8; even widths
+    run two levels per round, k16q.cuh): several tiles and a partial one,
+    uniform / Zipf / constant / long runs / single-class warp regions, vs the oracle."""
+    rng = np.random.default_rng(sigma + (kind == "wt"))
+    n = 3 * 16384 + 4 * 333 + 7
+    top = sigma - 1
+    texts = {
+        "uniform": rng.integers(0, sigma, n),
+        "zipf": rng.permutation(sigma)[rng.zipf(1.1, n) % sigma],
+        "const": np.full(n, top),
+        "runs": np.repeat(rng.integers(0, sigma, n // 700 + 1), 700)[:n],
+        "blocks256": np.repeat(rng.integers(0, sigma, n // 256 + 1), 256)[:n],
+        "alt": np.where(np.arange(n) % 2 == 0, 0, top),
+    }
+    for name, t in texts.items():
+        text = t.astype(np.uint16)
+        assert wv.dump_structure(wv.build_structure(text, sigma, kind)) == ref_dump(text, sigma, kind), (sigma, name)
