@@ -1615,10 +1615,18 @@ __device__ __forceinline__ uint64_t merge_word(int64_t wd, int64_t nbits, const 
 constexpr int MERGE_WORDS_PER_LANE = MERGE_WPL;
 
 // destination words [wlo, whi) of one gather_bits plan; warp `gw` of `nwarps`
+// PEER: task t's source is rank ranks[t]'s level (srcs[ranks[t]]) instead of `src`
+// (merge_word_peer is defined below)
+__device__ __forceinline__ uint64_t merge_word_peer(int64_t wd, int64_t nbits, const int64_t* __restrict__ bounds,
+                                                    const int64_t* __restrict__ starts,
+                                                    const int32_t* __restrict__ ranks,
+                                                    const uint64_t* const* __restrict__ srcs, int64_t t);
+template <bool PEER>
 __device__ __forceinline__ void merge_range(uint64_t* __restrict__ dst, int64_t wlo, int64_t whi, int64_t nbits,
                                             const int64_t* __restrict__ bounds,
                                             const int64_t* __restrict__ src_starts, int64_t ntasks,
-                                            const uint64_t* __restrict__ src, int64_t gw, int64_t nwarps) {
+                                            const uint64_t* __restrict__ src, const int32_t* __restrict__ ranks,
+                                            const uint64_t* const* __restrict__ srcs, int64_t gw, int64_t nwarps) {
   // a warp owns 32 * MERGE_WORDS_PER_LANE consecutive destination words
   // (coalesced stores; within a task coalesced source loads); lane 0
   // binary-searches the task of the warp's first bit, every lane walks forward
@@ -1638,50 +1646,71 @@ __device__ __forceinline__ void merge_range(uint64_t* __restrict__ dst, int64_t 
     }
     t0 = __shfl_sync(FULL, t0, 0);
     uint64_t v[MERGE_WORDS_PER_LANE];
-    // the task of every word's first bit first (small, cached arrays), then all
-    // source loads at once (independent, in flight together), then the words
-    // that straddle a task boundary on the slow path
-    int64_t sp[MERGE_WORDS_PER_LANE];
-    int nbk[MERGE_WORDS_PER_LANE];
-    uint32_t single = 0;
+    // the task of every word's first bit first, then all source loads at once
+    // (independent, in flight together), then the words that straddle a task
+    // boundary on the slow path.  The current task's bounds, source start and
+    // source level stay in registers: a lane's words are 2048 bits apart and
+    // mostly fall into the same piece, so the small plan arrays are read only
+    // when the task changes (no dependent lookups in front of the source loads).
+    const unsigned long long* pw[MERGE_WORDS_PER_LANE];  // first source word of a one-piece destination word
+    int shnb[MERGE_WORDS_PER_LANE];                      // its shift | (bits << 8); -1 - (t - t0): slow path from task t
     int64_t t = t0;
+    int64_t b0 = 0, b1 = 0, st = 0;
+    const unsigned long long* sbase = reinterpret_cast<const unsigned long long*>(src);
+    bool have = false;
 #pragma unroll
     for (int k = 0; k < MERGE_WORDS_PER_LANE; ++k) {
       const int64_t wd = w0 + 32 * k + lane;
       const int64_t here = wd << 6;
-      sp[k] = -1;
-      nbk[k] = 0;
+      pw[k] = nullptr;
+      shnb[k] = 0;
       if (wd < whi && here < nbits) {
-        while (__ldg(bounds + t + 1) <= here) ++t;
+        if (!have || b1 <= here) {
+          if (!have) b1 = __ldg(bounds + t + 1);
+          while (b1 <= here) {
+            ++t;
+            b1 = __ldg(bounds + t + 1);
+          }
+          b0 = __ldg(bounds + t);
+          st = __ldg(src_starts + t);
+          if (PEER) sbase = reinterpret_cast<const unsigned long long*>(srcs[__ldg(ranks + t)]);
+          have = true;
+        }
         const int64_t nb = min((int64_t)64, nbits - here);
-        if (__ldg(bounds + t + 1) >= here + nb) {
-          single |= 1u << k;
-          sp[k] = __ldg(src_starts + t) + (here - __ldg(bounds + t));
-          nbk[k] = (int)nb;
+        if (b1 >= here + nb) {
+          const int64_t pos = st + (here - b0);
+          pw[k] = sbase + (pos >> 6);
+          shnb[k] = (int)(pos & 63) | ((int)nb << 8);
+        } else {
+          shnb[k] = -1 - (int)(t - t0);
         }
       }
     }
-    const unsigned long long* s64 = reinterpret_cast<const unsigned long long*>(src);
     uint64_t lo[MERGE_WORDS_PER_LANE], hi[MERGE_WORDS_PER_LANE];
 #pragma unroll
     for (int k = 0; k < MERGE_WORDS_PER_LANE; ++k) {
       lo[k] = hi[k] = 0;
-      if ((single >> k) & 1u) {
-        lo[k] = __ldg(s64 + (sp[k] >> 6));
-        // the next source word only when the bits run into it (never past the source's end)
-        if ((int)(sp[k] & 63) + nbk[k] > 64) hi[k] = __ldg(s64 + (sp[k] >> 6) + 1);
+      if (pw[k]) {
+        // the next source word only when the bits run into it (never past the source's end);
+        // peer memory: plain loads (written by another device before the collective)
+        lo[k] = PEER ? pw[k][0] : __ldg(pw[k]);
+        if ((shnb[k] & 63) + (shnb[k] >> 8) > 64) hi[k] = PEER ? pw[k][1] : __ldg(pw[k] + 1);
       }
     }
 #pragma unroll
     for (int k = 0; k < MERGE_WORDS_PER_LANE; ++k) {
       const int64_t wd = w0 + 32 * k + lane;
-      if ((single >> k) & 1u) {
-        const int sh = (int)(sp[k] & 63);
+      if (pw[k]) {
+        const int sh = shnb[k] & 63, nbk = shnb[k] >> 8;
         uint64_t x = sh ? ((lo[k] >> sh) | (hi[k] << (64 - sh))) : lo[k];
-        if (nbk[k] < 64) x &= (1ull << nbk[k]) - 1ull;
+        if (nbk < 64) x &= (1ull << nbk) - 1ull;
         v[k] = x;
+      } else if (shnb[k] < 0) {
+        const int64_t tk = t0 + (int64_t)(-1 - shnb[k]);
+        v[k] = PEER ? merge_word_peer(wd, nbits, bounds, src_starts, ranks, srcs, tk)
+                    : merge_word(wd, nbits, bounds, src_starts, src, tk);
       } else {
-        v[k] = (wd < whi && (wd << 6) < nbits) ? merge_word(wd, nbits, bounds, src_starts, src, t0) : 0ull;
+        v[k] = 0ull;
       }
     }
 #pragma unroll
@@ -1696,8 +1725,9 @@ __global__ void __launch_bounds__(256) merge_bits_kernel(uint64_t* __restrict__ 
                                                          int64_t nbits, const int64_t* __restrict__ bounds,
                                                          const int64_t* __restrict__ src_starts, int64_t ntasks,
                                                          const uint64_t* __restrict__ src) {
-  merge_range(dst, wlo, whi, nbits, bounds, src_starts, ntasks, src,
-              (((int64_t)blockIdx.x * blockDim.x) >> 5) + (threadIdx.x >> 5), ((int64_t)gridDim.x * blockDim.x) >> 5);
+  merge_range<false>(dst, wlo, whi, nbits, bounds, src_starts, ntasks, src, nullptr, nullptr,
+                     (((int64_t)blockIdx.x * blockDim.x) >> 5) + (threadIdx.x >> 5),
+                     ((int64_t)gridDim.x * blockDim.x) >> 5);
 }
 
 // Multi-GPU merge over peer memory: every level's owned destination words are
@@ -1741,43 +1771,16 @@ __global__ void __launch_bounds__(256) merge_peer_kernel(uint64_t* __restrict__ 
                                                          const int32_t* __restrict__ ranks_all,
                                                          const int64_t* __restrict__ task_off,
                                                          const uint64_t* const* __restrict__ level_src, int nranks) {
-  constexpr int CH = 32 * MERGE_WORDS_PER_LANE;
   const int l = blockIdx.y;
   const int64_t t_lo = task_off[l], ntasks = task_off[l + 1] - t_lo;
   if (ntasks <= 0) return;
-  const int64_t* bounds = bounds_all + bounds_off[l];
-  const int64_t* starts = starts_all + t_lo;
-  const int32_t* ranks = ranks_all + t_lo;
-  const uint64_t* const* srcs = level_src + (int64_t)l * nranks;
-  uint64_t* drow = dst + (int64_t)l * dst_row - wlo;
-  const int lane = threadIdx.x & 31;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t w0 = wlo + ((((int64_t)blockIdx.x * blockDim.x) >> 5) + (threadIdx.x >> 5)) * CH; w0 < whi;
-       w0 += nwarps * CH) {
-    int64_t t0 = 0;
-    if (lane == 0 && (w0 << 6) < nbits) {
-      int64_t lo = 0, hi = ntasks;  // last t with bounds[t] <= bit
-      const int64_t bit = w0 << 6;
-      while (hi - lo > 1) {
-        const int64_t mid = (lo + hi) >> 1;
-        if (__ldg(bounds + mid) <= bit) lo = mid;
-        else hi = mid;
-      }
-      t0 = lo;
-    }
-    t0 = __shfl_sync(FULL, t0, 0);
-    uint64_t v[MERGE_WORDS_PER_LANE];
-#pragma unroll
-    for (int k = 0; k < MERGE_WORDS_PER_LANE; ++k) {
-      const int64_t wd = w0 + 32 * k + lane;
-      v[k] = (wd < whi && (wd << 6) < nbits) ? merge_word_peer(wd, nbits, bounds, starts, ranks, srcs, t0) : 0ull;
-    }
-#pragma unroll
-    for (int k = 0; k < MERGE_WORDS_PER_LANE; ++k) {
-      const int64_t wd = w0 + 32 * k + lane;
-      if (wd < whi) __stcs(reinterpret_cast<unsigned long long*>(drow) + wd, v[k]);
-    }
-  }
+  // the same word loop as the one-source merge: every word's task first, then
+  // all of a lane's source loads in flight together (peer reads over NVLink
+  // have a few microseconds of latency), words that straddle pieces last
+  merge_range<true>(dst + (int64_t)l * dst_row - wlo, wlo, whi, nbits, bounds_all + bounds_off[l], starts_all + t_lo,
+                    ntasks, nullptr, ranks_all + t_lo, level_src + (int64_t)l * nranks,
+                    (((int64_t)blockIdx.x * blockDim.x) >> 5) + (threadIdx.x >> 5),
+                    ((int64_t)gridDim.x * blockDim.x) >> 5);
 }
 
 // Merge plan of the sharded build on the device (construct._merge_plan,

@@ -142,7 +142,12 @@ def main():
     ap.add_argument("--ranks", nargs="*", type=int, default=[2, 4, 8])
     ap.add_argument("--log2n", type=int, default=None)
     ap.add_argument("--no-verify", action="store_true")
+    ap.add_argument("--variant", default=None, help="a tools/variants/<name>.so tuning build instead of the product library")
     a = ap.parse_args()
+    if a.variant:
+        from paper_1702_07578_b200 import _lib
+
+        _lib.load_variant(ROOT / "tools" / "variants" / f"{a.variant}.so")
     for c in a.configs:
         for r in a.ranks:
             run(c, r, (1 << a.log2n) if a.log2n else None, not a.no_verify)
