@@ -474,7 +474,10 @@ def main():
                      "peak_source": peak_src, "limiter": limiter},
         "metric_roofline": {"bytes_per_build": mbytes, "achieved_gbs": mbytes / (ms * 1e-3) / 1e9,
                             "frac": mbytes / (ms * 1e-3) / 1e9 / peak,
-                            "definition": "SURVEY 8d: B = L (n s + n/8), text read once per level + level bits"},
+                            "frac_of_nominal_8tbs": mbytes / (ms * 1e-3) / 1e9 / 8000.0,
+                            "definition": "SURVEY 8d: B = L (n s + n/8), text read once per level + level bits; "
+                                          "frac against the measured copy peak, frac_of_nominal_8tbs against "
+                                          "the 8 TB/s BASELINE.json names"},
         "stages_ms": stages,
         "clocks": clocks,
         "gpu_launches": args.steps * launches_per_build,
