@@ -73,6 +73,21 @@ __device__ __forceinline__ void clear_level_rows(uint64_t* lvl, int64_t nwords, 
   }
 }
 
+#ifndef H8_PLANE_BATCH
+#define H8_PLANE_BATCH 4  // 256-bit loads in flight per lane when counting from bit planes (measured: 4 < 2 < 1 ms)
+#endif
+// 32 bytes, streaming (read once)
+__device__ __forceinline__ void ld256_cs(uint32_t (&r)[8], const uint32_t* p) {
+  asm volatile("ld.global.cs.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "l"(p));
+}
+// exchange the bits selected by m with the bits sh above them
+__device__ __forceinline__ uint32_t delta_swap(uint32_t x, int sh, uint32_t m) {
+  const uint32_t t = ((x >> sh) ^ x) & m;
+  return x ^ t ^ (t << sh);
+}
+
 // It also writes level 0 (the top code bit of every symbol, already in text
 // order), so that level can leave for the host while the rest is built.
 template <int W>
@@ -93,7 +108,9 @@ __global__ void __launch_bounds__(H8_WARPS * 32) hist8_kernel(const uint8_t* __r
   const uint32_t zsrc = zero_row_init<K8_TILE / 64>(s_zero);
   __syncwarp();
   uint32_t vmax = 0;
-  const bool aligned = (((uintptr_t)text) & 15) == 0;
+  uint32_t hi_or = 0;  // (register-plane widths) OR of every word: a bit above the code width = out of range
+  constexpr bool PLANES_K = W <= H8_PLANE_W;
+  const bool aligned32 = (((uintptr_t)text) & (PLANES_K ? 31 : 15)) == 0;  // 256-bit / 128-bit loads
   const int64_t nwarps = (int64_t)gridDim.x * H8_WARPS;
   for (int64_t t = (int64_t)blockIdx.x * H8_WARPS + wid; t < ntiles; t += nwarps) {
     const int64_t first = t * K8_TILE;
@@ -101,19 +118,71 @@ __global__ void __launch_bounds__(H8_WARPS * 32) hist8_kernel(const uint8_t* __r
     // clear this tile's words of levels 1..W-1 (the pass ORs run-edge words)
     clear_level_rows<K8_TILE / 64>(level0, nwords, first >> 6, (int)min((int64_t)(K8_TILE / 64), nwords - (first >> 6)),
                                    W, zsrc, lane);
-    // narrow alphabets count in registers: per 16 symbols the W bit planes
-    // (bit 8 b + u = bit of byte b of word u), one POPC per value
+    // narrow alphabets count in registers from bit planes, one POPC per value
     constexpr bool PLANES = W <= H8_PLANE_W;
     uint32_t acc[PLANES ? NB : 1];
 #pragma unroll
     for (int v = 0; v < (PLANES ? NB : 1); ++v) acc[v] = 0;
-    const bool fast = cnt == K8_TILE && aligned;
-    if (fast) {
+    const bool fast = cnt == K8_TILE && aligned32;
+    if (PLANES && fast) {
+      // narrow alphabets: a lane takes 32 consecutive symbols per step (one 256-bit
+      // load) and turns them into W bit planes of 32 bits, bit 8k + u = symbol
+      // 4u + k (byte k of word u): one shift + one LOP3 per word and plane.  The
+      // values are counted with one POPC per value and 32 symbols; level 0 is
+      // the top plane transposed to text order by four delta swaps and stored
+      // as the lane's own 32-bit half word (coalesced, no shuffles).
+      const uint32_t* t32 = reinterpret_cast<const uint32_t*>(text + first);
+      uint32_t* l0 = reinterpret_cast<uint32_t*>(level0) + (first >> 5);
+      constexpr int NIT = K8_TILE / 32 / 32;
+      constexpr int NB2 = H8_PLANE_BATCH;
+      static_assert(NIT % NB2 == 0, "whole batches");
+      uint32_t qn[NB2][8];
+#pragma unroll
+      for (int k = 0; k < NB2; ++k) ld256_cs(qn[k], t32 + 8 * (k * 32 + lane));
+#pragma unroll 1
+      for (int it0 = 0; it0 < NIT; it0 += NB2) {
+        uint32_t q[NB2][8];
+#pragma unroll
+        for (int k = 0; k < NB2; ++k)
+#pragma unroll
+          for (int u = 0; u < 8; ++u) q[k][u] = qn[k][u];
+        if (it0 + NB2 < NIT) {
+#pragma unroll
+          for (int k = 0; k < NB2; ++k) ld256_cs(qn[k], t32 + 8 * ((it0 + NB2 + k) * 32 + lane));
+        }
+#pragma unroll
+        for (int k = 0; k < NB2; ++k) {
+          uint32_t pl[PLANES ? W : 1], nl[PLANES ? W : 1];
+          if (check) hi_or |= (q[k][0] | q[k][1] | q[k][2] | q[k][3]) | (q[k][4] | q[k][5] | q[k][6] | q[k][7]);
+#pragma unroll
+          for (int b = 0; b < (PLANES ? W : 1); ++b) {
+            uint32_t x = 0;
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+              x |= (u >= b ? q[k][u] << (u - b) : q[k][u] >> (b - u)) & (0x01010101u << u);
+            pl[b] = x;
+            nl[b] = ~x;
+          }
+#pragma unroll
+          for (int v = 0; v < (PLANES ? NB : 1); ++v) {
+            uint32_t m = (v & 1) ? pl[0] : nl[0];
+#pragma unroll
+            for (int b = 1; b < (PLANES ? W : 1); ++b) m &= ((v >> b) & 1) ? pl[b] : nl[b];
+            acc[v] += __popc(m);
+          }
+          uint32_t t = pl[(PLANES ? W : 1) - 1];  // bit (k1 k0 u2 u1 u0) -> bit (u2 u1 u0 k1 k0)
+          t = delta_swap(t, 12, 0x0000F0F0u);
+          t = delta_swap(t, 6, 0x00CC00CCu);
+          t = delta_swap(t, 3, 0x0A0A0A0Au);
+          t = delta_swap(t, 1, 0x22222222u);
+          l0[(it0 + k) * 32 + lane] = t;
+        }
+      }
+    } else if (!PLANES && fast) {
       const uint4* v4 = reinterpret_cast<const uint4*>(text + first);
-      // software-pipelined: the next batch's loads are in flight while this one
-      // is counted (measured: batches of 4 for the register-plane widths, 2 for
-      // the shared-atomic ones)
-      constexpr int NBAT = PLANES ? 4 : H8_ATOMIC_BATCH;
+      // (the widths that count by shared atomics) software-pipelined: the next
+      // batch's loads are in flight while this one is counted
+      constexpr int NBAT = H8_ATOMIC_BATCH;
       uint4 qn[NBAT];
 #pragma unroll
       for (int k = 0; k < NBAT; ++k) qn[k] = __ldcs(v4 + k * 32 + lane);
@@ -136,32 +205,12 @@ __global__ void __launch_bounds__(H8_WARPS * 32) hist8_kernel(const uint8_t* __r
             const uint32_t lo = wd[u] & ((uint32_t)(HALF - 1) * 0x01010101u);
             const uint32_t hb = (wd[u] >> (W - 1)) & 0x01010101u;
             m16 |= ((hb * 0x01020408u) >> 24) << (4 * u);
-            if (!PLANES) {
-              // increment 0x00010001 for a value with its top bit set, else 1, straight
-              // from one PRMT: the low half counts both values of the pair, the high
-              // half the upper one
+            // increment 0x00010001 for a value with its top bit set, else 1, straight
+            // from one PRMT: the low half counts both values of the pair, the high
+            // half the upper one
 #pragma unroll
-              for (int b = 0; b < 4; ++b)
-                atomicAdd(c32w + prmt(lo, 0, 0x4440 + b) * C, prmt(hb, 1u, 0x5054 + (b << 8)));
-            }
-          }
-          if (PLANES) {
-            uint32_t pl[PLANES ? W : 1], nl[PLANES ? W : 1];
-#pragma unroll
-            for (int b = 0; b < (PLANES ? W : 1); ++b) {
-              uint32_t x = 0;
-#pragma unroll
-              for (int u = 0; u < 4; ++u) x |= ((wd[u] >> b) & 0x01010101u) << u;
-              pl[b] = x;
-              nl[b] = x ^ 0x0F0F0F0Fu;
-            }
-#pragma unroll
-            for (int v = 0; v < (PLANES ? NB : 1); ++v) {
-              uint32_t m = (v & 1) ? pl[0] : nl[0];
-#pragma unroll
-              for (int b = 1; b < (PLANES ? W : 1); ++b) m &= ((v >> b) & 1) ? pl[b] : nl[b];
-              acc[v] += __popc(m);
-            }
+            for (int b = 0; b < 4; ++b)
+              atomicAdd(c32w + prmt(lo, 0, 0x4440 + b) * C, prmt(hb, 1u, 0x5054 + (b << 8)));
           }
           // lanes 4i..4i+3 hold 64 consecutive symbols: one level-0 word
           const uint32_t m32 = m16 | (__shfl_down_sync(FULL, m16, 1) << 16);
@@ -197,6 +246,7 @@ __global__ void __launch_bounds__(H8_WARPS * 32) hist8_kernel(const uint8_t* __r
       for (int v = 0; v < (PLANES ? NB : 1); ++v) {
         const uint32_t tot = __reduce_add_sync(FULL, acc[v]);
         if (lane == v) row_out[v] = tot;
+        if (check && (uint32_t)v > vmax_ok && tot) vmax = 0xFFu;  // a value in [sigma, 2^W)
       }
       continue;  // the shared counters were not touched
     }
@@ -217,6 +267,7 @@ __global__ void __launch_bounds__(H8_WARPS * 32) hist8_kernel(const uint8_t* __r
   }
   if (check) {
     vmax = max(max(vmax & 0xFFu, (vmax >> 8) & 0xFFu), max((vmax >> 16) & 0xFFu, vmax >> 24));
+    if (hi_or & ~((uint32_t)(NB - 1) * 0x01010101u)) vmax = 0xFFu;
     if (vmax > vmax_ok) atomicOr(status, WVLT_STATUS_RANGE);
   }
   zero_row_drain(lane);  // the zero row must outlive the bulk stores that read it
