@@ -2771,7 +2771,10 @@ int build_device_impl(const void* text, int sym_bytes, int64_t n, int64_t sigma,
 // chunk spread over several CPU threads (one thread copies ~15 GB/s, or far
 // less when it also takes the page faults of fresh output memory; PCIe moves
 // ~55 GB/s) and overlapped with the DMA of the neighbouring chunk.
-constexpr size_t STAGE_CHUNK = (size_t)32 << 20;
+#ifndef STAGE_CHUNK_MB
+#define STAGE_CHUNK_MB 32
+#endif
+constexpr size_t STAGE_CHUNK = (size_t)STAGE_CHUNK_MB << 20;
 #ifndef STAGE_MAX_THREADS
 #define STAGE_MAX_THREADS 8u
 #endif

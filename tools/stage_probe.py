@@ -8,6 +8,12 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import workloads  # noqa: E402
+
+if len(sys.argv) > 1:  # a tools/variants/<name>.so tuning build
+    from paper_1702_07578_b200 import _lib
+
+    _lib.load_variant(Path(__file__).resolve().parents[1] / "tools" / "variants" / f"{sys.argv[1]}.so")
+    print("variant", sys.argv[1])
 from paper_1702_07578_b200.device import DeviceBuilder  # noqa: E402
 
 text_d = workloads.generate("c2")
