@@ -44,7 +44,7 @@ extern "C" {
 #define WVLT_E_RANGE (-4)      /* a symbol lies outside [0, sigma) (host-buffer entry only) */
 
 /* largest supported code width ceil(lg sigma); the histogram fold chain is 2^(w+1) int64 */
-#define WVLT_MAX_WIDTH 24
+#define WVLT_MAX_WIDTH 28
 
 /* Bit in *status set by the device build when a symbol lies outside [0, sigma). */
 #define WVLT_STATUS_RANGE 1

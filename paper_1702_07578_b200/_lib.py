@@ -19,7 +19,7 @@ KIND_WM = 1
 KINDS = {"wt": KIND_WT, "wm": KIND_WM}
 E_ARG, E_WIDTH, E_WORKSPACE, E_RANGE = -1, -2, -3, -4
 STATUS_RANGE = 1
-MAX_WIDTH = 24
+MAX_WIDTH = 28
 STAGE_MEMSET, STAGE_HIST, STAGE_TABLES, STAGE_PASS0, STAGE_SCAN0, STAGE_REORDER = 0, 1, 2, 3, 64, 60
 
 _lib = None

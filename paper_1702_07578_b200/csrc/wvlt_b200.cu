@@ -1582,10 +1582,37 @@ __global__ void __launch_bounds__(U8_THREADS + U8_TABW, U8_CTAS_PER_SM) level_pa
 // ---------------------------------------------------------------------------
 // K5: merge (gather_bits)
 // ---------------------------------------------------------------------------
+// The task holding bit `here`, forward from task t whose end bounds[t + 1] <= here.
+// Pieces are usually longer than a word and a lane's next word is a few pieces on:
+// a linear walk.  `sparse` plans (many more pieces than destination words: the 2^l
+// groups of a wide alphabet over a few thousand words, nearly all empty) first look
+// 64 pieces ahead and binary-search from there.  bounds[ntasks] > here.
+__device__ __forceinline__ int64_t advance_task(const int64_t* __restrict__ bounds, int64_t t, int64_t ntasks,
+                                                int64_t here, bool sparse, int64_t* end = nullptr) {
+  if (sparse) {
+    const int64_t far = min(t + 64, ntasks);
+    if (__ldg(bounds + far) <= here) {
+      int64_t lo = far, hi = ntasks;  // bounds[lo] <= here < bounds[hi]
+      while (hi - lo > 1) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (__ldg(bounds + mid) <= here) lo = mid;
+        else hi = mid;
+      }
+      if (end) *end = __ldg(bounds + lo + 1);
+      return lo;
+    }
+  }
+  int64_t b1;
+  do b1 = __ldg(bounds + (++t) + 1);
+  while (b1 <= here);
+  if (end) *end = b1;
+  return t;
+}
+
 // destination word wd of a gather_bits plan, walking forward from task t
 __device__ __forceinline__ uint64_t merge_word(int64_t wd, int64_t nbits, const int64_t* __restrict__ bounds,
                                                const int64_t* __restrict__ src_starts,
-                                               const uint64_t* __restrict__ src, int64_t t) {
+                                               const uint64_t* __restrict__ src, int64_t t, int64_t ntasks, bool sparse) {
   const int64_t wb = wd << 6;
   int64_t nb = nbits - wb;
   if (nb > 64) nb = 64;
@@ -1593,7 +1620,7 @@ __device__ __forceinline__ uint64_t merge_word(int64_t wd, int64_t nbits, const 
   int filled = 0;
   while (filled < nb) {
     const int64_t here = wb + filled;
-    while (__ldg(bounds + t + 1) <= here) ++t;
+    if (__ldg(bounds + t + 1) <= here) t = advance_task(bounds, t, ntasks, here, sparse);
     int64_t take = nb - filled;
     const int64_t avail = __ldg(bounds + t + 1) - here;
     if (avail < take) take = avail;
@@ -1620,7 +1647,8 @@ constexpr int MERGE_WORDS_PER_LANE = MERGE_WPL;
 __device__ __forceinline__ uint64_t merge_word_peer(int64_t wd, int64_t nbits, const int64_t* __restrict__ bounds,
                                                     const int64_t* __restrict__ starts,
                                                     const int32_t* __restrict__ ranks,
-                                                    const uint64_t* const* __restrict__ srcs, int64_t t);
+                                                    const uint64_t* const* __restrict__ srcs, int64_t t,
+                                                    int64_t ntasks, bool sparse);
 template <bool PEER>
 __device__ __forceinline__ void merge_range(uint64_t* __restrict__ dst, int64_t wlo, int64_t whi, int64_t nbits,
                                             const int64_t* __restrict__ bounds,
@@ -1632,6 +1660,7 @@ __device__ __forceinline__ void merge_range(uint64_t* __restrict__ dst, int64_t 
   // binary-searches the task of the warp's first bit, every lane walks forward
   constexpr int CH = 32 * MERGE_WORDS_PER_LANE;
   const int lane = threadIdx.x & 31;
+  const bool sparse = ntasks > 8 * (whi - wlo);  // (see advance_task)
   for (int64_t w0 = wlo + gw * CH; w0 < whi; w0 += nwarps * CH) {
     int64_t t0 = 0;
     if (lane == 0 && (w0 << 6) < nbits) {
@@ -1667,9 +1696,8 @@ __device__ __forceinline__ void merge_range(uint64_t* __restrict__ dst, int64_t 
       if (wd < whi && here < nbits) {
         if (!have || b1 <= here) {
           if (!have) b1 = __ldg(bounds + t + 1);
-          while (b1 <= here) {
-            ++t;
-            b1 = __ldg(bounds + t + 1);
+          if (b1 <= here) {
+            t = advance_task(bounds, t, ntasks, here, sparse, &b1);
           }
           b0 = __ldg(bounds + t);
           st = __ldg(src_starts + t);
@@ -1707,8 +1735,8 @@ __device__ __forceinline__ void merge_range(uint64_t* __restrict__ dst, int64_t 
         v[k] = x;
       } else if (shnb[k] < 0) {
         const int64_t tk = t0 + (int64_t)(-1 - shnb[k]);
-        v[k] = PEER ? merge_word_peer(wd, nbits, bounds, src_starts, ranks, srcs, tk)
-                    : merge_word(wd, nbits, bounds, src_starts, src, tk);
+        v[k] = PEER ? merge_word_peer(wd, nbits, bounds, src_starts, ranks, srcs, tk, ntasks, sparse)
+                    : merge_word(wd, nbits, bounds, src_starts, src, tk, ntasks, sparse);
       } else {
         v[k] = 0ull;
       }
@@ -1738,7 +1766,8 @@ __global__ void __launch_bounds__(256) merge_bits_kernel(uint64_t* __restrict__ 
 __device__ __forceinline__ uint64_t merge_word_peer(int64_t wd, int64_t nbits, const int64_t* __restrict__ bounds,
                                                     const int64_t* __restrict__ starts,
                                                     const int32_t* __restrict__ ranks,
-                                                    const uint64_t* const* __restrict__ srcs, int64_t t) {
+                                                    const uint64_t* const* __restrict__ srcs, int64_t t,
+                                                    int64_t ntasks, bool sparse) {
   const int64_t wb = wd << 6;
   int64_t nb = nbits - wb;
   if (nb > 64) nb = 64;
@@ -1746,7 +1775,7 @@ __device__ __forceinline__ uint64_t merge_word_peer(int64_t wd, int64_t nbits, c
   int filled = 0;
   while (filled < nb) {
     const int64_t here = wb + filled;
-    while (__ldg(bounds + t + 1) <= here) ++t;
+    if (__ldg(bounds + t + 1) <= here) t = advance_task(bounds, t, ntasks, here, sparse);
     int64_t take = nb - filled;
     const int64_t avail = __ldg(bounds + t + 1) - here;
     if (avail < take) take = avail;
