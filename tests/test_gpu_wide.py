@@ -44,6 +44,10 @@ def test_code_widths_above_24(kind, w):
         if kind == "wm":
             assert zeros == oz
         if extras:
+            import paper_1702_07578_b200 as wv
+
+            st = wv.build_structure(host, sigma, kind)  # the drop-in call on the host array
+            assert wv.dump_structure(st) == oracle.dump(kind, n, sigma, ow, oz)
             hist = oracle.histogram(host, sigma)
             assert np.array_equal(res.hist.cpu().numpy(), hist)
             assert np.array_equal(res.borders.cpu().numpy()[: (1 << w) - 2], oracle.borders(hist, w, kind))
