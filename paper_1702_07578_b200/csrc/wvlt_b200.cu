@@ -1609,6 +1609,9 @@ __device__ __forceinline__ int64_t advance_task(const int64_t* __restrict__ boun
   return t;
 }
 
+// many more pieces than destination words: long stretches of empty pieces
+__device__ __forceinline__ bool merge_sparse(int64_t ntasks, int64_t nwords) { return ntasks > 8 * nwords; }
+
 // destination word wd of a gather_bits plan, walking forward from task t
 __device__ __forceinline__ uint64_t merge_word(int64_t wd, int64_t nbits, const int64_t* __restrict__ bounds,
                                                const int64_t* __restrict__ src_starts,
@@ -1649,7 +1652,7 @@ __device__ __forceinline__ uint64_t merge_word_peer(int64_t wd, int64_t nbits, c
                                                     const int32_t* __restrict__ ranks,
                                                     const uint64_t* const* __restrict__ srcs, int64_t t,
                                                     int64_t ntasks, bool sparse);
-template <bool PEER>
+template <bool PEER, bool SPARSE>
 __device__ __forceinline__ void merge_range(uint64_t* __restrict__ dst, int64_t wlo, int64_t whi, int64_t nbits,
                                             const int64_t* __restrict__ bounds,
                                             const int64_t* __restrict__ src_starts, int64_t ntasks,
@@ -1660,7 +1663,7 @@ __device__ __forceinline__ void merge_range(uint64_t* __restrict__ dst, int64_t 
   // binary-searches the task of the warp's first bit, every lane walks forward
   constexpr int CH = 32 * MERGE_WORDS_PER_LANE;
   const int lane = threadIdx.x & 31;
-  const bool sparse = ntasks > 8 * (whi - wlo);  // (see advance_task)
+  constexpr bool sparse = SPARSE;  // (see advance_task; chosen per launch by merge_sparse)
   for (int64_t w0 = wlo + gw * CH; w0 < whi; w0 += nwarps * CH) {
     int64_t t0 = 0;
     if (lane == 0 && (w0 << 6) < nbits) {
@@ -1753,9 +1756,12 @@ __global__ void __launch_bounds__(256) merge_bits_kernel(uint64_t* __restrict__ 
                                                          int64_t nbits, const int64_t* __restrict__ bounds,
                                                          const int64_t* __restrict__ src_starts, int64_t ntasks,
                                                          const uint64_t* __restrict__ src) {
-  merge_range<false>(dst, wlo, whi, nbits, bounds, src_starts, ntasks, src, nullptr, nullptr,
-                     (((int64_t)blockIdx.x * blockDim.x) >> 5) + (threadIdx.x >> 5),
-                     ((int64_t)gridDim.x * blockDim.x) >> 5);
+  const int64_t gw = (((int64_t)blockIdx.x * blockDim.x) >> 5) + (threadIdx.x >> 5);
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  if (merge_sparse(ntasks, whi - wlo))
+    merge_range<false, true>(dst, wlo, whi, nbits, bounds, src_starts, ntasks, src, nullptr, nullptr, gw, nwarps);
+  else
+    merge_range<false, false>(dst, wlo, whi, nbits, bounds, src_starts, ntasks, src, nullptr, nullptr, gw, nwarps);
 }
 
 // Multi-GPU merge over peer memory: every level's owned destination words are
@@ -1806,10 +1812,15 @@ __global__ void __launch_bounds__(256) merge_peer_kernel(uint64_t* __restrict__ 
   // the same word loop as the one-source merge: every word's task first, then
   // all of a lane's source loads in flight together (peer reads over NVLink
   // have a few microseconds of latency), words that straddle pieces last
-  merge_range<true>(dst + (int64_t)l * dst_row - wlo, wlo, whi, nbits, bounds_all + bounds_off[l], starts_all + t_lo,
-                    ntasks, nullptr, ranks_all + t_lo, level_src + (int64_t)l * nranks,
-                    (((int64_t)blockIdx.x * blockDim.x) >> 5) + (threadIdx.x >> 5),
-                    ((int64_t)gridDim.x * blockDim.x) >> 5);
+  const int64_t gw = (((int64_t)blockIdx.x * blockDim.x) >> 5) + (threadIdx.x >> 5);
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  uint64_t* drow = dst + (int64_t)l * dst_row - wlo;
+  if (merge_sparse(ntasks, whi - wlo))
+    merge_range<true, true>(drow, wlo, whi, nbits, bounds_all + bounds_off[l], starts_all + t_lo, ntasks, nullptr,
+                            ranks_all + t_lo, level_src + (int64_t)l * nranks, gw, nwarps);
+  else
+    merge_range<true, false>(drow, wlo, whi, nbits, bounds_all + bounds_off[l], starts_all + t_lo, ntasks, nullptr,
+                             ranks_all + t_lo, level_src + (int64_t)l * nranks, gw, nwarps);
 }
 
 // Merge plan of the sharded build on the device (construct._merge_plan,
