@@ -87,7 +87,9 @@ int wvlt_histogram(const void* text, int sym_bytes, int64_t n, int64_t sigma, in
  * (construct.py:292-387) and their kernels hist_and_msb_bits, fold_pairs,
  * starts_identity, starts_ordered, sort_level_pass, scatter_by_prefix and
  * write_bits_from_symbols (_kernels.py:23-193).
- *   text         device, n symbols (sym_bytes = 1, 2 or 4), values must lie in [0, sigma)
+ *   text         device, n symbols (sym_bytes = 1, 2 or 4), values must lie in [0, sigma);
+ *                any address works, but only a 16-byte aligned one (32 for sigma <= 8) gets
+ *                the vector / bulk loads -- several times slower otherwise
  *   level_words  device uint64[width * ceil(n/64)], fully overwritten
  *   zeros        device int64[width] or NULL: WM zero counts Z[l] (construct.py:273-288);
  *                for kind WT the same per-level zero counts are written

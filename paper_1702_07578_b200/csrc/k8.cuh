@@ -82,10 +82,80 @@ __device__ __forceinline__ void ld256_cs(uint32_t (&r)[8], const uint32_t* p) {
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
                : "l"(p));
 }
+// the same 32 bytes from an address that is only 16-byte aligned
+__device__ __forceinline__ void ld2x128_cs(uint32_t (&r)[8], const uint32_t* p) {
+  const uint4 a = __ldcs(reinterpret_cast<const uint4*>(p)), b = __ldcs(reinterpret_cast<const uint4*>(p) + 1);
+  r[0] = a.x, r[1] = a.y, r[2] = a.z, r[3] = a.w, r[4] = b.x, r[5] = b.y, r[6] = b.z, r[7] = b.w;
+}
 // exchange the bits selected by m with the bits sh above them
 __device__ __forceinline__ uint32_t delta_swap(uint32_t x, int sh, uint32_t m) {
   const uint32_t t = ((x >> sh) ^ x) & m;
   return x ^ t ^ (t << sh);
+}
+
+// One 16384-symbol tile of the register-plane counting (widths <= H8_PLANE_W): a
+// lane takes 32 consecutive symbols per step (one 256-bit load, or two 128-bit
+// ones from a text that is only 16-byte aligned) and turns them into W bit
+// planes of 32 bits, bit 8k + u = symbol 4u + k (byte k of word u): one shift +
+// one LOP3 per word and plane.  The values are counted with one POPC per value
+// and 32 symbols; level 0 is the top plane transposed to text order by four
+// delta swaps and stored as the lane's own 32-bit half word (coalesced, no
+// shuffles).
+template <int W, bool WIDE>
+__device__ __forceinline__ void hist8_planes_tile(const uint32_t* __restrict__ t32, uint32_t* __restrict__ l0, int lane,
+                                                  int check, uint32_t (&acc)[1 << W], uint32_t& hi_or) {
+  constexpr int NB = 1 << W;
+  constexpr int NIT = K8_TILE / 32 / 32;
+  constexpr int NB2 = H8_PLANE_BATCH;
+  static_assert(NIT % NB2 == 0, "whole batches");
+  uint32_t qn[NB2][8];
+#pragma unroll
+  for (int k = 0; k < NB2; ++k) {
+    if (WIDE) ld256_cs(qn[k], t32 + 8 * (k * 32 + lane));
+    else ld2x128_cs(qn[k], t32 + 8 * (k * 32 + lane));
+  }
+#pragma unroll 1
+  for (int it0 = 0; it0 < NIT; it0 += NB2) {
+    uint32_t q[NB2][8];
+#pragma unroll
+    for (int k = 0; k < NB2; ++k)
+#pragma unroll
+      for (int u = 0; u < 8; ++u) q[k][u] = qn[k][u];
+    if (it0 + NB2 < NIT) {
+#pragma unroll
+      for (int k = 0; k < NB2; ++k) {
+        if (WIDE) ld256_cs(qn[k], t32 + 8 * ((it0 + NB2 + k) * 32 + lane));
+        else ld2x128_cs(qn[k], t32 + 8 * ((it0 + NB2 + k) * 32 + lane));
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < NB2; ++k) {
+      uint32_t pl[W], nl[W];
+      if (check) hi_or |= (q[k][0] | q[k][1] | q[k][2] | q[k][3]) | (q[k][4] | q[k][5] | q[k][6] | q[k][7]);
+#pragma unroll
+      for (int b = 0; b < W; ++b) {
+        uint32_t x = 0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          x |= (u >= b ? q[k][u] << (u - b) : q[k][u] >> (b - u)) & (0x01010101u << u);
+        pl[b] = x;
+        nl[b] = ~x;
+      }
+#pragma unroll
+      for (int v = 0; v < NB; ++v) {
+        uint32_t m = (v & 1) ? pl[0] : nl[0];
+#pragma unroll
+        for (int b = 1; b < W; ++b) m &= ((v >> b) & 1) ? pl[b] : nl[b];
+        acc[v] += __popc(m);
+      }
+      uint32_t t = pl[W - 1];  // bit (k1 k0 u2 u1 u0) -> bit (u2 u1 u0 k1 k0)
+      t = delta_swap(t, 12, 0x0000F0F0u);
+      t = delta_swap(t, 6, 0x00CC00CCu);
+      t = delta_swap(t, 3, 0x0A0A0A0Au);
+      t = delta_swap(t, 1, 0x22222222u);
+      l0[(it0 + k) * 32 + lane] = t;
+    }
+  }
 }
 
 // It also writes level 0 (the top code bit of every symbol, already in text
@@ -109,8 +179,8 @@ __global__ void __launch_bounds__(H8_WARPS * 32) hist8_kernel(const uint8_t* __r
   __syncwarp();
   uint32_t vmax = 0;
   uint32_t hi_or = 0;  // (register-plane widths) OR of every word: a bit above the code width = out of range
-  constexpr bool PLANES_K = W <= H8_PLANE_W;
-  const bool aligned32 = (((uintptr_t)text) & (PLANES_K ? 31 : 15)) == 0;  // 256-bit / 128-bit loads
+  const bool aligned = (((uintptr_t)text) & 15) == 0;           // 128-bit loads
+  const bool wide = (((uintptr_t)text) & 31) == 0;              // (register-plane widths) 256-bit loads
   const int64_t nwarps = (int64_t)gridDim.x * H8_WARPS;
   for (int64_t t = (int64_t)blockIdx.x * H8_WARPS + wid; t < ntiles; t += nwarps) {
     const int64_t first = t * K8_TILE;
@@ -123,60 +193,14 @@ __global__ void __launch_bounds__(H8_WARPS * 32) hist8_kernel(const uint8_t* __r
     uint32_t acc[PLANES ? NB : 1];
 #pragma unroll
     for (int v = 0; v < (PLANES ? NB : 1); ++v) acc[v] = 0;
-    const bool fast = cnt == K8_TILE && aligned32;
+    const bool fast = cnt == K8_TILE && aligned;
     if (PLANES && fast) {
-      // narrow alphabets: a lane takes 32 consecutive symbols per step (one 256-bit
-      // load) and turns them into W bit planes of 32 bits, bit 8k + u = symbol
-      // 4u + k (byte k of word u): one shift + one LOP3 per word and plane.  The
-      // values are counted with one POPC per value and 32 symbols; level 0 is
-      // the top plane transposed to text order by four delta swaps and stored
-      // as the lane's own 32-bit half word (coalesced, no shuffles).
+      // narrow alphabets: counted from bit planes in registers (hist8_planes_tile)
       const uint32_t* t32 = reinterpret_cast<const uint32_t*>(text + first);
       uint32_t* l0 = reinterpret_cast<uint32_t*>(level0) + (first >> 5);
-      constexpr int NIT = K8_TILE / 32 / 32;
-      constexpr int NB2 = H8_PLANE_BATCH;
-      static_assert(NIT % NB2 == 0, "whole batches");
-      uint32_t qn[NB2][8];
-#pragma unroll
-      for (int k = 0; k < NB2; ++k) ld256_cs(qn[k], t32 + 8 * (k * 32 + lane));
-#pragma unroll 1
-      for (int it0 = 0; it0 < NIT; it0 += NB2) {
-        uint32_t q[NB2][8];
-#pragma unroll
-        for (int k = 0; k < NB2; ++k)
-#pragma unroll
-          for (int u = 0; u < 8; ++u) q[k][u] = qn[k][u];
-        if (it0 + NB2 < NIT) {
-#pragma unroll
-          for (int k = 0; k < NB2; ++k) ld256_cs(qn[k], t32 + 8 * ((it0 + NB2 + k) * 32 + lane));
-        }
-#pragma unroll
-        for (int k = 0; k < NB2; ++k) {
-          uint32_t pl[PLANES ? W : 1], nl[PLANES ? W : 1];
-          if (check) hi_or |= (q[k][0] | q[k][1] | q[k][2] | q[k][3]) | (q[k][4] | q[k][5] | q[k][6] | q[k][7]);
-#pragma unroll
-          for (int b = 0; b < (PLANES ? W : 1); ++b) {
-            uint32_t x = 0;
-#pragma unroll
-            for (int u = 0; u < 8; ++u)
-              x |= (u >= b ? q[k][u] << (u - b) : q[k][u] >> (b - u)) & (0x01010101u << u);
-            pl[b] = x;
-            nl[b] = ~x;
-          }
-#pragma unroll
-          for (int v = 0; v < (PLANES ? NB : 1); ++v) {
-            uint32_t m = (v & 1) ? pl[0] : nl[0];
-#pragma unroll
-            for (int b = 1; b < (PLANES ? W : 1); ++b) m &= ((v >> b) & 1) ? pl[b] : nl[b];
-            acc[v] += __popc(m);
-          }
-          uint32_t t = pl[(PLANES ? W : 1) - 1];  // bit (k1 k0 u2 u1 u0) -> bit (u2 u1 u0 k1 k0)
-          t = delta_swap(t, 12, 0x0000F0F0u);
-          t = delta_swap(t, 6, 0x00CC00CCu);
-          t = delta_swap(t, 3, 0x0A0A0A0Au);
-          t = delta_swap(t, 1, 0x22222222u);
-          l0[(it0 + k) * 32 + lane] = t;
-        }
+      if constexpr (PLANES) {
+        if (wide) hist8_planes_tile<W, true>(t32, l0, lane, check, acc, hi_or);
+        else hist8_planes_tile<W, false>(t32, l0, lane, check, acc, hi_or);
       }
     } else if (!PLANES && fast) {
       const uint4* v4 = reinterpret_cast<const uint4*>(text + first);
