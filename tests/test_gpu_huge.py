@@ -36,6 +36,13 @@ def test_build_around_2_pow_32_symbols(sigma, kind, dt, n):
     free, _ = torch.cuda.mem_get_info()
     if free < 40 * (1 << 30):  # pragma: no cover
         pytest.skip("needs ~40 GB of device memory")
+    try:
+        import psutil
+
+        if psutil.virtual_memory().available < 48 * (1 << 30):  # pragma: no cover
+            pytest.skip("needs ~48 GB of host memory for the oracle")
+    except ImportError:  # pragma: no cover
+        pass
     tdt = getattr(torch, dt)
     g = torch.Generator(device="cuda")
     g.manual_seed(sigma + n % 1000)
